@@ -1,0 +1,306 @@
+/*
+ * oracle/direct.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct direct O(m^2)/O(m^3) convolution sums that
+ * define what the implicitly dealiased convolutions of Bowman & Roberts
+ * (arXiv 1008.1366, /root/reference/PAPER.md = "P:") must compute.  Only
+ * tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference legs may load this library.  It shares no code with the CUDA
+ * path (paper_1008_1366_b200/csrc) and includes none of its headers.
+ *
+ * Definitions:
+ *   D1 cconv1d  h_k = sum_{p=0}^{k} f_p g_{k-p},          k = 0..m-1
+ *   D2 hconv1d  h_k = sum_{p=k-m+1}^{m-1} f_p g_{k-p},    k = 0..m-1
+ *               with f_{-p} := conj(f_p) and f_0 := Re f_0 (AMB-7)
+ *   D3 tconv1d  t_k = sum_{p+q+r=k, |p|,|q|,|r|<=m-1} f_p g_q h_r
+ *   D4 cconv2d, D6 cconv3d: the 2D/3D analogues of D1
+ *   D5 hconv2d, D7 hconv3d: centered x (and y), Hermitian last axis
+ *
+ * Accuracy: every product is split exactly with TwoProd (fma) and all terms
+ * are accumulated with Neumaier compensated summation (AMB-20).
+ * Complex numbers are interleaved (re, im) doubles.  Compile with
+ * -ffp-contract=off so that the error-free transforms stay error free.
+ *
+ * Every entry point returns 0 on success, -1 if the number of multiply-adds
+ * would exceed the work cap (orc_set_work_cap, default 2^36), -2 on bad args.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct { double s, c; } acc_t;          /* Neumaier accumulator */
+
+static inline void acc_add(acc_t *a, double x) {
+  double t = a->s + x;
+  if (fabs(a->s) >= fabs(x)) a->c += (a->s - t) + x;
+  else                       a->c += (x - t) + a->s;
+  a->s = t;
+}
+static inline double acc_val(const acc_t *a) { return a->s + a->c; }
+
+/* exact product x*y = p + e, added to the accumulator */
+static inline void acc_addprod(acc_t *a, double x, double y) {
+  double p = x * y;
+  double e = fma(x, y, -p);
+  acc_add(a, p);
+  acc_add(a, e);
+}
+
+typedef struct { acc_t re, im; } cacc_t;
+
+/* (ar + i ai)(br + i bi) = (ar br - ai bi) + i (ar bi + ai br) */
+static inline void cacc_addmul(cacc_t *a, double ar, double ai, double br, double bi) {
+  acc_addprod(&a->re, ar, br);
+  acc_addprod(&a->re, -ai, bi);
+  acc_addprod(&a->im, ar, bi);
+  acc_addprod(&a->im, ai, br);
+}
+
+static double g_work_cap = 68719476736.0; /* 2^36 complex MACs */
+void orc_set_work_cap(double macs) { g_work_cap = macs; }
+static int over_cap(double macs) { return macs > g_work_cap; }
+
+/* ------------------------------------------------------------------ D1 -- */
+int orc_cconv1d(const double *f, const double *g, double *h, int64_t m, int64_t batch) {
+  if (m < 1 || batch < 1) return -2;
+  if (over_cap(0.5 * (double)m * (double)(m + 1) * (double)batch)) return -1;
+#pragma omp parallel for collapse(2) schedule(dynamic, 16)
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t k = 0; k < m; ++k) {
+      const double *F = f + 2 * b * m, *G = g + 2 * b * m;
+      cacc_t a = {{0, 0}, {0, 0}};
+      for (int64_t p = 0; p <= k; ++p)
+        cacc_addmul(&a, F[2 * p], F[2 * p + 1], G[2 * (k - p)], G[2 * (k - p) + 1]);
+      h[2 * (b * m + k)] = acc_val(&a.re);
+      h[2 * (b * m + k) + 1] = acc_val(&a.im);
+    }
+  return 0;
+}
+
+/* centered Hermitian extension of a length-m half spectrum:
+ * E[p + (m-1)] = U_p for p = -(m-1)..(m-1), U_{-p} = conj(U_p), U_0 := Re U_0 */
+static void hermitian_extend1d(const double *U, double *E, int64_t m) {
+  for (int64_t p = 0; p < m; ++p) {
+    E[2 * (m - 1 + p)] = U[2 * p];
+    E[2 * (m - 1 + p) + 1] = U[2 * p + 1];
+    E[2 * (m - 1 - p)] = U[2 * p];
+    E[2 * (m - 1 - p) + 1] = -U[2 * p + 1];
+  }
+  E[2 * (m - 1) + 1] = 0.0;
+}
+
+/* ------------------------------------------------------------------ D2 -- */
+int orc_hconv1d(const double *f, const double *g, double *h, int64_t m, int64_t batch) {
+  if (m < 1 || batch < 1) return -2;
+  if (over_cap((double)m * (double)(2 * m) * (double)batch)) return -1;
+  int64_t n = 2 * m - 1;
+  double *E = (double *)malloc(sizeof(double) * 4 * n * batch);
+  if (!E) return -2;
+  for (int64_t b = 0; b < batch; ++b) {
+    hermitian_extend1d(f + 2 * b * m, E + 4 * b * n, m);
+    hermitian_extend1d(g + 2 * b * m, E + 4 * b * n + 2 * n, m);
+  }
+#pragma omp parallel for collapse(2) schedule(dynamic, 16)
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t k = 0; k < m; ++k) {
+      const double *F = E + 4 * b * n, *G = E + 4 * b * n + 2 * n;
+      cacc_t a = {{0, 0}, {0, 0}};
+      for (int64_t p = k - m + 1; p <= m - 1; ++p) {
+        int64_t q = k - p; /* |q| <= m-1 holds for p in this range */
+        cacc_addmul(&a, F[2 * (p + m - 1)], F[2 * (p + m - 1) + 1],
+                    G[2 * (q + m - 1)], G[2 * (q + m - 1) + 1]);
+      }
+      h[2 * (b * m + k)] = acc_val(&a.re);
+      h[2 * (b * m + k) + 1] = acc_val(&a.im);
+    }
+  free(E);
+  return 0;
+}
+
+/* ------------------------------------------------------------------ D3 -- */
+/* Two-stage exact form: e_s = sum_p f_p g_{s-p} (|p|,|s-p| <= m-1), kept as a
+ * double-double (hi + lo); then t_k = sum_s e_s h_{k-s} over |k-s| <= m-1. */
+int orc_tconv1d(const double *f, const double *g, const double *hh, double *t, int64_t m, int64_t batch) {
+  if (m < 1 || batch < 1) return -2;
+  if (over_cap(((double)(4 * m) * (double)(2 * m) + (double)m * (double)(2 * m)) * (double)batch)) return -1;
+  int64_t n = 2 * m - 1, ne = 4 * m - 3;
+  double *E = (double *)malloc(sizeof(double) * 2 * n * 3 * batch);
+  double *ehi = (double *)malloc(sizeof(double) * 2 * ne * batch);
+  double *elo = (double *)malloc(sizeof(double) * 2 * ne * batch);
+  if (!E || !ehi || !elo) { free(E); free(ehi); free(elo); return -2; }
+  for (int64_t b = 0; b < batch; ++b) {
+    hermitian_extend1d(f + 2 * b * m, E + 2 * n * (3 * b + 0), m);
+    hermitian_extend1d(g + 2 * b * m, E + 2 * n * (3 * b + 1), m);
+    hermitian_extend1d(hh + 2 * b * m, E + 2 * n * (3 * b + 2), m);
+  }
+#pragma omp parallel for collapse(2) schedule(dynamic, 16)
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t si = 0; si < ne; ++si) {
+      int64_t s = si - (2 * m - 2);
+      const double *F = E + 2 * n * (3 * b), *G = E + 2 * n * (3 * b + 1);
+      int64_t plo = s - (m - 1) > -(m - 1) ? s - (m - 1) : -(m - 1);
+      int64_t phi = s + (m - 1) < (m - 1) ? s + (m - 1) : (m - 1);
+      cacc_t a = {{0, 0}, {0, 0}};
+      for (int64_t p = plo; p <= phi; ++p)
+        cacc_addmul(&a, F[2 * (p + m - 1)], F[2 * (p + m - 1) + 1],
+                    G[2 * (s - p + m - 1)], G[2 * (s - p + m - 1) + 1]);
+      double hr = acc_val(&a.re), hi = acc_val(&a.im);
+      ehi[2 * (b * ne + si)] = hr;
+      ehi[2 * (b * ne + si) + 1] = hi;
+      elo[2 * (b * ne + si)] = (a.re.s - hr) + a.re.c;
+      elo[2 * (b * ne + si) + 1] = (a.im.s - hi) + a.im.c;
+    }
+#pragma omp parallel for collapse(2) schedule(dynamic, 16)
+  for (int64_t b = 0; b < batch; ++b)
+    for (int64_t k = 0; k < m; ++k) {
+      const double *H = E + 2 * n * (3 * b + 2);
+      cacc_t a = {{0, 0}, {0, 0}};
+      for (int64_t s = k - (m - 1); s <= k + (m - 1); ++s) {
+        if (s < -(2 * m - 2) || s > 2 * m - 2) continue;
+        int64_t si = s + 2 * m - 2, r = k - s;
+        double hr = H[2 * (r + m - 1)], hi = H[2 * (r + m - 1) + 1];
+        cacc_addmul(&a, ehi[2 * (b * ne + si)], ehi[2 * (b * ne + si) + 1], hr, hi);
+        cacc_addmul(&a, elo[2 * (b * ne + si)], elo[2 * (b * ne + si) + 1], hr, hi);
+      }
+      t[2 * (b * m + k)] = acc_val(&a.re);
+      t[2 * (b * m + k) + 1] = acc_val(&a.im);
+    }
+  free(E); free(ehi); free(elo);
+  return 0;
+}
+
+/* brute-force triple sum (small m only), the literal definition P:963-964.
+ * Accumulated in x86 long double (64-bit mantissa): for m <= 32 the at most
+ * (2m-1)^2 terms leave an error far below double rounding. */
+int orc_tconv1d_brute(const double *f, const double *g, const double *hh, double *t, int64_t m) {
+  if (m < 1) return -2;
+  if (over_cap((double)m * (double)(2 * m) * (double)(2 * m))) return -1;
+  int64_t n = 2 * m - 1;
+  double *E = (double *)malloc(sizeof(double) * 6 * n);
+  if (!E) return -2;
+  hermitian_extend1d(f, E, m);
+  hermitian_extend1d(g, E + 2 * n, m);
+  hermitian_extend1d(hh, E + 4 * n, m);
+  for (int64_t k = 0; k < m; ++k) {
+    long double sr = 0.0L, si = 0.0L;
+    for (int64_t p = -(m - 1); p <= m - 1; ++p)
+      for (int64_t q = -(m - 1); q <= m - 1; ++q) {
+        int64_t r = k - p - q;
+        if (r < -(m - 1) || r > m - 1) continue;
+        const double *F = E + 2 * (p + m - 1), *G = E + 2 * n + 2 * (q + m - 1), *H = E + 4 * n + 2 * (r + m - 1);
+        long double ar = (long double)F[0] * G[0] - (long double)F[1] * G[1];
+        long double ai = (long double)F[0] * G[1] + (long double)F[1] * G[0];
+        sr += ar * H[0] - ai * H[1];
+        si += ar * H[1] + ai * H[0];
+      }
+    t[2 * k] = (double)sr;
+    t[2 * k + 1] = (double)si;
+  }
+  free(E);
+  return 0;
+}
+
+/* ------------------------------------------------------------ D4 / D6 -- */
+/* Complex d-dimensional (d = 2, 3) truncated linear convolution at a list of
+ * output points.  Arrays are row-major (n0, n1, n2) with n2 = 1 for 2D.
+ * out_idx holds nout linear indices i*(n1*n2) + j*n2 + l. */
+int orc_cconv3d_at(const double *f, const double *g, int64_t n0, int64_t n1, int64_t n2,
+                   const int64_t *out_idx, int64_t nout, double *out) {
+  if (n0 < 1 || n1 < 1 || n2 < 1 || nout < 0) return -2;
+  double per = (double)n0 * (double)n1 * (double)n2; /* upper bound per point */
+  if (over_cap(per * (double)nout)) return -1;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t o = 0; o < nout; ++o) {
+    int64_t lin = out_idx[o];
+    int64_t i = lin / (n1 * n2), j = (lin / n2) % n1, l = lin % n2;
+    cacc_t a = {{0, 0}, {0, 0}};
+    for (int64_t p = 0; p <= i; ++p)
+      for (int64_t q = 0; q <= j; ++q)
+        for (int64_t r = 0; r <= l; ++r) {
+          const double *F = f + 2 * ((p * n1 + q) * n2 + r);
+          const double *G = g + 2 * (((i - p) * n1 + (j - q)) * n2 + (l - r));
+          cacc_addmul(&a, F[0], F[1], G[0], G[1]);
+        }
+    out[2 * o] = acc_val(&a.re);
+    out[2 * o + 1] = acc_val(&a.im);
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------ D5 / D7 -- */
+/* Centered-Hermitian 3D (2D when my == 1 is passed as a centered length-1 axis):
+ * storage A[i][j][l], i in [0, 2mx-1), j in [0, 2my-1), l in [0, mz),
+ * A[i][j][l] = U_{i-(mx-1), j-(my-1), l}.  Extension U_{kx,ky,-kz} :=
+ * conj(U_{-kx,-ky,kz}); the kz = 0 plane is projected
+ * U_{kx,ky,0} := (U_{kx,ky,0} + conj(U_{-kx,-ky,0}))/2  (AMB-7).
+ * The full centered array X[(2mx-1)][(2my-1)][(2mz-1)] is built first, then
+ * h_{k} = sum_p X_p X'_{k-p} over the centered box, at the requested output
+ * points (linear indices into the (2mx-1, 2my-1, mz) storage). */
+static void hermitian_extend3d(const double *A, double *X, int64_t mx, int64_t my, int64_t mz) {
+  int64_t nx = 2 * mx - 1, ny = 2 * my - 1, nz = 2 * mz - 1;
+  for (int64_t i = 0; i < nx; ++i)
+    for (int64_t j = 0; j < ny; ++j)
+      for (int64_t l = 0; l < mz; ++l) {
+        const double *a = A + 2 * ((i * ny + j) * mz + l);
+        const double *b = A + 2 * (((nx - 1 - i) * ny + (ny - 1 - j)) * mz + l); /* mirror (-kx,-ky) */
+        double *x = X + 2 * ((i * ny + j) * nz + (mz - 1 + l));
+        double *xm = X + 2 * (((nx - 1 - i) * ny + (ny - 1 - j)) * nz + (mz - 1 - l));
+        if (l == 0) {
+          x[0] = 0.5 * (a[0] + b[0]);
+          x[1] = 0.5 * (a[1] - b[1]);
+        } else {
+          x[0] = a[0];
+          x[1] = a[1];
+          xm[0] = a[0];
+          xm[1] = -a[1];
+        }
+      }
+}
+
+int orc_hconv3d_at(const double *f, const double *g, int64_t mx, int64_t my, int64_t mz,
+                   const int64_t *out_idx, int64_t nout, double *out) {
+  if (mx < 1 || my < 1 || mz < 1 || nout < 0) return -2;
+  int64_t nx = 2 * mx - 1, ny = 2 * my - 1, nz = 2 * mz - 1;
+  if (over_cap((double)nx * (double)ny * (double)nz * (double)nout)) return -1;
+  double *F = (double *)malloc(sizeof(double) * 2 * nx * ny * nz);
+  double *G = (double *)malloc(sizeof(double) * 2 * nx * ny * nz);
+  if (!F || !G) { free(F); free(G); return -2; }
+  hermitian_extend3d(f, F, mx, my, mz);
+  hermitian_extend3d(g, G, mx, my, mz);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t o = 0; o < nout; ++o) {
+    int64_t lin = out_idx[o];
+    int64_t i = lin / (ny * mz), j = (lin / mz) % ny, l = lin % mz;
+    int64_t kx = i - (mx - 1), ky = j - (my - 1), kz = l;
+    cacc_t a = {{0, 0}, {0, 0}};
+    for (int64_t px = -(mx - 1); px <= mx - 1; ++px) {
+      int64_t qx = kx - px;
+      if (qx < -(mx - 1) || qx > mx - 1) continue;
+      for (int64_t py = -(my - 1); py <= my - 1; ++py) {
+        int64_t qy = ky - py;
+        if (qy < -(my - 1) || qy > my - 1) continue;
+        for (int64_t pz = -(mz - 1); pz <= mz - 1; ++pz) {
+          int64_t qz = kz - pz;
+          if (qz < -(mz - 1) || qz > mz - 1) continue;
+          const double *x = F + 2 * (((px + mx - 1) * ny + (py + my - 1)) * nz + (pz + mz - 1));
+          const double *y = G + 2 * (((qx + mx - 1) * ny + (qy + my - 1)) * nz + (qz + mz - 1));
+          cacc_addmul(&a, x[0], x[1], y[0], y[1]);
+        }
+      }
+    }
+    out[2 * o] = acc_val(&a.re);
+    out[2 * o + 1] = acc_val(&a.im);
+  }
+  free(F); free(G);
+  return 0;
+}
+
+/* 2D centered Hermitian (D5): storage (2mx-1, my); it is the my-axis-Hermitian
+ * special case of the above with a centered y axis of length 1 removed.
+ * Extension U_{kx,-ky} := conj(U_{-kx,ky}); ky = 0 line projected. */
+int orc_hconv2d_at(const double *f, const double *g, int64_t mx, int64_t my,
+                   const int64_t *out_idx, int64_t nout, double *out) {
+  /* (2mx-1, my) == (2mx-1, 2*1-1, my): reuse the 3D routine with my_c = 1 */
+  return orc_hconv3d_at(f, g, mx, 1, my, out_idx, nout, out);
+}
