@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the implicitly dealiased convolution hot path on B200.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` prints ONE
+JSON line on rank 0.  Default workload = BASELINE.json configs[1]: the 1D
+centered Hermitian convolution (hconv1d) and the 1D centered Hermitian
+ternary convolution (tconv1d) at m = 4096, B = 4096 rows each, complex128.
+One step = one hconv1d call over its batch + one tconv1d call over its
+batch (every row of the §8(a) 1D path: twiddle split, backward FFTs,
+products, forward FFTs, recombination), inputs resident in HBM.  The arrays
+(0.5-0.75 GB per call) exceed the 126 MB L2 and are restored from pristine
+copies before every step (the call is in place), which also flushes L2.
+
+Multi-GPU: the rows are independent problems, so every rank runs its own
+batch (different seeded items) with no collective on the data path;
+``scaling`` = "weak", value = all ranks' convolutions / max-over-ranks time.
+
+``--impl reference`` times the oracle (oracle/, plain C direct sums, the
+CPU reference of this tier) on the host cores on a bounded sample of the same
+workload, and prints the same JSON line with ``"impl": "reference"``.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synthgen  # noqa: E402  (seeded inputs; no method arithmetic)
+
+METRIC = "dealiased convolutions/sec (fp64) and achieved HBM GB/s vs B200 peak"
+W = 16  # bytes per complex128 word
+
+
+def peaks():
+    """Roofline denominators: HBM from MEASURED_PEAKS.json (driver-written),
+    fp64 from the unit count x max clock."""
+    hbm = 6548.8
+    src = "MEASURED_PEAKS.json"
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            hbm = float(json.load(fh)["hbm_gbs"])
+    except Exception:
+        src = "fallback 6650 (B200_PROFILING.md)"
+        hbm = 6650.0
+    # 148 SMs x 64 fp64 FMA lanes x 2 flop x 1.965 GHz (measured DFMA loop: 34.2 TF/s, profiles/r01_peaks.txt)
+    fp64 = 148 * 64 * 2 * 1.965e9 / 1e12
+    return {"hbm_gbs": hbm, "hbm_src": src, "fp64_tflops": fp64}
+
+
+# --------------------------------------------------------------- workloads --
+
+def flops_rfft(n):      # 2.5 n log2 n per real transform
+    return 2.5 * n * np.log2(n) if n > 1 else 0.0
+
+
+def flops_cfft(n):      # 5 n log2 n per complex transform
+    return 5.0 * n * np.log2(n) if n > 1 else 0.0
+
+
+WORKLOADS = {
+    # name: dict(kind, m, batch, arrays, bytes per conv, flops per conv)
+    "c2": dict(desc="configs[1]: hconv1d m=4096 B=4096 + tconv1d m=4096 B=4096", parts=[
+        dict(kind="hconv1d", m=4096, batch=4096, narr=2),
+        dict(kind="tconv1d", m=4096, batch=4096, narr=3)]),
+    "c1": dict(desc="configs[0]: cconv1d m=1024 B=32768", parts=[
+        dict(kind="cconv1d", m=1024, batch=32768, narr=2)]),
+}
+
+
+def part_model(p):
+    """Algorithmic HBM bytes and convention flops per convolution."""
+    m, kind = p["m"], p["kind"]
+    if kind == "cconv1d":
+        return 3 * W * m, 6 * flops_cfft(m)                 # 6 complex FFTs of size m
+    if kind == "hconv1d":
+        return 3 * W * m, 9 * flops_rfft(m)                 # 9 real FFTs of size m
+    if kind == "tconv1d":
+        return 4 * W * m, 8 * flops_rfft(2 * m)             # 8 real FFTs of size 2m
+    raise ValueError(kind)
+
+
+# -------------------------------------------------------------- GPU clocks --
+
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 3 + i and r[3 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- helpers --
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_inputs(idc, torch, p, rank, dev):
+    """Seeded device inputs for one part; item ids offset by rank (weak scaling)."""
+    m, B, narr = p["m"], p["batch"], p["narr"]
+    arrs = []
+    for role in range(narr):
+        a = torch.empty((B, m), dtype=torch.complex128, device=dev)
+        for b in range(B):
+            idc.fill_uniform(a[b], synthgen.array_id(role, rank * B + b), synthgen.SEED)
+        if p["kind"] != "cconv1d":
+            a[:, 0] = a[:, 0].real.to(torch.complex128)   # Im U_0 := 0 (config 2)
+        arrs.append(a)
+    return arrs
+
+
+def call(idc, p, arrs):
+    fn = {"cconv1d": idc.cconv1d, "hconv1d": idc.hconv1d, "tconv1d": idc.tconv1d}[p["kind"]]
+    return fn(*arrs)
+
+
+# -------------------------------------------------------------- our arm ----
+
+def run_ours(args):
+    import torch
+    import torch.distributed as tdist
+    from paper_1008_1366_b200 import idconv as idc
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        tdist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    wl = WORKLOADS[args.workload]
+    parts = wl["parts"]
+
+    pristine = [make_inputs(idc, torch, p, rank, dev) for p in parts]
+    work = [[torch.empty_like(a) for a in arrs] for arrs in pristine]
+    torch.cuda.synchronize()
+
+    def restore():
+        for src, dst in zip(pristine, work):
+            for s, d in zip(src, dst):
+                d.copy_(s)
+
+    for _ in range(args.warmup):
+        restore()
+        for p, arrs in zip(parts, work):
+            call(idc, p, arrs)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream(dev)
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in parts]
+           for _ in range(args.steps)]
+    if ws > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    launches = 0
+    with ClockSampler(local) as clk:
+        t_wall0 = time.perf_counter()
+        for k in range(args.steps):
+            restore()
+            for j, (p, arrs) in enumerate(zip(parts, work)):
+                evs[k][j][0].record(stream)
+                call(idc, p, arrs)
+                evs[k][j][1].record(stream)
+                launches += 1
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    if ws > 1:
+        tdist.barrier()
+    part_ms = [sum(evs[k][j][0].elapsed_time(evs[k][j][1]) for k in range(args.steps)) for j in range(len(parts))]
+    total_ms = sum(part_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    total_ms_max = float(t.item())
+    convs_per_step = sum(p["batch"] for p in parts) * ws
+    value = convs_per_step * args.steps / (total_ms_max / 1e3)
+
+    # per-part model and roofline of the dominant kernel
+    pk = peaks()
+    part_info = []
+    for p, ms in zip(parts, part_ms):
+        b, fl = part_model(p)
+        sec = ms / 1e3 / args.steps
+        t_b = b * p["batch"] / (pk["hbm_gbs"] * 1e9)
+        t_f = fl * p["batch"] / (pk["fp64_tflops"] * 1e12)
+        part_info.append(dict(kind=p["kind"], m=p["m"], batch=p["batch"], ms_per_call=sec * 1e3,
+                              conv_per_s=p["batch"] / sec, hbm_gbs_alg=b * p["batch"] / sec / 1e9,
+                              fp64_tflops_alg=fl * p["batch"] / sec / 1e12, t_roof_ms=max(t_b, t_f) * 1e3,
+                              roofline_frac=max(t_b, t_f) / sec, bound="hbm" if t_b >= t_f else "alu"))
+    dom = max(range(len(parts)), key=lambda j: part_ms[j])
+    d = part_info[dom]
+    if d["bound"] == "hbm":
+        roof = {"bound": "hbm", "achieved": d["hbm_gbs_alg"], "peak": pk["hbm_gbs"], "unit": "GB/s"}
+    else:
+        roof = {"bound": "alu", "achieved": d["fp64_tflops_alg"], "peak": pk["fp64_tflops"], "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["kernel"] = f"k_{d['kind'][:5]}_rows<{d['m']}>"
+    roof["hbm_frac"] = d["hbm_gbs_alg"] / pk["hbm_gbs"]
+    roof["traffic"] = load_traffic(d["kind"], d["m"])
+    roof["peak_src"] = pk["hbm_src"] if roof["bound"] == "hbm" else \
+        "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md); measured DFMA loop 34.2"
+
+    # ---------------------------------------------------------- e2e arm --
+    e2e = run_e2e(args, idc, torch, parts, pristine, dev, ws)
+
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "conv/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl["desc"], "parallelism": f"replicas{ws}",
+                       "l2": "inputs > L2 (0.5-0.75 GB per call), restored from pristine copies before each step",
+                       "seed": synthgen.SEED},
+            "parts": part_info, "roofline": roof, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "wall_s_timed_loop": t_wall,
+        }
+        if not args.no_cpu_baseline and ws == 1:
+            out["cpu_baseline"] = cpu_baseline(args, parts)
+        elif ws > 1:
+            out["cpu_baseline"] = None
+    if ws > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+    return out
+
+
+def load_traffic(kind, m):
+    """dram bytes per launch from the committed ncu --set full capture, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(f"{kind}:{m}")
+    except Exception:
+        return None
+
+
+def run_e2e(args, idc, torch, parts, pristine, dev, ws):
+    """Same metric through the public API with HOST (pinned) buffers: the
+    H2D copy of every input and the D2H copy of the result are inside the
+    timed region of every step."""
+    host = [[a.cpu().pin_memory() for a in arrs] for arrs in pristine]
+    host_f0 = [arrs[0].clone() for arrs in host]
+    stream = torch.cuda.current_stream(dev)
+    steps = max(1, min(args.steps, args.e2e_steps))
+    bi = sum(a.numel() * 16 for arrs in host for a in arrs)
+    bo = sum(arrs[0].numel() * 16 for arrs in host)
+    # warm-up once
+    for p, arrs in zip(parts, host):
+        call(idc, p, arrs)
+    torch.cuda.synchronize()
+    ms = 0.0
+    for _ in range(steps):
+        for arrs, f0 in zip(host, host_f0):
+            arrs[0].copy_(f0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for p, arrs in zip(parts, host):
+            call(idc, p, arrs)  # H2D inputs, kernel, D2H result into the pinned f
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        import torch.distributed as tdist
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    convs = sum(p["batch"] for p in parts) * ws * steps
+    return {"value": convs / (float(t.item()) / 1e3), "unit": "conv/s", "h2d_bytes_per_step": bi,
+            "d2h_bytes_per_step": bo, "steps": steps}
+
+
+# ----------------------------------------------------------- oracle (CPU) --
+
+def oracle_sample(parts, budget_s):
+    """Time the oracle (direct sums) on a bounded sample of the workload's rows.
+    Returns (conv/s over the sample, description, threads)."""
+    import oracle
+    from oracle import direct
+    fns = {"cconv1d": direct.cconv1d, "hconv1d": direct.hconv1d, "tconv1d": direct.tconv1d}
+    # calibrate on one row of each part, then size the sample to the budget
+    per_row = []
+    for p in parts:
+        arrs = [np.stack([synthgen.uniform_complex(p["m"], synthgen.array_id(r, 0))]) for r in range(p["narr"])]
+        t0 = time.perf_counter()
+        fns[p["kind"]](*arrs)
+        per_row.append(time.perf_counter() - t0)
+    share = budget_s / len(parts)
+    convs, secs, desc = 0, 0.0, []
+    for p, pr in zip(parts, per_row):
+        n = int(max(1, min(p["batch"], share / max(pr, 1e-6))))
+        arrs = [np.stack([synthgen.uniform_complex(p["m"], synthgen.array_id(r, b)) for b in range(n)])
+                for r in range(p["narr"])]
+        t0 = time.perf_counter()
+        fns[p["kind"]](*arrs)
+        secs += time.perf_counter() - t0
+        convs += n
+        desc.append(f"{n} of {p['batch']} {p['kind']} rows (m={p['m']})")
+    # the step's mix: time per step = sum over parts of batch * per-row time
+    return convs, secs, "; ".join(desc)
+
+
+def cpu_baseline(args, parts):
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    convs, secs, desc = oracle_sample(parts, args.cpu_budget)
+    return {"value": convs / secs, "unit": "conv/s", "cores": threads, "kind": "oracle",
+            "sample": desc + " -- oracle direct sums (TwoProd+Neumaier, OpenMP), oracle/direct.c"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    wl = WORKLOADS[args.workload]
+    parts = wl["parts"]
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    budget = max(2.0, args.cpu_budget / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        oracle_sample(parts, budget)
+    convs, secs, desc = 0, 0.0, ""
+    for _ in range(args.steps):
+        c, s, desc = oracle_sample(parts, budget)
+        convs += c
+        secs += s
+    value = convs / secs
+    return {"metric": METRIC, "value": value, "unit": "conv/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": wl["desc"], "parallelism": "host cores", "seed": synthgen.SEED},
+            "cpu_baseline": {"value": value, "unit": "conv/s", "cores": threads, "kind": "oracle",
+                             "sample": desc + " per step"},
+            "e2e": {"value": value, "unit": "conv/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="idconv", choices=["idconv", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle CPU work")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "idconv":
+        print("warning: the contract asks for >= 3 warm-up steps", file=sys.stderr)
+    out = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

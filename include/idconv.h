@@ -1,0 +1,171 @@
+/*
+ * idconv.h -- C ABI of the B200-native implicitly dealiased convolutions
+ * (Bowman & Roberts, "Efficient Dealiased Convolutions without Padding",
+ * arXiv 1008.1366; citations "P:<line>" refer to /root/reference/PAPER.md,
+ * "S:<line>" to SPEC.md, "AMB-n" to the readings in DESIGN.md).
+ *
+ * Library: paper_1008_1366_b200/libidconv.so (sm_100a).  No torch types cross
+ * this boundary: plain pointers, sizes and an opaque CUDA stream.
+ *
+ * Conventions shared by every call
+ * --------------------------------
+ *  - Complex numbers are idc_c128 = {double re, im} (layout-identical to
+ *    double2 / cuDoubleComplex / a torch.complex128 element).  All
+ *    arithmetic is IEEE fp64 (AMB-14); no tensor cores, no fp32.
+ *  - f, g, h, work are DEVICE pointers (cudaMalloc / torch CUDA storage) on
+ *    the current device, 16-byte aligned, row-major, innermost dimension unit
+ *    stride, no row padding; batch items are contiguous (distance = one
+ *    array).
+ *  - Semantics: f <- the dealiased convolution, IN PLACE (the paper's "Return
+ *    f", P:346/373/643/1078).  g and h are used as scratch and their contents
+ *    are UNSPECIFIED on return (the paper reuses g, P:358-364, P:1069-1071;
+ *    AMB-18).  The caller owns every buffer.
+ *  - work: caller-owned device workspace of at least idc_workspace_bytes()
+ *    bytes, never overlapping f/g/h, contents undefined on entry and exit
+ *    (the paper's "work memory need not be contiguous with the input data",
+ *    P:19-20).  work may be NULL when the query returns 0.
+ *  - stream: a cudaStream_t (NULL = legacy default stream).  Every call is
+ *    asynchronous and stream-ordered; it never synchronises the host and never
+ *    allocates device memory on the call path except the one-time, mutex-
+ *    protected twiddle/plan upload per (kind, size, device).
+ *  - Errors are returned synchronously; no exception crosses the ABI.
+ *    IDC_ERR_INVALID: null/misaligned pointer, zero size or batch, aliasing
+ *    between f/g/h/work.  IDC_ERR_UNSUPPORTED: a size outside the supported
+ *    set (below).  IDC_ERR_WORKSPACE: work_bytes too small.  IDC_ERR_CUDA: a
+ *    launch failed (asynchronous faults surface at the next synchronisation).
+ *  - Supported sizes (AMB-16): every m (per axis) is
+ *    a power of two with 1 <= m <= 8192.  (The paper documents only even m
+ *    for the Hermitian case; m = 1 is the degenerate DC-only case
+ *    and is computed exactly.)
+ */
+#ifndef IDCONV_H
+#define IDCONV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define IDC_API __attribute__((visibility("default")))
+#else
+#define IDC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct { double re, im; } idc_c128;
+typedef void* idc_stream; /* cudaStream_t */
+
+typedef enum {
+  IDC_OK = 0,
+  IDC_ERR_INVALID = 1,
+  IDC_ERR_UNSUPPORTED = 2,
+  IDC_ERR_WORKSPACE = 3,
+  IDC_ERR_CUDA = 4,
+  IDC_ERR_NCCL = 5
+} idc_status;
+
+typedef enum {
+  IDC_CCONV1D = 0,
+  IDC_HCONV1D = 1,
+  IDC_TCONV1D = 2,
+  IDC_CCONV2D = 3,
+  IDC_HCONV2D = 4,
+  IDC_CCONV3D = 5,
+  IDC_HCONV3D = 6
+} idc_kind;
+
+/* Human-readable name of a status code (static storage). */
+IDC_API const char* idc_status_string(idc_status s);
+
+/* Library version string, e.g. "idconv 0.1 sm_100a". */
+IDC_API const char* idc_version(void);
+
+/* Bytes of device workspace `work` the call of kind k needs for the given
+ * sizes (unused sizes are ignored; pass 1).  1D: m0 = m.  2D: (m0, m1) =
+ * (mx, my).  3D: (m0, m1, m2) = (mx, my, mz).  Returns 0 for unsupported
+ * sizes (the call itself then reports IDC_ERR_UNSUPPORTED). */
+IDC_API size_t idc_workspace_bytes(idc_kind k, size_t m0, size_t m1, size_t m2, size_t batch);
+
+/* ---- 1D -------------------------------------------------------------- */
+
+/* cconv1d: implicitly dealiased complex convolution (Function cconv,
+ * P:352-378; Eqs. cconv1backward/cconv1forward).
+ * f, g: batch x m complex.  On return
+ *   f[b][k] = sum_{p=0}^{k} f[b][p] g[b][k-p],   k = 0..m-1
+ * computed as two residue streams (unshifted, and shifted by zeta_{2m}^k) of
+ * size-m FFTs, pointwise products, inverse FFTs, recombination /(2m). */
+IDC_API idc_status idc_cconv1d(idc_c128* f, idc_c128* g, size_t m, size_t batch,
+                       void* work, size_t work_bytes, idc_stream stream);
+
+/* hconv1d: implicitly dealiased centered Hermitian convolution (2/3 rule;
+ * Function conv; Eqs. fft0backwardA + Hermitian w_{k,r} +
+ * fft0forwardB).  f, g: batch x m complex holding
+ * k = 0..m-1 of a Hermitian spectrum (f_{-k} = conj f_k implied; Im f_0 is
+ * discarded, AMB-7).  On return
+ *   f[b][k] = sum_{p=k-m+1}^{m-1} f_p g_{k-p},   k = 0..m-1
+ * computed with N = 3m as three residue streams r in {-1,0,1}. */
+IDC_API idc_status idc_hconv1d(idc_c128* f, idc_c128* g, size_t m, size_t batch,
+                       void* work, size_t work_bytes, idc_stream stream);
+
+/* tconv1d: implicitly dealiased centered Hermitian TERNARY convolution
+ * (Function tconv), N = 4m.  f, g, h as for hconv1d.  On return
+ *   f[b][k] = sum_{p+q+r=k, |p|,|q|,|r|<=m-1} f_p g_q h_r,  k = 0..m-1
+ * g and h are left unspecified. */
+IDC_API idc_status idc_tconv1d(idc_c128* f, idc_c128* g, idc_c128* h, size_t m, size_t batch,
+                       void* work, size_t work_bytes, idc_stream stream);
+
+/* ---- 2D -------------------------------------------------------------- */
+
+/* cconv2d: Function cconv2.  f, g: batch x mx x my (y unit
+ * stride).  f[b][i][j] <- sum_{p<=i, q<=j} f[b][p][q] g[b][i-p][j-q]. */
+IDC_API idc_status idc_cconv2d(idc_c128* f, idc_c128* g, size_t mx, size_t my, size_t batch,
+                       void* work, size_t work_bytes, idc_stream stream);
+
+/* hconv2d: Function conv2.  f, g: (2mx-1) x my, row i holds
+ * kx = i-(mx-1), column j holds ky = j >= 0; U_{kx,-ky} = conj U_{-kx,ky}
+ * implied; the ky = 0 line is used through its Hermitian projection (AMB-7).
+ * f <- the centered Hermitian convolution on the same index set. */
+IDC_API idc_status idc_hconv2d(idc_c128* f, idc_c128* g, size_t mx, size_t my,
+                       void* work, size_t work_bytes, idc_stream stream);
+
+/* ---- 3D -------------------------------------------------------------- */
+
+/* cconv3d: Function cconv3.  f, g: mx x my x mz. */
+IDC_API idc_status idc_cconv3d(idc_c128* f, idc_c128* g, size_t mx, size_t my, size_t mz,
+                       void* work, size_t work_bytes, idc_stream stream);
+
+/* hconv3d: centered Hermitian 3D "in an analogous manner" (P:891-897,
+ * AMB-9).  f, g: (2mx-1) x (2my-1) x mz, kx, ky centered, kz >= 0. */
+IDC_API idc_status idc_hconv3d(idc_c128* f, idc_c128* g, size_t mx, size_t my, size_t mz,
+                       void* work, size_t work_bytes, idc_stream stream);
+
+/* ---- distributed 3D (one process per GPU, NCCL over NVLink) ------------ */
+
+/* Create a communicator from a 128-byte ncclUniqueId that the caller has
+ * broadcast (e.g. with torch.distributed).  *comm receives an opaque handle. */
+IDC_API idc_status idc_comm_init(void** comm, int nranks, int rank, const void* nccl_unique_id);
+IDC_API idc_status idc_comm_destroy(void* comm);
+/* Writes a fresh 128-byte ncclUniqueId into id_out (rank 0 calls this). */
+IDC_API idc_status idc_comm_unique_id(void* id_out);
+
+IDC_API size_t idc_dist_workspace_bytes(idc_kind k, size_t mx, size_t my, size_t mz, int nranks);
+
+/* f, g hold this rank's x-slab [rank*mx/P, (rank+1)*mx/P) of the global
+ * mx x my x mz arrays (complex) -- result in place, same layout. */
+IDC_API idc_status idc_cconv3d_dist(void* comm, idc_c128* f, idc_c128* g, size_t mx, size_t my, size_t mz,
+                            void* work, size_t work_bytes, idc_stream stream);
+
+/* ---- synthetic inputs (not part of the method) -------------------------- */
+
+/* Fill n complex values with the counter-based splitmix64 generator of
+ * synthgen: value(i) = U[-1,1) from
+ * sm(sm(seed ^ sm(array_id)) + 2*(start+i) + part).  Device pointer. */
+IDC_API idc_status idc_fill_uniform(idc_c128* out, size_t n, uint64_t seed, uint64_t array_id,
+                            uint64_t start, idc_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IDCONV_H */

@@ -1,0 +1,28 @@
+// kernels.cuh -- launchers of the fused hot-path kernels (host side).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+
+namespace idc {
+
+// Bytes of global stash the row kernels need for rows of length m (0 when the
+// stash fits in shared memory).
+size_t cconv_rows_work_bytes(int m);
+size_t hconv_rows_work_bytes(int m);
+size_t tconv_rows_work_bytes(int m);
+
+// K2: Function cconv on `nrows` independent row pairs
+// (f + r*ldf, g + r*ldg), rows of m complex, result in f.
+cudaError_t launch_cconv_rows(double2* f, double2* g, int m, long nrows, double2* work, cudaStream_t s);
+
+// K3: centered Hermitian conv (P:529-554 / Function conv) on rows.
+cudaError_t launch_hconv_rows(double2* f, double2* g, int m, long nrows, double2* work, cudaStream_t s);
+
+// K4: centered Hermitian ternary conv (Function tconv) on rows.
+cudaError_t launch_tconv_rows(double2* f, double2* g, double2* h, int m, long nrows, double2* work,
+                              cudaStream_t s);
+
+// Number of SMs of the current device (cached).
+int num_sms();
+
+}  // namespace idc

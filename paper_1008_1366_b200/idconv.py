@@ -1,0 +1,224 @@
+"""Thin ctypes binding of include/idconv.h (argument marshalling only).
+
+Every step of the convolution runs in libidconv.so (hand-written CUDA for
+sm_100a).  PyTorch supplies device memory and the current CUDA stream; there
+is no CPU fallback: if the library or a GPU is missing the calls raise.
+
+All functions follow the C ABI: the result overwrites ``f`` in place (the
+paper's "Return f"), ``g`` / ``h`` are scratch and unspecified afterwards.
+Inputs must be contiguous ``torch.complex128`` tensors.  CUDA tensors are
+processed where they live.  CPU tensors are accepted too (the end-to-end
+path): they are copied to the current device, convolved, and the result is
+copied back into ``f`` -- pinned memory makes those copies asynchronous.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libidconv.so")
+
+OK, ERR_INVALID, ERR_UNSUPPORTED, ERR_WORKSPACE, ERR_CUDA, ERR_NCCL = range(6)
+CCONV1D, HCONV1D, TCONV1D, CCONV2D, HCONV2D, CCONV3D, HCONV3D = range(7)
+
+# name -> (argtypes, restype)
+_P, _S, _I, _U64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint64
+SIGNATURES = {
+    "idc_status_string": ([_I], ctypes.c_char_p),
+    "idc_version": ([], ctypes.c_char_p),
+    "idc_workspace_bytes": ([_I, _S, _S, _S, _S], _S),
+    "idc_cconv1d": ([_P, _P, _S, _S, _P, _S, _P], _I),
+    "idc_hconv1d": ([_P, _P, _S, _S, _P, _S, _P], _I),
+    "idc_tconv1d": ([_P, _P, _P, _S, _S, _P, _S, _P], _I),
+    "idc_cconv2d": ([_P, _P, _S, _S, _S, _P, _S, _P], _I),
+    "idc_hconv2d": ([_P, _P, _S, _S, _P, _S, _P], _I),
+    "idc_cconv3d": ([_P, _P, _S, _S, _S, _P, _S, _P], _I),
+    "idc_hconv3d": ([_P, _P, _S, _S, _S, _P, _S, _P], _I),
+    "idc_comm_init": ([ctypes.POINTER(ctypes.c_void_p), _I, _I, _P], _I),
+    "idc_comm_destroy": ([_P], _I),
+    "idc_comm_unique_id": ([_P], _I),
+    "idc_dist_workspace_bytes": ([_I, _S, _S, _S, _I], _S),
+    "idc_cconv3d_dist": ([_P, _P, _P, _S, _S, _S, _P, _S, _P], _I),
+    "idc_fill_uniform": ([_P, _S, _U64, _U64, _U64, _P], _I),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class IdcError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"{what}: {status_string(code)} (code {code})")
+        self.code = code
+
+
+def lib() -> ctypes.CDLL:
+    """Load libidconv.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback)")
+                L = ctypes.CDLL(LIB_PATH)
+                for name, (args, res) in SIGNATURES.items():
+                    fn = getattr(L, name)
+                    fn.argtypes = args
+                    fn.restype = res
+                _lib = L
+    return _lib
+
+
+def status_string(code: int) -> str:
+    return lib().idc_status_string(code).decode()
+
+
+def version() -> str:
+    return lib().idc_version().decode()
+
+
+def _check(code: int, what: str):
+    if code != OK:
+        raise IdcError(code, what)
+
+
+def workspace_bytes(kind: int, m0: int, m1: int = 1, m2: int = 1, batch: int = 1) -> int:
+    return int(lib().idc_workspace_bytes(kind, m0, m1, m2, batch))
+
+
+_work_cache: dict = {}
+
+
+def _workspace(nbytes: int, device, work):
+    if nbytes == 0:
+        return None, 0
+    if work is not None:
+        if work.numel() * work.element_size() < nbytes:
+            raise IdcError(ERR_WORKSPACE, "workspace")
+        return work, work.numel() * work.element_size()
+    key = (device, nbytes)
+    w = _work_cache.get(key)
+    if w is None:
+        _work_cache.clear()
+        w = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _work_cache[key] = w
+    return w, nbytes
+
+
+def _stream_ptr(stream, device):
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _prep(arrs):
+    for a in arrs:
+        if a.dtype != torch.complex128:
+            raise TypeError("idconv expects torch.complex128 tensors")
+        if not a.is_contiguous():
+            raise ValueError("idconv expects contiguous tensors")
+    dev = arrs[0].device
+    if any(a.device != dev for a in arrs):
+        raise ValueError("all arrays must be on the same device")
+    return dev.type == "cuda"
+
+
+def _run(arrs, kind, sizes, batch, call, work, stream):
+    """Marshal (possibly host) tensors through one C-ABI call."""
+    on_dev = _prep(arrs)
+    if on_dev:
+        dev_arrs = arrs
+        device = arrs[0].device
+    else:
+        device = torch.device("cuda", torch.cuda.current_device())
+        dev_arrs = [a.to(device, non_blocking=True) for a in arrs]
+    w, wb = _workspace(workspace_bytes(kind, *sizes, batch=batch), device, work)
+    ptrs = [ctypes.c_void_p(a.data_ptr()) for a in dev_arrs]
+    code = call(ptrs, ctypes.c_void_p(w.data_ptr()) if w is not None else None, wb, _stream_ptr(stream, device))
+    _check(code, call.__name__ if hasattr(call, "__name__") else "idconv")
+    if not on_dev:
+        arrs[0].copy_(dev_arrs[0], non_blocking=True)
+    return arrs[0]
+
+
+# ------------------------------------------------------------------- 1D --
+
+def cconv1d(f, g, work=None, stream=None):
+    """Function cconv on f, g of shape (..., m); f <- result."""
+    m = f.shape[-1]
+    B = f.numel() // m
+    L = lib()
+    return _run([f, g], CCONV1D, (m, 1, 1), B,
+                lambda p, w, wb, s: L.idc_cconv1d(p[0], p[1], m, B, w, wb, s), work, stream)
+
+
+def hconv1d(f, g, work=None, stream=None):
+    """Centered Hermitian convolution (Function conv); f <- result."""
+    m = f.shape[-1]
+    B = f.numel() // m
+    L = lib()
+    return _run([f, g], HCONV1D, (m, 1, 1), B,
+                lambda p, w, wb, s: L.idc_hconv1d(p[0], p[1], m, B, w, wb, s), work, stream)
+
+
+def tconv1d(f, g, h, work=None, stream=None):
+    """Centered Hermitian ternary convolution (Function tconv)."""
+    m = f.shape[-1]
+    B = f.numel() // m
+    L = lib()
+    return _run([f, g, h], TCONV1D, (m, 1, 1), B,
+                lambda p, w, wb, s: L.idc_tconv1d(p[0], p[1], p[2], m, B, w, wb, s), work, stream)
+
+
+# ------------------------------------------------------------------- 2D --
+
+def cconv2d(f, g, work=None, stream=None):
+    """Function cconv2 on (..., mx, my); f <- result."""
+    mx, my = f.shape[-2], f.shape[-1]
+    B = f.numel() // (mx * my)
+    L = lib()
+    return _run([f, g], CCONV2D, (mx, my, 1), B,
+                lambda p, w, wb, s: L.idc_cconv2d(p[0], p[1], mx, my, B, w, wb, s), work, stream)
+
+
+def hconv2d(f, g, work=None, stream=None):
+    """Function conv2 on (2mx-1, my); f <- result."""
+    nx, my = f.shape[-2], f.shape[-1]
+    mx = (nx + 1) // 2
+    L = lib()
+    return _run([f, g], HCONV2D, (mx, my, 1), 1,
+                lambda p, w, wb, s: L.idc_hconv2d(p[0], p[1], mx, my, w, wb, s), work, stream)
+
+
+# ------------------------------------------------------------------- 3D --
+
+def cconv3d(f, g, work=None, stream=None):
+    """Function cconv3 on (mx, my, mz); f <- result."""
+    mx, my, mz = f.shape[-3:]
+    L = lib()
+    return _run([f, g], CCONV3D, (mx, my, mz), 1,
+                lambda p, w, wb, s: L.idc_cconv3d(p[0], p[1], mx, my, mz, w, wb, s), work, stream)
+
+
+def hconv3d(f, g, work=None, stream=None):
+    """Centered Hermitian 3D (AMB-9) on (2mx-1, 2my-1, mz)."""
+    nx, ny, mz = f.shape[-3:]
+    mx, my = (nx + 1) // 2, (ny + 1) // 2
+    L = lib()
+    return _run([f, g], HCONV3D, (mx, my, mz), 1,
+                lambda p, w, wb, s: L.idc_hconv3d(p[0], p[1], mx, my, mz, w, wb, s), work, stream)
+
+
+# --------------------------------------------------------- synthetic data --
+
+def fill_uniform(out, array_id: int, seed: int, start: int = 0, stream=None):
+    """Device twin of synthgen.uniform_complex (not part of the method)."""
+    _prep([out])
+    if not out.is_cuda:
+        raise ValueError("fill_uniform writes device memory")
+    _check(lib().idc_fill_uniform(ctypes.c_void_p(out.data_ptr()), out.numel(), seed, array_id, start,
+                                  _stream_ptr(stream, out.device)), "idc_fill_uniform")
+    return out

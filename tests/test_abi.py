@@ -1,0 +1,103 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every
+symbol include/idconv.h declares, and rejects bad arguments synchronously
+before touching the device (include/idconv.h "Errors")."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_1008_1366_b200 import idconv
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "idconv.h")
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"IDC_API\s+[\w\s\*]+?\b(idc_\w+)\s*\(", txt)))
+
+
+def test_header_declares_the_north_star_calls():
+    syms = declared_symbols()
+    for name in ["idc_cconv1d", "idc_hconv1d", "idc_tconv1d", "idc_cconv2d", "idc_hconv2d", "idc_cconv3d",
+                 "idc_hconv3d", "idc_workspace_bytes", "idc_status_string"]:
+        assert name in syms
+
+
+def test_library_exports_every_declared_symbol():
+    L = idconv.lib()
+    for name in declared_symbols():
+        assert hasattr(L, name), name
+        assert name in idconv.SIGNATURES, name
+
+
+def test_exports_match_nm():
+    out = os.popen(f"nm -D --defined-only {idconv.LIB_PATH}").read()
+    exported = set(re.findall(r"\bT (idc_\w+)", out))
+    assert set(declared_symbols()) <= exported
+
+
+def test_version_and_status_strings():
+    assert "sm_100a" in idconv.version()
+    for code in range(6):
+        assert idconv.status_string(code).startswith("IDC_")
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {idconv.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out
+
+
+def _fake(addr):
+    return ctypes.c_void_p(addr)
+
+
+@pytest.mark.parametrize("m", [0, 3, 12, 16384])
+def test_bad_sizes_rejected(m):
+    L = idconv.lib()
+    code = L.idc_cconv1d(_fake(0x1000), _fake(0x100000), m, 1, None, 0, None)
+    assert code == (idconv.ERR_INVALID if m == 0 else idconv.ERR_UNSUPPORTED)
+    code = L.idc_hconv1d(_fake(0x1000), _fake(0x100000), m, 1, None, 0, None)
+    assert code == (idconv.ERR_INVALID if m == 0 else idconv.ERR_UNSUPPORTED)
+
+
+def test_null_misaligned_aliasing_batch0():
+    L = idconv.lib()
+    assert L.idc_cconv1d(None, _fake(0x100000), 16, 1, None, 0, None) == idconv.ERR_INVALID
+    assert L.idc_cconv1d(_fake(0x1008), _fake(0x100000), 16, 1, None, 0, None) == idconv.ERR_INVALID
+    # f and g overlap: 16 complex = 256 bytes each
+    assert L.idc_cconv1d(_fake(0x1000), _fake(0x1080), 16, 1, None, 0, None) == idconv.ERR_INVALID
+    assert L.idc_cconv1d(_fake(0x1000), _fake(0x100000), 16, 0, None, 0, None) == idconv.ERR_INVALID
+    assert L.idc_tconv1d(_fake(0x1000), _fake(0x2000), _fake(0x1000), 16, 1, None, 0, None) == idconv.ERR_INVALID
+
+
+def test_workspace_queries():
+    # 1D rows keep their work vectors on chip up to m = 4096 (P:374-377 u, v live in smem/registers)
+    for m in [1, 2, 64, 1024, 4096]:
+        assert idconv.workspace_bytes(idconv.CCONV1D, m) == 0
+        assert idconv.workspace_bytes(idconv.HCONV1D, m) == 0
+        assert idconv.workspace_bytes(idconv.TCONV1D, m) == 0
+    assert idconv.workspace_bytes(idconv.CCONV1D, 8192) > 0
+    assert idconv.workspace_bytes(idconv.CCONV1D, 3) == 0
+
+
+def test_workspace_too_small_is_reported():
+    L = idconv.lib()
+    need = idconv.workspace_bytes(idconv.CCONV1D, 8192)
+    assert L.idc_cconv1d(_fake(0x1000), _fake(0x10000000), 8192, 1, _fake(0x40000000), need - 16, None) \
+        == idconv.ERR_WORKSPACE
+    # workspace aliasing f
+    assert L.idc_cconv1d(_fake(0x1000), _fake(0x10000000), 8192, 1, _fake(0x1000), need, None) \
+        == idconv.ERR_INVALID
+
+
+def test_no_cpu_fallback():
+    """The product path refuses CPU execution when no GPU exists (no fallback)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    f = torch.zeros(4, dtype=torch.complex128)
+    with pytest.raises(Exception):
+        idconv.cconv1d(f, f.clone())
