@@ -189,6 +189,8 @@ def run_ours(args):
             for s, d in zip(src, dst):
                 d.copy_(s)
 
+    clk = ClockSampler(local).__enter__()   # sample from warm-up through the timed loop
+    time.sleep(0.3)
     for _ in range(args.warmup):
         restore()
         for p, arrs in zip(parts, work):
@@ -202,17 +204,18 @@ def run_ours(args):
         tdist.barrier()
     torch.cuda.synchronize()
     launches = 0
-    with ClockSampler(local) as clk:
-        t_wall0 = time.perf_counter()
-        for k in range(args.steps):
-            restore()
-            for j, (p, arrs) in enumerate(zip(parts, work)):
-                evs[k][j][0].record(stream)
-                call(idc, p, arrs)
-                evs[k][j][1].record(stream)
-                launches += 1
-        torch.cuda.synchronize()
-        t_wall = time.perf_counter() - t_wall0
+    t_wall0 = time.perf_counter()
+    for k in range(args.steps):
+        restore()
+        for j, (p, arrs) in enumerate(zip(parts, work)):
+            evs[k][j][0].record(stream)
+            call(idc, p, arrs)
+            evs[k][j][1].record(stream)
+            launches += 1
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall0
+    time.sleep(0.25)
+    clk.__exit__()
     if ws > 1:
         tdist.barrier()
     part_ms = [sum(evs[k][j][0].elapsed_time(evs[k][j][1]) for k in range(args.steps)) for j in range(len(parts))]

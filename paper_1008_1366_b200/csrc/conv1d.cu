@@ -404,6 +404,10 @@ size_t stash_bytes() {
     default: break;                      \
   }
 
+#ifndef IDC_V2_MAX_M
+#define IDC_V2_MAX_M 4096
+#endif
+
 size_t cconv_rows_work_bytes(int m) {
   IDC_DISPATCH_M(m, return stash_bytes<MM, kCconvStash<MM>>());
   return 0;
@@ -418,15 +422,18 @@ size_t tconv_rows_work_bytes(int m) {
 }
 
 cudaError_t launch_cconv_rows(double2* f, double2* g, int m, long nrows, double2* work, cudaStream_t s) {
+  if (m <= IDC_V2_MAX_M) { IDC_DISPATCH_M(m, return cconv_rows2<MM>(f, g, nrows, s)); }
   IDC_DISPATCH_M(m, return cconv_m<MM>(f, g, nrows, work, s));
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_hconv_rows(double2* f, double2* g, int m, long nrows, double2* work, cudaStream_t s) {
+  if (m <= IDC_V2_MAX_M) { IDC_DISPATCH_M(m, return hconv_rows2<MM>(f, g, nrows, s)); }
   IDC_DISPATCH_M(m, return hconv_m<MM>(f, g, nrows, work, s));
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_tconv_rows(double2* f, double2* g, double2* h, int m, long nrows, double2* work,
                               cudaStream_t s) {
+  if (m <= IDC_V2_MAX_M) { IDC_DISPATCH_M(m, return tconv_rows2<MM>(f, g, h, nrows, s)); }
   IDC_DISPATCH_M(m, return tconv_m<MM>(f, g, h, nrows, work, s));
   return cudaErrorInvalidValue;
 }

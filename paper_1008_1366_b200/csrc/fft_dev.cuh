@@ -40,6 +40,29 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
 }
+// Twiddle-table load.  Volatile so the compiler cannot hoist the (loop
+// invariant) table reads of every pass of every transform to the top of the
+// row loop and keep them all live -- that costs ~90 registers per thread.
+#ifndef IDC_TW_NC
+#define IDC_TW_NC 1
+#endif
+__device__ __forceinline__ double2 ldtw(const double2* p) {
+#if IDC_TW_NC
+  return __ldg(p);   // read-only path; ptxas may hoist and keep twiddles in registers
+#else
+  double2 r;
+  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+#endif
+}
+// Data load that the compiler may not merge with an earlier load of the same
+// address (the residue loops re-read the row; keeping the first read live
+// across transforms would cost 4 registers per element).  L1-cached.
+__device__ __forceinline__ double2 ldv(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 // multiply by w (SIGN > 0) or conj(w) (SIGN < 0)
@@ -158,7 +181,7 @@ __device__ __forceinline__ void pass_compute(double2 (&v)[E], int t, const doubl
       const int jm = (t + T * b) & (NS - 1);
       constexpr int STEP = N / (NS * R);
 #pragma unroll
-      for (int r = 1; r < R; ++r) x[r] = cmul_dir<SIGN>(x[r], __ldg(&tw[r * jm * STEP]));
+      for (int r = 1; r < R; ++r) x[r] = cmul_dir<SIGN>(x[r], ldtw(&tw[r * jm * STEP]));
     }
     dft<R, SIGN>(x);
 #pragma unroll
@@ -210,11 +233,27 @@ template <int N, int E, int SIGN, class Sync, class XS = IdentitySlot>
 __device__ __forceinline__ void fft(double2 (&v)[E], int t, double2* __restrict__ xb,
                                     const double2* __restrict__ tw, Sync sync, XS xs = XS{}) {
   static_assert(N % E == 0 && (E & (E - 1)) == 0 && (N & (N - 1)) == 0, "power-of-two sizes");
-  fft_passes<N, E, 1, SIGN>(v, t, xb, tw, sync, xs);
+  // Launder the thread index so that the (thread-invariant) exchange and
+  // twiddle addresses are recomputed per transform instead of being hoisted
+  // out of the caller's row loop and held live in registers across it.
+  int tl;
+  asm volatile("mov.b32 %0, %1;" : "=r"(tl) : "r"(t));
+  fft_passes<N, E, 1, SIGN>(v, tl, xb, tw, sync, xs);
 }
 
+// CTA barrier as volatile asm: it keeps its order relative to the volatile
+// table loads (ldtw), so the next pass's twiddles are not hoisted above it.
 struct CtaSync {
-  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync 0;" ::: "memory"); }
+};
+
+// Barrier over one thread group (named barrier `id`, `n` threads, n % 32 == 0)
+// so that the row groups of a CTA progress independently.
+struct GroupSync {
+  int id, n;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+  }
 };
 
 }  // namespace idc

@@ -22,6 +22,11 @@ cudaError_t launch_hconv_rows(double2* f, double2* g, int m, long nrows, double2
 cudaError_t launch_tconv_rows(double2* f, double2* g, double2* h, int m, long nrows, double2* work,
                               cudaStream_t s);
 
+// Register-resident variants (rows2.cu), m <= 4096.
+template <int M> cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s);
+template <int M> cudaError_t hconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s);
+template <int M> cudaError_t tconv_rows2(double2* f, double2* g, double2* h, long nrows, cudaStream_t s);
+
 // Number of SMs of the current device (cached).
 int num_sms();
 

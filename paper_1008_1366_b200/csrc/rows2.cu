@@ -1,0 +1,376 @@
+// rows2.cu -- fused 1D row convolutions, register-resident variant (m <= 4096).
+//
+// Same method and equations as conv1d.cu (K2/K3/K4, Functions cconv / conv /
+// tconv of the paper), organised for occupancy:
+//   * E = 8 elements per thread (radix-8 Stockham passes), T = m/8 threads
+//     per row, rows of a CTA synchronise with their own named barrier;
+//   * the per-row intermediates that must survive a transform (the r = 0
+//     product of cconv, the (p0, p1) spectrum of hconv, the output
+//     accumulator of tconv) stay in registers; shared memory holds only the
+//     Stockham exchange buffer (plus, for tconv, the f*g stream products), so
+//     the row's inputs stay L1-resident for the mirrored (U_{m-k}) loads.
+#include "fft_dev.cuh"
+#include "kernels.cuh"
+#include "tables.cuh"
+
+namespace idc {
+
+namespace {
+
+template <int M, int E, int G>
+struct Cfg2 {
+  static constexpr int T = M / E;
+  static constexpr int THREADS = G * T;
+  static constexpr int XB = xbuf_elems<M, E>() > M ? xbuf_elems<M, E>() : M;
+  static constexpr bool NAMED = (T % 32 == 0) && G > 1;
+  // cap registers at 128 per thread: 16 warps per SM for 512-thread CTAs,
+  // two 256-thread CTAs per SM otherwise
+#ifndef IDC_ROWS_REGS
+#define IDC_ROWS_REGS 255
+#endif
+  static constexpr int MINB = (65536 / (THREADS * IDC_ROWS_REGS)) < 1 ? 1 : 65536 / (THREADS * IDC_ROWS_REGS);
+};
+
+template <bool NAMED>
+struct RowSync;
+template <>
+struct RowSync<true> {
+  int id, n;
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+};
+template <>
+struct RowSync<false> {
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync 0;" ::: "memory"); }
+};
+
+template <int M, int E, int G>
+__device__ __forceinline__ RowSync<Cfg2<M, E, G>::NAMED> row_sync(int grp) {
+  if constexpr (Cfg2<M, E, G>::NAMED) return RowSync<true>{1 + grp, Cfg2<M, E, G>::T};
+  else return RowSync<false>{};
+}
+
+// Z_k = w^f_{k,r} + i w^g_{k,r}, w_{k,r} = zr (U_k + c conj U_{m-k}), k >= 1
+__device__ __forceinline__ double2 herm_pair2(double2 fk, double2 gk, double2 fm, double2 gm, double2 zr, double2 c) {
+  const double2 P = make_double2(fk.x - gk.y, fk.y + gk.x);
+  const double2 R = make_double2(fm.x + gm.y, gm.x - fm.y);
+  return cmul(zr, cadd(P, cmul(c, R)));
+}
+
+}  // namespace
+
+// ====================================================================== K2 ==
+// Function cconv, see conv1d.cu for the step-by-step mapping.
+template <int M, int E, int G>
+__global__ void __launch_bounds__(Cfg2<M, E, G>::THREADS, Cfg2<M, E, G>::MINB)
+k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, const double2* __restrict__ twM,
+              const double2* __restrict__ tw2M) {
+  using C = Cfg2<M, E, G>;
+  constexpr int T = C::T;
+  extern __shared__ __align__(16) double2 smem[];
+  const int grp = threadIdx.x / T, t = threadIdx.x - grp * T;
+  double2* xb = smem + grp * (C::XB + 2 * M);
+  double2* S = xb + C::XB;
+  double2* P = S + M;
+  const auto sync = row_sync<M, E, G>(grp);
+  const double inv = 1.0 / (2.0 * M);
+  for (long row0 = (long)blockIdx.x * G; row0 < nrows; row0 += (long)gridDim.x * G) {
+    const long row = row0 + grp;
+    if constexpr (C::NAMED) {
+      if (row >= nrows) break;
+    }
+    const bool ok = row < nrows;
+    const double2* fr = f + (ok ? row : 0) * (long)M;
+    const double2* gr = g + (ok ? row : 0) * (long)M;
+    double2 v[E];
+    // r = 0: u = fft^{-1} f ; v = fft^{-1} g ; u*v
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = ldv(&fr[t + T * i]);
+    fft<M, E, +1>(v, t, xb, twM, sync);
+#pragma unroll
+    for (int i = 0; i < E; ++i) S[t + T * i] = v[i];
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = ldv(&gr[t + T * i]);
+    fft<M, E, +1>(v, t, xb, twM, sync);
+#pragma unroll
+    for (int i = 0; i < E; ++i) P[t + T * i] = cmul(S[t + T * i], v[i]);
+    // r = 1: zeta_{2m}^k-shifted streams
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = cmul(ldv(&fr[t + T * i]), ldtw(&tw2M[t + T * i]));
+    fft<M, E, +1>(v, t, xb, twM, sync);
+#pragma unroll
+    for (int i = 0; i < E; ++i) S[t + T * i] = v[i];
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = cmul(ldv(&gr[t + T * i]), ldtw(&tw2M[t + T * i]));
+    fft<M, E, +1>(v, t, xb, twM, sync);
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = cmul(S[t + T * i], v[i]);
+    // forward transforms, recombination and 1/(2m)
+    fft<M, E, -1>(v, t, xb, twM, sync);
+#pragma unroll
+    for (int i = 0; i < E; ++i) S[t + T * i] = cmulc(v[i], ldtw(&tw2M[t + T * i]));
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = P[t + T * i];
+    fft<M, E, -1>(v, t, xb, twM, sync);
+    if (ok) {
+      double2* fw = f + row * (long)M;
+#pragma unroll
+      for (int i = 0; i < E; ++i) fw[t + T * i] = cscale(cadd(v[i], S[t + T * i]), inv);
+    }
+  }
+}
+
+// ====================================================================== K3 ==
+// Centered Hermitian convolution, N = 3m; see conv1d.cu.
+// Order: r = 0 (p0 kept), r = 1 -> FFT(p0 + i p1) = Q kept in registers,
+// r = -1 -> FFT(p_{-1}); then Q_{m-k} through shared memory and the
+// recombination 3m h_k = P_0 + zeta_{3m}^{k} P_{-1} + zeta_{3m}^{-k} P_1.
+template <int M, int E, int G>
+__global__ void __launch_bounds__(Cfg2<M, E, G>::THREADS, Cfg2<M, E, G>::MINB)
+k_hconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, const double2* __restrict__ twM,
+              const double2* __restrict__ tw3M) {
+  using C = Cfg2<M, E, G>;
+  constexpr int T = C::T;
+  extern __shared__ __align__(16) double2 smem[];
+  const int grp = threadIdx.x / T, t = threadIdx.x - grp * T;
+  double2* xb = smem + grp * (C::XB + M + (M + 1) / 2);
+  double2* QS = xb + C::XB;
+  double* P0S = reinterpret_cast<double*>(QS + M);
+  const auto sync = row_sync<M, E, G>(grp);
+  const double inv = 1.0 / (3.0 * M);
+  const double s3 = 0.86602540378443864676372317075294;  // sqrt(3)/2
+  for (long row0 = (long)blockIdx.x * G; row0 < nrows; row0 += (long)gridDim.x * G) {
+    const long row = row0 + grp;
+    if constexpr (C::NAMED) {
+      if (row >= nrows) break;
+    }
+    const bool ok = row < nrows;
+    const double2* fr = f + (ok ? row : 0) * (long)M;
+    const double2* gr = g + (ok ? row : 0) * (long)M;
+    double2 v[E];
+#pragma unroll
+    for (int rr = 0; rr < 3; ++rr) {
+      const int r = rr == 0 ? 0 : (rr == 1 ? 1 : -1);
+      const double2 c = make_double2(r == 0 ? 1.0 : -0.5, r == 0 ? 0.0 : (r < 0 ? s3 : -s3));  // zeta_3^{-r}
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int k = t + T * i;
+        if (k == 0) {
+          v[i] = make_double2(ldv(&fr[0]).x, ldv(&gr[0]).x);                 // w_{0,r} = Re U_0 (AMB-7)
+        } else {
+          const double2 tz = ldtw(&tw3M[k]);
+          const double2 zr = r == 0 ? make_double2(1.0, 0.0) : (r > 0 ? tz : cconj(tz));
+          v[i] = herm_pair2(ldv(&fr[k]), ldv(&gr[k]), ldv(&fr[M - k]), ldv(&gr[M - k]), zr, c);
+        }
+      }
+      fft<M, E, +1>(v, t, xb, twM, sync);                      // two c2r in one complex FFT
+      if (r == 0) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) P0S[t + T * i] = v[i].x * v[i].y;
+      } else if (r == 1) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) v[i] = make_double2(P0S[t + T * i], v[i].x * v[i].y);
+        fft<M, E, -1>(v, t, xb, twM, sync);
+#pragma unroll
+        for (int i = 0; i < E; ++i) QS[t + T * i] = v[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) v[i] = make_double2(v[i].x * v[i].y, 0.0);
+        fft<M, E, -1>(v, t, xb, twM, sync);
+      }
+    }
+    // separate P_0, P_1 from Q via Q_{m-k}; recombine (Eq. fft0forwardB)
+    sync();   // every thread's Q is in QS
+    if (ok) {
+      double2* fw = f + row * (long)M;
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int k = t + T * i;
+        const double2 a = QS[k], b = cconj(QS[(M - k) & (M - 1)]);
+        const double2 tz = ldtw(&tw3M[k]);
+        const double2 pp0 = cscale(cadd(a, b), 0.5);
+        const double2 d = csub(a, b);
+        const double2 pp1 = make_double2(0.5 * d.y, -0.5 * d.x);
+        const double2 h = cadd(cadd(pp0, cmul(v[i], tz)), cmulc(pp1, tz));
+        fw[k] = cscale(h, inv);
+      }
+    }
+    sync();
+  }
+}
+
+// ====================================================================== K4 ==
+// Centered Hermitian ternary convolution, N = 4m, four residues of size m
+// (see conv1d.cu and DESIGN.md "tconv with four residues").
+template <int M, int E, int G>
+__global__ void __launch_bounds__(Cfg2<M, E, G>::THREADS, Cfg2<M, E, G>::MINB)
+k_tconv_rows2(double2* __restrict__ f, double2* __restrict__ g, double2* __restrict__ h, long nrows,
+              const double2* __restrict__ twM, const double2* __restrict__ tw4M) {
+  using C = Cfg2<M, E, G>;
+  constexpr int T = C::T;
+  extern __shared__ __align__(16) double2 smem[];
+  const int grp = threadIdx.x / T, t = threadIdx.x - grp * T;
+  double2* xb = smem + grp * (C::XB + 2 * M);
+  double2* AP = xb + C::XB;
+  double2* ACC = AP + M;
+  const auto sync = row_sync<M, E, G>(grp);
+  const double inv = 1.0 / (4.0 * M);
+  for (long row0 = (long)blockIdx.x * G; row0 < nrows; row0 += (long)gridDim.x * G) {
+    const long row = row0 + grp;
+    if constexpr (C::NAMED) {
+      if (row >= nrows) break;
+    }
+    const bool ok = row < nrows;
+    const double2* fr = f + (ok ? row : 0) * (long)M;
+    const double2* gr = g + (ok ? row : 0) * (long)M;
+    const double2* hr = h + (ok ? row : 0) * (long)M;
+    double2 v[E];
+#pragma unroll
+    for (int r0 = 0; r0 < 4; r0 += 2) {
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int r = r0 + s;
+        const double2 c = r == 0 ? make_double2(1, 0) : r == 1 ? make_double2(0, -1) : r == 2 ? make_double2(-1, 0)
+                                                                                    : make_double2(0, 1);  // (-i)^r
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int k = t + T * i;
+          if (k == 0) v[i] = make_double2(ldv(&fr[0]).x, ldv(&gr[0]).x);
+          else v[i] = herm_pair2(ldv(&fr[k]), ldv(&gr[k]), ldv(&fr[M - k]), ldv(&gr[M - k]), ldtw(&tw4M[r * k]), c);
+        }
+        fft<M, E, +1>(v, t, xb, twM, sync);
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          if (s == 0) AP[t + T * i].x = v[i].x * v[i].y;
+          else AP[t + T * i].y = v[i].x * v[i].y;
+        }
+      }
+      {  // h packed across the residue pair: w^h_r + i w^h_{r+1}
+        const double2 c0 = r0 == 0 ? make_double2(1, 0) : make_double2(-1, 0);
+        const double2 c1 = r0 == 0 ? make_double2(0, -1) : make_double2(0, 1);
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int k = t + T * i;
+          if (k == 0) {
+            v[i] = make_double2(ldv(&hr[0]).x, ldv(&hr[0]).x);
+          } else {
+            const double2 hk = ldv(&hr[k]), hm = cconj(ldv(&hr[M - k]));
+            const double2 w0 = cmul(ldtw(&tw4M[r0 * k]), cadd(hk, cmul(c0, hm)));
+            const double2 w1 = cmul(ldtw(&tw4M[(r0 + 1) * k]), cadd(hk, cmul(c1, hm)));
+            v[i] = make_double2(w0.x - w1.y, w0.y + w1.x);
+          }
+        }
+      }
+      fft<M, E, +1>(v, t, xb, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const double2 a = AP[t + T * i];
+        v[i] = make_double2(a.x * v[i].x, a.y * v[i].y);
+      }
+      fft<M, E, -1>(v, t, xb, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) xb[t + T * i] = v[i];
+      sync();
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int k = t + T * i;
+        const double2 a = v[i], b = cconj(xb[(M - k) & (M - 1)]);
+        const double2 pp0 = cscale(cadd(a, b), 0.5);
+        const double2 d = csub(a, b);
+        const double2 pp1 = make_double2(0.5 * d.y, -0.5 * d.x);
+        const double2 ct = cadd(cmulc(pp0, ldtw(&tw4M[r0 * k])), cmulc(pp1, ldtw(&tw4M[(r0 + 1) * k])));
+        ACC[k] = r0 == 0 ? ct : cadd(ACC[k], ct);
+      }
+      sync();
+    }
+    if (ok) {
+      double2* fw = f + row * (long)M;
+#pragma unroll
+      for (int i = 0; i < E; ++i) fw[t + T * i] = cscale(ACC[t + T * i], inv);
+    }
+  }
+}
+
+// ================================================================ launchers ==
+namespace {
+
+template <class K>
+cudaError_t launch2(K kernel, int threads, size_t smem, long nrows, int groups, cudaStream_t s, void** args) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  long need = (nrows + groups - 1) / groups;
+  long grid = (long)num_sms() * per_sm;
+  if (need < grid) grid = need;
+  if (grid < 1) grid = 1;
+  return cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s);
+}
+
+// elements per thread and rows per CTA of the v2 kernels
+#ifndef IDC_ROWS_E
+#define IDC_ROWS_E 16
+#endif
+template <int M>
+struct Tune {
+  static constexpr int E = M < IDC_ROWS_E ? M : IDC_ROWS_E;
+  static constexpr int T = M / E;
+  static constexpr int G = T >= 256 ? 1 : 256 / T;
+};
+
+}  // namespace
+
+template <int M>
+cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s) {
+  constexpr int E = Tune<M>::E, G = Tune<M>::G;
+  using C = Cfg2<M, E, G>;
+  const double2* twM = zeta_table(M);
+  const double2* tw2M = zeta_table(2 * M);
+  if (!twM || !tw2M) return cudaErrorMemoryAllocation;
+  void* args[] = {&f, &g, &nrows, &twM, &tw2M};
+  return launch2(k_cconv_rows2<M, E, G>, C::THREADS, (size_t)G * (C::XB + 2 * M) * 16, nrows, G, s, args);
+}
+
+template <int M>
+cudaError_t hconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s) {
+  constexpr int E = Tune<M>::E, G = Tune<M>::G;
+  using C = Cfg2<M, E, G>;
+  const double2* twM = zeta_table(M);
+  const double2* tw3M = zeta_table(3 * M);
+  if (!twM || !tw3M) return cudaErrorMemoryAllocation;
+  void* args[] = {&f, &g, &nrows, &twM, &tw3M};
+  return launch2(k_hconv_rows2<M, E, G>, C::THREADS, (size_t)G * (C::XB + M + (M + 1) / 2) * 16, nrows, G, s,
+                 args);
+}
+
+template <int M>
+cudaError_t tconv_rows2(double2* f, double2* g, double2* h, long nrows, cudaStream_t s) {
+  constexpr int E = Tune<M>::E, G = Tune<M>::G;
+  using C = Cfg2<M, E, G>;
+  const double2* twM = zeta_table(M);
+  const double2* tw4M = zeta_table(4 * M);
+  if (!twM || !tw4M) return cudaErrorMemoryAllocation;
+  void* args[] = {&f, &g, &h, &nrows, &twM, &tw4M};
+  return launch2(k_tconv_rows2<M, E, G>, C::THREADS, (size_t)G * (C::XB + 2 * M) * 16, nrows, G, s, args);
+}
+
+#define IDC_INST2(M)                                                                        \
+  template cudaError_t cconv_rows2<M>(double2*, double2*, long, cudaStream_t);              \
+  template cudaError_t hconv_rows2<M>(double2*, double2*, long, cudaStream_t);              \
+  template cudaError_t tconv_rows2<M>(double2*, double2*, double2*, long, cudaStream_t);
+IDC_INST2(1)
+IDC_INST2(2)
+IDC_INST2(4)
+IDC_INST2(8)
+IDC_INST2(16)
+IDC_INST2(32)
+IDC_INST2(64)
+IDC_INST2(128)
+IDC_INST2(256)
+IDC_INST2(512)
+IDC_INST2(1024)
+IDC_INST2(2048)
+IDC_INST2(4096)
+
+}  // namespace idc

@@ -20,7 +20,7 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libidconv.so")
+LIB_PATH = os.environ.get("IDCONV_LIB") or os.path.join(_HERE, "libidconv.so")
 
 OK, ERR_INVALID, ERR_UNSUPPORTED, ERR_WORKSPACE, ERR_CUDA, ERR_NCCL = range(6)
 CCONV1D, HCONV1D, TCONV1D, CCONV2D, HCONV2D, CCONV3D, HCONV3D = range(7)

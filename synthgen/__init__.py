@@ -50,7 +50,7 @@ _C2 = np.uint64(0x94D049BB133111EB)
 def sm_scalar(x: int) -> int:
     """splitmix64 finalizer on a Python int (reference scalar form)."""
     m = (1 << 64) - 1
-    z = (x + 0x9E3779B97F4A7C15) & m
+    z = (int(x) + 0x9E3779B97F4A7C15) & m
     z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
     z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
     return z ^ (z >> 31)
@@ -66,7 +66,7 @@ def sm(x: np.ndarray) -> np.ndarray:
 
 
 def stream_key(seed: int, array_id: int) -> int:
-    return sm_scalar(seed ^ sm_scalar(array_id))
+    return sm_scalar(int(seed) ^ sm_scalar(int(array_id)))
 
 
 def uniform_complex(n: int, array_id: int, seed: int = SEED, start: int = 0) -> np.ndarray:
@@ -91,7 +91,7 @@ def uniform_at(array_id: int, linear_index: int, seed: int = SEED) -> complex:
     s = stream_key(seed, array_id)
     vals = []
     for part in (0, 1):
-        x = sm_scalar((s + 2 * linear_index + part) & ((1 << 64) - 1))
+        x = sm_scalar((s + 2 * int(linear_index) + part) & ((1 << 64) - 1))
         vals.append((x >> 11) * (2.0 ** -53) * 2.0 - 1.0)
     return complex(vals[0], vals[1])
 
