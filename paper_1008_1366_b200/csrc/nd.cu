@@ -1,13 +1,155 @@
-// nd.cu -- 2D / 3D compositions (placeholder until the pencil kernels land).
+// nd.cu -- 2D and 3D implicitly dealiased convolutions composed from the
+// pencil kernels (K5-K8, pencils.cu) and the fused row kernels (K2/K3).
+//
+//   cconv2d  Function cconv2:  K5 along x -> K2 on the rows of
+//            both residue streams (f, U) -> K6 along x.
+//   hconv2d  Function conv2:  K7 along x -> K3 on the 2mx-1
+//            rows of f and the mx+1 rows of U -> K8 along x.
+//   cconv3d  Function cconv3:  K5 along x over all (y,z)
+//            columns, then cconv2 on every x-residue slab, K6 along x.
+//   hconv3d  "analogous manner" (AMB-9): K7 along x, conv2 on
+//            every x-residue slab, K8 along x.
+//
+// The paper reuses one set of 2D work arrays u2, v2 for all slabs (P:880-889,
+// P:920-925).  Here the slabs are processed in groups of G whose 2D work
+// arrays U2, V2 (G slabs each) are sized to stay resident in L2
+// (SURVEY §8(a) a9), so only the slab read and the slab result write reach
+// HBM.  All launches are stream-ordered on the caller's stream.
+#include <algorithm>
+
+#include "kernels.cuh"
 #include "nd.cuh"
+#include "nd_internal.cuh"
 
 namespace idc {
-size_t cconv2d_work_bytes(size_t, size_t, size_t) { return 0; }
-size_t hconv2d_work_bytes(size_t, size_t) { return 0; }
-size_t cconv3d_work_bytes(size_t, size_t, size_t) { return 0; }
-size_t hconv3d_work_bytes(size_t, size_t, size_t) { return 0; }
-cudaError_t run_cconv2d(double2*, double2*, int, int, long, double2*, cudaStream_t) { return cudaErrorNotSupported; }
-cudaError_t run_hconv2d(double2*, double2*, int, int, double2*, cudaStream_t) { return cudaErrorNotSupported; }
-cudaError_t run_cconv3d(double2*, double2*, int, int, int, double2*, cudaStream_t) { return cudaErrorNotSupported; }
-cudaError_t run_hconv3d(double2*, double2*, int, int, int, double2*, cudaStream_t) { return cudaErrorNotSupported; }
+
+namespace {
+constexpr size_t W16 = sizeof(double2);
+bool pow2ok(size_t m) { return m >= 1 && m <= 8192 && (m & (m - 1)) == 0; }
+
+size_t l2_bytes() {
+  static int l2 = 0;
+  if (l2 == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess || l2 <= 0) l2 = 126 << 20;
+  }
+  return (size_t)l2;
+}
+
+// slabs per group: keep f/g slabs + U2/V2 of a group within ~half of L2
+long slab_group(size_t slab_bytes_all, long nslabs) {
+  long G = (long)((l2_bytes() / 2) / std::max<size_t>(slab_bytes_all, 1));
+  return std::max<long>(1, std::min<long>(G, nslabs));
+}
+}  // namespace
+
+// ------------------------------------------------------------ workspaces --
+size_t cconv2d_work_bytes(size_t mx, size_t my, size_t batch) {
+  if (!pow2ok(mx) || !pow2ok(my) || batch == 0) return 0;
+  return 2 * batch * mx * my * W16 + cconv_rows_work_bytes((int)my);
+}
+size_t hconv2d_work_bytes(size_t mx, size_t my) {
+  if (!pow2ok(mx) || !pow2ok(my)) return 0;
+  return 2 * (mx + 1) * my * W16 + hconv_rows_work_bytes((int)my);
+}
+static long c3_group(size_t mx, size_t my, size_t mz) { return slab_group(4 * my * mz * W16, 2 * (long)mx); }
+static long h3_group(size_t mx, size_t my, size_t mz) {
+  return slab_group(2 * ((2 * my - 1) + (my + 1)) * mz * W16, 3 * (long)mx);
+}
+size_t cconv3d_work_bytes(size_t mx, size_t my, size_t mz) {
+  if (!pow2ok(mx) || !pow2ok(my) || !pow2ok(mz)) return 0;
+  const long G = c3_group(mx, my, mz);
+  return 2 * mx * my * mz * W16 + 2 * (size_t)G * my * mz * W16 + cconv_rows_work_bytes((int)mz);
+}
+size_t hconv3d_work_bytes(size_t mx, size_t my, size_t mz) {
+  if (!pow2ok(mx) || !pow2ok(my) || !pow2ok(mz)) return 0;
+  const long G = h3_group(mx, my, mz);
+  return 2 * (mx + 1) * (2 * my - 1) * mz * W16 + 2 * (size_t)G * (my + 1) * mz * W16 +
+         hconv_rows_work_bytes((int)mz);
+}
+
+// ------------------------------------------------------------------- 2D --
+#define IDC_TRY(x)                       \
+  do {                                   \
+    cudaError_t e_ = (x);                \
+    if (e_ != cudaSuccess) return e_;    \
+  } while (0)
+
+cudaError_t run_cconv2d(double2* f, double2* g, int mx, int my, long batch, double2* work, cudaStream_t s) {
+  const long n = (long)mx * my;
+  double2* U = work;
+  double2* V = work + batch * n;
+  double2* rw = V + batch * n;
+  IDC_TRY(launch_pad_bwd(f, g, U, V, mx, my, batch, n, n, s));            // fftpadBackward on columns
+  IDC_TRY(launch_cconv_rows(f, g, my, batch * mx, rw, s));                // cconv on rows of stream 0
+  IDC_TRY(launch_cconv_rows(U, V, my, batch * mx, rw, s));                // cconv on rows of stream 1
+  return launch_pad_fwd(f, U, mx, my, batch, n, n, s);                    // fftpadForward on columns
+}
+
+cudaError_t run_hconv2d(double2* f, double2* g, int mx, int my, double2* work, cudaStream_t s) {
+  double2* U = work;
+  double2* V = work + (long)(mx + 1) * my;
+  double2* rw = V + (long)(mx + 1) * my;
+  IDC_TRY(launch_pad0_bwd(f, g, U, V, mx, my, 1, 0, 0, s));               // fft0padBackward on columns
+  IDC_TRY(launch_hconv_rows(f, g, my, 2L * mx - 1, rw, s));               // conv on rows i = 0..2mx-2
+  IDC_TRY(launch_hconv_rows(U, V, my, (long)mx + 1, rw, s));              // conv on rows i = 0..mx
+  return launch_pad0_fwd(f, U, mx, my, 1, 0, 0, s);                       // fft0padForward on columns
+}
+
+// ------------------------------------------------------------------- 3D --
+cudaError_t run_cconv3d(double2* f, double2* g, int mx, int my, int mz, double2* work, cudaStream_t s) {
+  const long slab = (long)my * mz, n = (long)mx * slab;
+  const long G = c3_group(mx, my, mz);
+  double2* U = work;
+  double2* V = U + n;
+  double2* U2 = V + n;
+  double2* V2 = U2 + G * slab;
+  double2* rw = V2 + G * slab;
+  IDC_TRY(launch_pad_bwd(f, g, U, V, mx, slab, 1, 0, 0, s));              // x: fftpadBackward over all (y,z)
+  for (int half = 0; half < 2; ++half) {                                   // x-residue slabs: f (even), U (odd)
+    double2* A = half == 0 ? f : U;
+    double2* B = half == 0 ? g : V;
+    for (long s0 = 0; s0 < mx; s0 += G) {
+      const long gs = std::min<long>(G, mx - s0);
+      double2* a = A + s0 * slab;
+      double2* b = B + s0 * slab;
+      // cconv2 on the group's slabs, reusing U2/V2
+      IDC_TRY(launch_pad_bwd(a, b, U2, V2, my, mz, gs, slab, slab, s));
+      IDC_TRY(launch_cconv_rows(a, b, mz, gs * my, rw, s));
+      IDC_TRY(launch_cconv_rows(U2, V2, mz, gs * my, rw, s));
+      IDC_TRY(launch_pad_fwd(a, U2, my, mz, gs, slab, slab, s));
+    }
+  }
+  return launch_pad_fwd(f, U, mx, slab, 1, 0, 0, s);                     // x: fftpadForward
+}
+
+cudaError_t run_hconv3d(double2* f, double2* g, int mx, int my, int mz, double2* work, cudaStream_t s) {
+  const long slab = (long)(2 * my - 1) * mz;       // one x-residue slab (2my-1) x mz
+  const long uslab = (long)(my + 1) * mz;          // its y work array (my+1) x mz
+  const long G = h3_group(mx, my, mz);
+  double2* U = work;                                // (mx+1) slabs
+  double2* V = U + (long)(mx + 1) * slab;
+  double2* U2 = V + (long)(mx + 1) * slab;
+  double2* V2 = U2 + G * uslab;
+  double2* rw = V2 + G * uslab;
+  IDC_TRY(launch_pad0_bwd(f, g, U, V, mx, slab, 1, 0, 0, s));             // x: fft0padBackward
+  for (int half = 0; half < 2; ++half) {                                   // slabs: 2mx-1 in f, mx+1 in U
+    double2* A = half == 0 ? f : U;
+    double2* B = half == 0 ? g : V;
+    const long ns = half == 0 ? 2L * mx - 1 : (long)mx + 1;
+    for (long s0 = 0; s0 < ns; s0 += G) {
+      const long gs = std::min<long>(G, ns - s0);
+      double2* a = A + s0 * slab;
+      double2* b = B + s0 * slab;
+      // conv2 on the group's slabs, reusing U2/V2
+      IDC_TRY(launch_pad0_bwd(a, b, U2, V2, my, mz, gs, slab, uslab, s));
+      IDC_TRY(launch_hconv_rows(a, b, mz, gs * (2L * my - 1), rw, s));
+      IDC_TRY(launch_hconv_rows(U2, V2, mz, gs * ((long)my + 1), rw, s));
+      IDC_TRY(launch_pad0_fwd(a, U2, my, mz, gs, slab, uslab, s));
+    }
+  }
+  return launch_pad0_fwd(f, U, mx, slab, 1, 0, 0, s);                    // x: fft0padForward
+}
+
 }  // namespace idc

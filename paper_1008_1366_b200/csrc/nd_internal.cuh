@@ -1,0 +1,21 @@
+// nd_internal.cuh -- pencil-kernel launchers shared by the 2D/3D drivers.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace idc {
+
+// K5: fftpadBackward on the m-row pencils of (batch x m x ncols) arrays f
+// (and g if non-null): even stream in place, odd stream into U (V).
+cudaError_t launch_pad_bwd(double2* f, double2* g, double2* U, double2* V, int m, long ncols, long batch,
+                           long bstride, long ustride, cudaStream_t s);
+// K6: fftpadForward: f <- (FFT f + zeta^{-k} FFT U)/(2m).
+cudaError_t launch_pad_fwd(double2* f, const double2* U, int m, long ncols, long batch, long bstride, long ustride,
+                           cudaStream_t s);
+// K7: centered fft0padBackward on (2m-1)-row pencils; streams in f (2m-1 rows) + U (m+1 rows).
+cudaError_t launch_pad0_bwd(double2* f, double2* g, double2* U, double2* V, int m, long ncols, long batch,
+                            long bstride, long ustride, cudaStream_t s);
+// K8: centered fft0padForward.
+cudaError_t launch_pad0_fwd(double2* f, const double2* U, int m, long ncols, long batch, long bstride, long ustride,
+                            cudaStream_t s);
+
+}  // namespace idc

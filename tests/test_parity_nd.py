@@ -1,0 +1,148 @@
+"""GPU parity of the 2D / 3D kinds against the oracle's direct sums
+(SURVEY §8(c) D4-D7): small sizes over every axis length class (including
+ragged column tiles and m = 1 axes) element by element, and the full-size
+configs 3 and 4 on sampled outputs plus their corners/edges (O5)."""
+import numpy as np
+import pytest
+import torch
+
+import synthgen
+from oracle import closed, direct, rel_l2
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-14
+
+
+@pytest.fixture(scope="module")
+def idc():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_1008_1366_b200 import idconv
+    return idconv
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("mx,my,B", [(1, 1, 1), (1, 8, 2), (8, 1, 2), (2, 4, 3), (4, 8, 1), (16, 8, 2),
+                                     (8, 32, 1), (32, 16, 1), (64, 64, 1), (128, 16, 1), (16, 128, 1)])
+def test_cconv2d_small(idc, mx, my, B):
+    f, g = synthgen.cconv2d_inputs(mx, my, B)
+    ref = np.stack([direct.cconv2d(f[b], g[b]) for b in range(B)])
+    F, G = dev(f), dev(g)
+    idc.cconv2d(F, G)
+    err = rel_l2(F.cpu().numpy(), ref)
+    assert err < TOL, err
+
+
+@pytest.mark.parametrize("mx,my", [(1, 1), (2, 2), (1, 4), (4, 1), (2, 8), (4, 4), (8, 16), (16, 8), (32, 32),
+                                   (64, 16)])
+def test_hconv2d_small(idc, mx, my):
+    f, g = synthgen.hconv2d_inputs(mx, my, scaled=False)
+    ref = direct.hconv2d(f, g)
+    F, G = dev(f), dev(g)
+    idc.hconv2d(F, G)
+    err = rel_l2(F.cpu().numpy(), ref)
+    assert err < TOL, err
+
+
+def test_hconv2d_unsymmetrized_input_is_projected(idc):
+    """AMB-7: a ky=0 line that is not conjugate-symmetric is used through its projection."""
+    f, g = synthgen.cconv2d_inputs(7, 8, 1)
+    f, g = f[0], g[0]                      # 7 x 8 = (2*4-1) x 8, raw random (not symmetric)
+    ref = direct.hconv2d(f, g)              # oracle projects (U + conj U(-kx))/2
+    F, G = dev(f), dev(g)
+    idc.hconv2d(F, G)
+    assert rel_l2(F.cpu().numpy(), ref) < TOL
+
+
+def test_nd_closed_families(idc):
+    f, g, H = closed.cconv_nd((16, 32))
+    F, G = dev(f), dev(g)
+    idc.cconv2d(F, G)
+    assert rel_l2(F.cpu().numpy(), H) < TOL
+    f, g, H = closed.hconv_nd((16, 8))
+    F, G = dev(f), dev(g)
+    idc.hconv2d(F, G)
+    assert rel_l2(F.cpu().numpy(), H) < TOL
+    f, g, H = closed.cconv_nd((8, 4, 16))
+    F, G = dev(f), dev(g)
+    idc.cconv3d(F, G)
+    assert rel_l2(F.cpu().numpy(), H) < TOL
+    f, g, H = closed.hconv_nd((4, 8, 8))
+    F, G = dev(f), dev(g)
+    idc.hconv3d(F, G)
+    assert rel_l2(F.cpu().numpy(), H) < TOL
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (2, 2, 2), (4, 4, 4), (8, 4, 16), (4, 16, 8), (16, 16, 16)])
+def test_cconv3d_small(idc, shape):
+    f, g = synthgen.cconv3d_inputs(*shape)
+    ref = direct.cconv3d(f, g)
+    F, G = dev(f), dev(g)
+    idc.cconv3d(F, G)
+    assert rel_l2(F.cpu().numpy(), ref) < TOL
+
+
+@pytest.mark.parametrize("ms", [(1, 1, 1), (2, 2, 2), (2, 4, 2), (4, 2, 4), (4, 4, 4), (8, 8, 8)])
+def test_hconv3d_small(idc, ms):
+    f, g = synthgen.hconv3d_inputs(*ms)
+    ref = direct.hconv3d(f, g)
+    F, G = dev(f), dev(g)
+    idc.hconv3d(F, G)
+    out = F.cpu().numpy()
+    assert rel_l2(out, ref) < TOL
+    # output kz = 0 plane stays Hermitian
+    p = out[:, :, 0]
+    assert np.max(np.abs(p - np.conj(p[::-1, ::-1]))) < 1e-13 * np.max(np.abs(out))
+
+
+# ------------------------------------------------------- full-size configs --
+
+def sample_idx(shape, n, seed=11, origin=None):
+    """n random outputs + every corner + a small block around the Fourier
+    origin (where the 1/(1+|k|^2)-scaled configs have their largest outputs,
+    so that the sampled relative L2 error is measured against the output's
+    own scale, not only against its tiny high-|k| tail)."""
+    rs = np.random.default_rng(seed)
+    size = int(np.prod(shape))
+    corners = [np.ravel_multi_index(tuple(c), shape) for c in np.ndindex(*(2,) * len(shape))
+               for c in [tuple((s - 1) * b for s, b in zip(shape, c))]]
+    near = []
+    if origin is not None:
+        for off in np.ndindex(*(3,) * len(shape)):
+            p = tuple(min(max(o + d - 1, 0), s - 1) for o, d, s in zip(origin, off, shape))
+            near.append(np.ravel_multi_index(p, shape))
+    return np.unique(np.concatenate([corners, near, rs.choice(size, n, replace=False)]).astype(np.int64))
+
+
+def test_config3a_cconv2d_1024(idc):
+    m = 1024
+    f, g = synthgen.cconv2d_inputs(m, m, 1)
+    F, G = dev(f), dev(g)
+    idc.cconv2d(F, G)
+    idx = sample_idx((m, m), 48, origin=(0, 0))
+    out = F.cpu().numpy().reshape(-1)[idx]
+    assert rel_l2(out, direct.cconv_nd_at(f[0], g[0], idx)) < TOL
+
+
+def test_config3b_cconv2d_batch64_256(idc):
+    m, B = 256, 64
+    f, g = synthgen.cconv2d_inputs(m, m, B)
+    F, G = dev(f), dev(g)
+    idc.cconv2d(F, G)
+    out = F.cpu().numpy()
+    for b in (0, 37, 63):
+        idx = sample_idx((m, m), 24, seed=b, origin=(0, 0))
+        assert rel_l2(out[b].reshape(-1)[idx], direct.cconv_nd_at(f[b], g[b], idx)) < TOL
+
+
+def test_config4_hconv2d_2048(idc):
+    mx = my = 2048
+    f, g = synthgen.hconv2d_inputs(mx, my)
+    F, G = dev(f), dev(g)
+    idc.hconv2d(F, G)
+    idx = sample_idx((2 * mx - 1, my), 24, origin=(mx - 1, 0))
+    out = F.cpu().numpy().reshape(-1)[idx]
+    assert rel_l2(out, direct.hconv2d_at(f, g, idx)) < TOL
