@@ -152,10 +152,29 @@ IDC_API idc_status idc_comm_unique_id(void* id_out);
 
 IDC_API size_t idc_dist_workspace_bytes(idc_kind k, size_t mx, size_t my, size_t mz, int nranks);
 
-/* f, g hold this rank's x-slab [rank*mx/P, (rank+1)*mx/P) of the global
- * mx x my x mz arrays (complex) -- result in place, same layout. */
+/* Distributed cconv3d (the decomposition is ours, AMB-19: the
+ * paper is single-process).  f, g hold this rank's x-slab
+ * [rank*mx/P, (rank+1)*mx/P) of the global mx x my x mz arrays (each rank's
+ * slab contiguous, row-major) -- result in place, same layout.  Requires P a
+ * power of two dividing mx and 2*my.  Internally: fftpadBackward along the
+ * locally complete y axis, ncclAlltoAll of the y-residue streams, the 2D
+ * (x, z) implicit convolution (Function cconv2) of every owned
+ * y-residue, ncclAlltoAll back, fftpadForward along y.  All on `stream`. */
 IDC_API idc_status idc_cconv3d_dist(void* comm, idc_c128* f, idc_c128* g, size_t mx, size_t my, size_t mz,
                             void* work, size_t work_bytes, idc_stream stream);
+
+/* Host-side plan of the decomposition (no GPU needed): out[0..5] =
+ * {local x planes nx, y-residues per rank nres, elements per peer block,
+ * first local plane x0, first owned residue q0, elements per y-stream S}. */
+IDC_API idc_status idc_dist_plan(size_t mx, size_t my, size_t mz, int nranks, int rank, long long* out);
+
+/* Single-GPU emulation of nranks ranks (validation of the P > 1 path without
+ * P GPUs): f_slabs[r], g_slabs[r] are device pointers to rank r's x-slabs;
+ * the all-to-alls are device copies between the virtual ranks' buffers; the
+ * compute phases are exactly those of idc_cconv3d_dist. */
+IDC_API size_t idc_dist_emulated_workspace_bytes(size_t mx, size_t my, size_t mz, int nranks);
+IDC_API idc_status idc_cconv3d_dist_emulated(int nranks, idc_c128** f_slabs, idc_c128** g_slabs, size_t mx,
+                                             size_t my, size_t mz, void* work, size_t work_bytes, idc_stream stream);
 
 /* ---- synthetic inputs (not part of the method) -------------------------- */
 

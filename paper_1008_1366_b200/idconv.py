@@ -44,6 +44,10 @@ SIGNATURES = {
     "idc_dist_workspace_bytes": ([_I, _S, _S, _S, _I], _S),
     "idc_cconv3d_dist": ([_P, _P, _P, _S, _S, _S, _P, _S, _P], _I),
     "idc_fill_uniform": ([_P, _S, _U64, _U64, _U64, _P], _I),
+    "idc_dist_plan": ([_S, _S, _S, _I, _I, ctypes.POINTER(ctypes.c_longlong)], _I),
+    "idc_dist_emulated_workspace_bytes": ([_S, _S, _S, _I], _S),
+    "idc_cconv3d_dist_emulated": ([_I, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), _S, _S, _S,
+                                   _P, _S, _P], _I),
 }
 
 _lib = None
@@ -222,3 +226,70 @@ def fill_uniform(out, array_id: int, seed: int, start: int = 0, stream=None):
     _check(lib().idc_fill_uniform(ctypes.c_void_p(out.data_ptr()), out.numel(), seed, array_id, start,
                                   _stream_ptr(stream, out.device)), "idc_fill_uniform")
     return out
+
+
+# ------------------------------------------------------ distributed 3D --
+
+def dist_plan(mx: int, my: int, mz: int, nranks: int, rank: int) -> dict:
+    """Host-side decomposition plan (pure logic in the C library, no GPU)."""
+    out = (ctypes.c_longlong * 6)()
+    _check(lib().idc_dist_plan(mx, my, mz, nranks, rank, out), "idc_dist_plan")
+    return dict(nx=out[0], nres=out[1], blk=out[2], x0=out[3], q0=out[4], S=out[5])
+
+
+class Comm:
+    """NCCL communicator of the library, bootstrapped over a torch.distributed
+    process group (the 128-byte ncclUniqueId is broadcast from rank 0)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if self.rank == 0:
+            buf = (ctypes.c_ubyte * 128)()
+            _check(lib().idc_comm_unique_id(buf), "idc_comm_unique_id")
+            uid = torch.tensor(list(buf), dtype=torch.uint8)
+        backend = dist.get_backend(group)
+        if backend == "nccl":
+            uid = uid.cuda()
+            dist.broadcast(uid, 0, group=group)
+            uid = uid.cpu()
+        else:
+            dist.broadcast(uid, 0, group=group)
+        idbuf = (ctypes.c_ubyte * 128)(*uid.tolist())
+        self.handle = ctypes.c_void_p()
+        _check(lib().idc_comm_init(ctypes.byref(self.handle), self.size, self.rank, idbuf), "idc_comm_init")
+
+    def close(self):
+        if self.handle:
+            lib().idc_comm_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+
+def cconv3d_dist(comm: Comm, f, g, mx: int, my: int, mz: int, work=None, stream=None):
+    """Distributed cconv3d on this rank's x-slab f, g (shape (mx/P, my, mz))."""
+    _prep([f, g])
+    nb = int(lib().idc_dist_workspace_bytes(CCONV3D, mx, my, mz, comm.size))
+    if nb == 0:
+        raise IdcError(ERR_UNSUPPORTED, "idc_cconv3d_dist")
+    w, wb = _workspace(nb, f.device, work)
+    _check(lib().idc_cconv3d_dist(comm.handle, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(g.data_ptr()),
+                                  mx, my, mz, ctypes.c_void_p(w.data_ptr()), wb, _stream_ptr(stream, f.device)),
+           "idc_cconv3d_dist")
+    return f
+
+
+def cconv3d_dist_emulated(f_slabs, g_slabs, mx: int, my: int, mz: int, stream=None):
+    """Single-GPU emulation of len(f_slabs) ranks (validation of the P > 1 path)."""
+    P = len(f_slabs)
+    _prep(list(f_slabs) + list(g_slabs))
+    nb = int(lib().idc_dist_emulated_workspace_bytes(mx, my, mz, P))
+    if nb == 0:
+        raise IdcError(ERR_UNSUPPORTED, "idc_cconv3d_dist_emulated")
+    w = torch.empty(nb, dtype=torch.uint8, device=f_slabs[0].device)
+    fp = (ctypes.c_void_p * P)(*[a.data_ptr() for a in f_slabs])
+    gp = (ctypes.c_void_p * P)(*[a.data_ptr() for a in g_slabs])
+    _check(lib().idc_cconv3d_dist_emulated(P, fp, gp, mx, my, mz, ctypes.c_void_p(w.data_ptr()), nb,
+                                           _stream_ptr(stream, f_slabs[0].device)), "idc_cconv3d_dist_emulated")
+    return f_slabs

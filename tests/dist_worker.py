@@ -1,0 +1,68 @@
+"""Worker of the 2-process gloo test of the distributed cconv3d decomposition.
+
+Each rank follows the library's own host-side plan (idc_dist_plan, pure C
+logic) for which x-planes it owns and which y-residues it receives, moves the
+residue blocks with a real collective (torch.distributed all_to_all_single
+over gloo), and evaluates the per-rank arithmetic with the oracle's implicit
+equations (numpy; the GPU kernels are covered by the emulated-rank GPU test).
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def run(rank, world, port, shape, outdir):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import implicit
+    from paper_1008_1366_b200 import idconv
+    import synthgen
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mx, my, mz = shape
+    plan = idconv.dist_plan(mx, my, mz, world, rank)
+    nx, nres, x0 = plan["nx"], plan["nres"], plan["x0"]
+    f, g = synthgen.cconv3d_inputs(mx, my, mz)
+    fl, gl = f[x0:x0 + nx], g[x0:x0 + nx]
+
+    # phase A: fftpadBackward along y on the local planes (Eq. cconv1backward)
+    def ypass(a):
+        e, o = implicit.fftpad_backward(np.swapaxes(a, 1, 2))      # along y
+        return np.concatenate([np.swapaxes(e, 1, 2), np.swapaxes(o, 1, 2)], axis=1)  # residues q = 0..2my-1
+
+    def pack(streams):
+        blocks = [streams[:, p * nres:(p + 1) * nres, :] for p in range(world)]
+        return torch.from_numpy(np.ascontiguousarray(np.stack(blocks)))   # [p][x][q'][z]
+
+    sf, sg = pack(ypass(fl)), pack(ypass(gl))
+    rf, rg = torch.empty_like(sf), torch.empty_like(sg)
+    dist.all_to_all_single(rf.view(torch.float64), sf.view(torch.float64))
+    dist.all_to_all_single(rg.view(torch.float64), sg.view(torch.float64))
+    # received [src][x_local][q'][z] == [x][q'][z]
+    Rf = rf.numpy().reshape(mx, nres, mz)
+    Rg = rg.numpy().reshape(mx, nres, mz)
+    # phase B: 2D (x, z) convolution of every owned y-residue (Function cconv2)
+    out = np.stack([implicit.cconv2d(Rf[:, q, :], Rg[:, q, :]) for q in range(nres)], axis=1)
+    send_back = torch.from_numpy(np.ascontiguousarray(out.reshape(world, nx, nres, mz)))
+    back = torch.empty_like(send_back)
+    dist.all_to_all_single(back.view(torch.float64), send_back.view(torch.float64))
+    # phase C: unpack residues of every source rank, fftpadForward along y
+    streams = np.concatenate([back.numpy()[p] for p in range(world)], axis=1)   # [x][2my][z]
+    e, o = streams[:, :my, :], streams[:, my:, :]
+    res = np.swapaxes(implicit.fftpad_forward(np.swapaxes(e, 1, 2), np.swapaxes(o, 1, 2)), 1, 2)
+    np.save(os.path.join(outdir, f"rank{rank}.npy"), res)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    rank, world, port = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
+    shape = tuple(int(x) for x in sys.argv[4].split(","))
+    run(rank, world, port, shape, sys.argv[5])
