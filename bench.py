@@ -68,17 +68,45 @@ def flops_cfft(n):      # 5 n log2 n per complex transform
 
 
 WORKLOADS = {
-    # name: dict(kind, m, batch, arrays, bytes per conv, flops per conv)
+    # name: parts, each one C-ABI call per step over its batch
     "c2": dict(desc="configs[1]: hconv1d m=4096 B=4096 + tconv1d m=4096 B=4096", parts=[
         dict(kind="hconv1d", m=4096, batch=4096, narr=2),
         dict(kind="tconv1d", m=4096, batch=4096, narr=3)]),
     "c1": dict(desc="configs[0]: cconv1d m=1024 B=32768", parts=[
         dict(kind="cconv1d", m=1024, batch=32768, narr=2)]),
+    "c3a": dict(desc="configs[2]: cconv2d 1024x1024", parts=[
+        dict(kind="cconv2d", m=(1024, 1024), batch=1, narr=2)]),
+    "c3b": dict(desc="configs[2]: cconv2d batch 64 x 256x256", parts=[
+        dict(kind="cconv2d", m=(256, 256), batch=64, narr=2)]),
+    "c4": dict(desc="configs[3]: hconv2d mx=my=2048 ((2mx-1) x my)", parts=[
+        dict(kind="hconv2d", m=(2048, 2048), batch=1, narr=2)]),
+    "c5a": dict(desc="configs[4]: cconv3d 512^3", parts=[
+        dict(kind="cconv3d", m=(512, 512, 512), batch=1, narr=2)]),
+    "c5b": dict(desc="configs[4]: hconv3d 512^3 modes ((2m-1)^2 x m)", parts=[
+        dict(kind="hconv3d", m=(512, 512, 512), batch=1, narr=2)]),
 }
 
 
+def shape_of(p):
+    m, k = p["m"], p["kind"]
+    if k.endswith("1d"):
+        return (p["batch"], m)
+    if k == "cconv2d":
+        return (p["batch"],) + tuple(m)
+    if k == "hconv2d":
+        return (2 * m[0] - 1, m[1])
+    if k == "cconv3d":
+        return tuple(m)
+    if k == "hconv3d":
+        return (2 * m[0] - 1, 2 * m[1] - 1, m[2])
+    raise ValueError(k)
+
+
 def part_model(p):
-    """Algorithmic HBM bytes and convention flops per convolution."""
+    """Algorithmic HBM bytes and convention flops per convolution:
+    bytes = the method's minimum traffic with one HBM round trip per dependent
+    phase and per-row work on chip; flops = 5 n log2 n per complex FFT(n),
+    2.5 n log2 n per real FFT(n), counted with the paper's transform counts."""
     m, kind = p["m"], p["kind"]
     if kind == "cconv1d":
         return 3 * W * m, 6 * flops_cfft(m)                 # 6 complex FFTs of size m (P:228)
@@ -86,6 +114,23 @@ def part_model(p):
         return 3 * W * m, 9 * flops_rfft(m)                 # 9 real FFTs of size m
     if kind == "tconv1d":
         return 4 * W * m, 8 * flops_rfft(2 * m)             # 8 real FFTs of size 2m
+    if kind == "cconv2d":
+        mx, my = m
+        fl = 6 * my * flops_cfft(mx) + 2 * mx * 6 * flops_cfft(my)
+        return 15 * W * mx * my, fl
+    if kind == "hconv2d":
+        mx, my = m
+        fl = 9 * my * flops_cfft(mx) + 3 * mx * 9 * flops_rfft(my)
+        return W * (3 * (2 * mx - 1) * my + 18 * mx * my), fl
+    if kind == "cconv3d":
+        mx, my, mz = m
+        fl = 6 * my * mz * flops_cfft(mx) + 2 * mx * (6 * mz * flops_cfft(my) + 2 * my * 6 * flops_cfft(mz))
+        return 15 * W * mx * my * mz, fl
+    if kind == "hconv3d":
+        mx, my, mz = m
+        ny = 2 * my - 1
+        fl = 9 * ny * mz * flops_cfft(mx) + 3 * mx * (9 * mz * flops_cfft(my) + 3 * my * 9 * flops_rfft(mz))
+        return W * (3 * (2 * mx - 1) * ny * mz + 18 * mx * ny * mz), fl
     raise ValueError(kind)
 
 
@@ -147,22 +192,46 @@ def dist_env():
 
 
 def make_inputs(idc, torch, p, rank, dev):
-    """Seeded device inputs for one part; item ids offset by rank (weak scaling)."""
-    m, B, narr = p["m"], p["batch"], p["narr"]
+    """Seeded device inputs for one part (the config's recipe, DESIGN.md "Input
+    recipe"); item ids offset by rank (weak scaling)."""
+    kind, B, narr = p["kind"], p["batch"], p["narr"]
+    shp = shape_of(p)
     arrs = []
     for role in range(narr):
-        a = torch.empty((B, m), dtype=torch.complex128, device=dev)
-        for b in range(B):
-            idc.fill_uniform(a[b], synthgen.array_id(role, rank * B + b), synthgen.SEED)
-        if p["kind"] != "cconv1d":
+        a = torch.empty(shp, dtype=torch.complex128, device=dev)
+        if kind.endswith("1d") or kind == "cconv2d":
+            for b in range(B):
+                idc.fill_uniform(a[b], synthgen.array_id(role, rank * B + b), synthgen.SEED)
+        else:
+            idc.fill_uniform(a, synthgen.array_id(role, rank), synthgen.SEED)
+        if kind in ("hconv1d", "tconv1d"):
             a[:, 0] = a[:, 0].real.to(torch.complex128)   # Im U_0 := 0 (config 2)
+        elif kind in ("hconv2d", "cconv3d", "hconv3d"):
+            axes = []
+            for d, n in enumerate(shp):
+                k = torch.arange(n, device=dev, dtype=torch.float64)
+                centered = (kind == "hconv2d" and d == 0) or (kind == "hconv3d" and d < 2)
+                if centered:
+                    k = k - (n - 1) // 2
+                axes.append(k)
+            k2 = sum((ax ** 2).reshape([-1 if i == j else 1 for i in range(len(shp))]) for j, ax in enumerate(axes))
+            a /= (1.0 + k2)
+            if kind == "hconv2d":                      # ky = 0 line conjugate-symmetric, U_00 real
+                c = (shp[0] - 1) // 2
+                a[:c, 0] = torch.conj(torch.flip(a[c + 1:, 0], dims=(0,)))
+                a[c, 0] = a[c, 0].real.to(torch.complex128)
+            elif kind == "hconv3d":                    # kz = 0 plane conjugate-symmetric
+                cx, cy = (shp[0] - 1) // 2, (shp[1] - 1) // 2
+                pl = a[:, :, 0]
+                pl[:cx, :] = torch.conj(torch.flip(pl[cx + 1:, :], dims=(0, 1)))
+                pl[cx, :cy] = torch.conj(torch.flip(pl[cx, cy + 1:], dims=(0,)))
+                pl[cx, cy] = pl[cx, cy].real.to(torch.complex128)
         arrs.append(a)
     return arrs
 
 
 def call(idc, p, arrs):
-    fn = {"cconv1d": idc.cconv1d, "hconv1d": idc.hconv1d, "tconv1d": idc.tconv1d}[p["kind"]]
-    return fn(*arrs)
+    return getattr(idc, p["kind"])(*arrs)
 
 
 # -------------------------------------------------------------- our arm ----
@@ -184,10 +253,13 @@ def run_ours(args):
     work = [[torch.empty_like(a) for a in arrs] for arrs in pristine]
     torch.cuda.synchronize()
 
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 2x L2
+
     def restore():
         for src, dst in zip(pristine, work):
             for s, d in zip(src, dst):
                 d.copy_(s)
+        flush.zero_()                                                  # cold L2 for every step
 
     clk = ClockSampler(local).__enter__()   # sample from warm-up through the timed loop
     time.sleep(0.3)
@@ -246,9 +318,10 @@ def run_ours(args):
     else:
         roof = {"bound": "alu", "achieved": d["fp64_tflops_alg"], "peak": pk["fp64_tflops"], "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["kernel"] = f"k_{d['kind'][:5]}_rows<{d['m']}>"
+    roof["kernel"] = d["kind"] + ("" if d["kind"].endswith("1d") else " (pencil + row kernels)")
     roof["hbm_frac"] = d["hbm_gbs_alg"] / pk["hbm_gbs"]
     roof["traffic"] = load_traffic(d["kind"], d["m"])
+    roof["units_per_launch"] = d["batch"]
     roof["peak_src"] = pk["hbm_src"] if roof["bound"] == "hbm" else \
         "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md); measured DFMA loop 34.2"
 
@@ -262,7 +335,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": wl["desc"], "parallelism": f"replicas{ws}",
-                       "l2": "inputs > L2 (0.5-0.75 GB per call), restored from pristine copies before each step",
+                       "l2": "L2 flushed (256 MB write) and inputs restored from pristine copies before every step",
                        "seed": synthgen.SEED},
             "parts": part_info, "roofline": roof, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "wall_s_timed_loop": t_wall,
@@ -281,7 +354,7 @@ def load_traffic(kind, m):
     """dram bytes per launch from the committed ncu --set full capture, if any."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return json.load(fh).get(f"{kind}:{m}")
+            return json.load(fh).get(f"{kind}:{m if isinstance(m, int) else 'x'.join(map(str, m))}")
     except Exception:
         return None
 

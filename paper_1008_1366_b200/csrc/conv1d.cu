@@ -93,19 +93,19 @@ k_cconv_rows(double2* __restrict__ f, double2* __restrict__ g, long nrows,
     for (int i = 0; i < E; ++i) S1[t + T * i] = cmul(S1[t + T * i], v[i]);
     // ---- r = 1 (zeta_{2m}^k shift)
 #pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = cmul(fr[t + T * i], __ldg(&tw2M[t + T * i]));
+    for (int i = 0; i < E; ++i) v[i] = cmul(fr[t + T * i], ldtw(&tw2M[t + T * i]));
     fft<M, E, +1>(v, t, xb, twM, sync);
 #pragma unroll
     for (int i = 0; i < E; ++i) S2[t + T * i] = v[i];
 #pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = cmul(gr[t + T * i], __ldg(&tw2M[t + T * i]));
+    for (int i = 0; i < E; ++i) v[i] = cmul(gr[t + T * i], ldtw(&tw2M[t + T * i]));
     fft<M, E, +1>(v, t, xb, twM, sync);
 #pragma unroll
     for (int i = 0; i < E; ++i) v[i] = cmul(S2[t + T * i], v[i]);
     // ---- forward transforms + recombination
     fft<M, E, -1>(v, t, xb, twM, sync);
 #pragma unroll
-    for (int i = 0; i < E; ++i) S2[t + T * i] = cmulc(v[i], __ldg(&tw2M[t + T * i]));
+    for (int i = 0; i < E; ++i) S2[t + T * i] = cmulc(v[i], ldtw(&tw2M[t + T * i]));
 #pragma unroll
     for (int i = 0; i < E; ++i) v[i] = S1[t + T * i];
     fft<M, E, -1>(v, t, xb, twM, sync);
@@ -169,7 +169,7 @@ k_hconv_rows(double2* __restrict__ f, double2* __restrict__ g, long nrows,
         if (k == 0) {
           v[i] = make_double2(fr[0].x, gr[0].x);
         } else {
-          const double2 tz = __ldg(&tw3M[k]);
+          const double2 tz = ldtw(&tw3M[k]);
           const double2 zr = r == 0 ? make_double2(1.0, 0.0) : (r > 0 ? tz : cconj(tz));
           v[i] = herm_pair(fr[k], gr[k], fr[M - k], gr[M - k], zr, c);
         }
@@ -180,7 +180,7 @@ k_hconv_rows(double2* __restrict__ f, double2* __restrict__ g, long nrows,
         for (int i = 0; i < E; ++i) v[i] = make_double2(v[i].x * v[i].y, 0.0);
         fft<M, E, -1>(v, t, xb, twM, sync);
 #pragma unroll
-        for (int i = 0; i < E; ++i) ACC[t + T * i] = cmul(v[i], __ldg(&tw3M[t + T * i]));  // zeta_{3m}^{+k} P_{-1}
+        for (int i = 0; i < E; ++i) ACC[t + T * i] = cmul(v[i], ldtw(&tw3M[t + T * i]));  // zeta_{3m}^{+k} P_{-1}
       } else if (r == 0) {
 #pragma unroll
         for (int i = 0; i < E; ++i) P0[t + T * i] = v[i].x * v[i].y;
@@ -205,7 +205,7 @@ k_hconv_rows(double2* __restrict__ f, double2* __restrict__ g, long nrows,
             const double2 p0 = cscale(cadd(a, b), 0.5);
             const double2 d = csub(a, b);
             const double2 p1 = make_double2(0.5 * d.y, -0.5 * d.x);
-            const double2 h = cadd(cadd(ACC[k], p0), cmulc(p1, __ldg(&tw3M[k])));
+            const double2 h = cadd(cadd(ACC[k], p0), cmulc(p1, ldtw(&tw3M[k])));
             fw[k] = cscale(h, inv);
           }
         }
@@ -259,7 +259,7 @@ k_tconv_rows(double2* __restrict__ f, double2* __restrict__ g, double2* __restri
         for (int i = 0; i < E; ++i) {
           const int k = t + T * i;
           if (k == 0) v[i] = make_double2(fr[0].x, gr[0].x);
-          else v[i] = herm_pair(fr[k], gr[k], fr[M - k], gr[M - k], __ldg(&tw4M[r * k]), c);
+          else v[i] = herm_pair(fr[k], gr[k], fr[M - k], gr[M - k], ldtw(&tw4M[r * k]), c);
         }
         fft<M, E, +1>(v, t, xb, twM, sync);
 #pragma unroll
@@ -281,8 +281,8 @@ k_tconv_rows(double2* __restrict__ f, double2* __restrict__ g, double2* __restri
             v[i] = make_double2(hr[0].x, hr[0].x);
           } else {
             const double2 hk = hr[k], hm = cconj(hr[M - k]);
-            const double2 w0 = cmul(__ldg(&tw4M[r * k]), cadd(hk, cmul(c0, hm)));
-            const double2 w1 = cmul(__ldg(&tw4M[(r + 1) * k]), cadd(hk, cmul(c1, hm)));
+            const double2 w0 = cmul(ldtw(&tw4M[r * k]), cadd(hk, cmul(c0, hm)));
+            const double2 w1 = cmul(ldtw(&tw4M[(r + 1) * k]), cadd(hk, cmul(c1, hm)));
             v[i] = make_double2(w0.x - w1.y, w0.y + w1.x);
           }
         }
@@ -308,7 +308,7 @@ k_tconv_rows(double2* __restrict__ f, double2* __restrict__ g, double2* __restri
         const double2 p0 = cscale(cadd(a, b), 0.5);
         const double2 d = csub(a, b);
         const double2 p1 = make_double2(0.5 * d.y, -0.5 * d.x);
-        const double2 contrib = cadd(cmulc(p0, __ldg(&tw4M[r0 * k])), cmulc(p1, __ldg(&tw4M[(r0 + 1) * k])));
+        const double2 contrib = cadd(cmulc(p0, ldtw(&tw4M[r0 * k])), cmulc(p1, ldtw(&tw4M[(r0 + 1) * k])));
         ACC[k] = r0 == 0 ? contrib : cadd(ACC[k], contrib);
       }
     }

@@ -43,18 +43,16 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
 // Twiddle-table load.  Volatile so the compiler cannot hoist the (loop
 // invariant) table reads of every pass of every transform to the top of the
 // row loop and keep them all live -- that costs ~90 registers per thread.
-#ifndef IDC_TW_NC
-#define IDC_TW_NC 1
-#endif
+// Per-element table loads (zeta_{qm}^{rk} of the residue split / recombination):
+// coherent loads, so ptxas cannot hoist these loop-invariant reads out of a
+// row loop and hold E x (#residues) complex values live (~200 registers).
 __device__ __forceinline__ double2 ldtw(const double2* p) {
-#if IDC_TW_NC
-  return __ldg(p);   // read-only path; ptxas may hoist and keep twiddles in registers
-#else
   double2 r;
   asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
-#endif
 }
+// Stockham pass twiddles: read-only path (few per pass, kept in registers).
+__device__ __forceinline__ double2 ldtw_pass(const double2* p) { return __ldg(p); }
 // Data load that the compiler may not merge with an earlier load of the same
 // address (the residue loops re-read the row; keeping the first read live
 // across transforms would cost 4 registers per element).  L1-cached.
@@ -178,10 +176,22 @@ __device__ __forceinline__ void pass_compute(double2 (&v)[E], int t, const doubl
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r] = v[b + r * B];
     if constexpr (NS > 1) {
+      // w^r, w = exp(2 pi i jm/(NS R)), r = Q a + c: load w^c (c < Q) and
+      // w^{Qa} (a < R/Q), one complex product for the mixed terms
       const int jm = (t + T * b) & (NS - 1);
       constexpr int STEP = N / (NS * R);
+      constexpr int Q = R >= 16 ? 4 : (R >= 4 ? 2 : 1);
+      double2 lo[Q], hi[R / Q];
 #pragma unroll
-      for (int r = 1; r < R; ++r) x[r] = cmul_dir<SIGN>(x[r], ldtw(&tw[r * jm * STEP]));
+      for (int c = 1; c < Q; ++c) lo[c] = ldtw_pass(&tw[c * jm * STEP]);
+#pragma unroll
+      for (int a = 1; a < R / Q; ++a) hi[a] = ldtw_pass(&tw[Q * a * jm * STEP]);
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const int a = r / Q, c = r % Q;
+        const double2 w = a == 0 ? lo[c] : (c == 0 ? hi[a] : cmul(hi[a], lo[c]));
+        x[r] = cmul_dir<SIGN>(x[r], w);
+      }
     }
     dft<R, SIGN>(x);
 #pragma unroll

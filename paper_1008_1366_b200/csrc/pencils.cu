@@ -68,7 +68,7 @@ k_pad_bwd(double2* __restrict__ f, double2* __restrict__ g, double2* __restrict_
   for (int i = 0; i < E; ++i) x0[i] = ok ? a[(long)(t + T * i) * pc.ncols] : make_double2(0, 0);
   // odd stream u_{2l+1} = sum_k zeta_m^{lk} zeta_{2m}^k U_k  (Eq. cconv1backward)
 #pragma unroll
-  for (int i = 0; i < E; ++i) v[i] = cmul(x0[i], __ldg(&tw2N[t + T * i]));
+  for (int i = 0; i < E; ++i) v[i] = cmul(x0[i], ldtw(&tw2N[t + T * i]));
   fft<N, E, +1>(v, t, smem, twN, CtaSync{}, xs);
   if (ok) {
 #pragma unroll
@@ -101,7 +101,7 @@ k_pad_fwd(double2* __restrict__ f, const double2* __restrict__ U, Pencil pc, con
   for (int i = 0; i < E; ++i) v[i] = ok ? u[(long)(t + T * i) * pc.ncols] : make_double2(0, 0);
   fft<N, E, -1>(v, t, smem, twN, CtaSync{}, xs);
 #pragma unroll
-  for (int i = 0; i < E; ++i) s[i] = cmulc(v[i], __ldg(&tw2N[t + T * i]));  // zeta_{2m}^{-k} U_k
+  for (int i = 0; i < E; ++i) s[i] = cmulc(v[i], ldtw(&tw2N[t + T * i]));  // zeta_{2m}^{-k} U_k
 #pragma unroll
   for (int i = 0; i < E; ++i) v[i] = ok ? a[(long)(t + T * i) * pc.ncols] : make_double2(0, 0);
   fft<N, E, -1>(v, t, smem, twN, CtaSync{}, xs);
@@ -146,7 +146,7 @@ k_pad0_bwd(double2* __restrict__ f, double2* __restrict__ g, double2* __restrict
       if (k == 0) {
         v[i] = up[i];                                                      // w_{0,r} = U_0
       } else {
-        const double2 tz = __ldg(&tw3N[k]);
+        const double2 tz = ldtw(&tw3N[k]);
         const double2 zr = r == 0 ? make_double2(1, 0) : (r > 0 ? tz : cconj(tz));
         v[i] = cmul(zr, cadd(up[i], cmul(z3, un[i])));
       }
@@ -200,7 +200,7 @@ k_pad0_fwd(double2* __restrict__ f, const double2* __restrict__ U, Pencil pc, co
 #pragma unroll
     for (int i = 0; i < E; ++i) {
       const int k = t + T * i;
-      const double2 tz = __ldg(&tw3N[k]);
+      const double2 tz = ldtw(&tw3N[k]);
       const double2 zr = r == 0 ? make_double2(1, 0) : (r > 0 ? cconj(tz) : tz);  // zeta_{3m}^{-rk}
       const double2 p = cmul(zr, v[i]);
       if (rr == 0) {
