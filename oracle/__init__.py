@@ -69,6 +69,8 @@ def lib():
             "orc_cconv3d_at": [P, P, I, I, I, P, I, P],
             "orc_hconv3d_at": [P, P, I, I, I, P, I, P],
             "orc_hconv2d_at": [P, P, I, I, P, I, P],
+            "orc_hconv3d_at_mirror": [P, P, I, I, I, P, I, P],
+            "orc_cconv3d_at_par": [P, P, I, I, I, P, I, P],
         }.items():
             fn = getattr(_LIB, name)
             fn.argtypes = args
@@ -192,6 +194,28 @@ class direct:
         idx = np.ascontiguousarray(idx, dtype=np.int64)
         out = np.empty(idx.size, dtype=np.complex128)
         _check(lib().orc_hconv3d_at(_ptr(f), _ptr(g), mx, my, mz, _ptr(idx), idx.size, _ptr(out)), "hconv3d_at")
+        return out
+
+    @staticmethod
+    def hconv3d_at_large(f, g, idx):
+        """D7 at sampled outputs of a large array: mirror/projection on the fly
+        (no 8x extended copy), each point parallelised over px."""
+        f, g = _c(f), _c(g)
+        mx, my, mz = (f.shape[0] + 1) // 2, (f.shape[1] + 1) // 2, f.shape[2]
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        out = np.empty(idx.size, dtype=np.complex128)
+        _check(lib().orc_hconv3d_at_mirror(_ptr(f), _ptr(g), mx, my, mz, _ptr(idx), idx.size, _ptr(out)),
+               "hconv3d_at_large")
+        return out
+
+    @staticmethod
+    def cconv3d_at_large(f, g, idx):
+        """D6 at sampled outputs of a large array, each point parallelised."""
+        f, g = _c(f), _c(g)
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        out = np.empty(idx.size, dtype=np.complex128)
+        _check(lib().orc_cconv3d_at_par(_ptr(f), _ptr(g), *f.shape, _ptr(idx), idx.size, _ptr(out)),
+               "cconv3d_at_large")
         return out
 
     @staticmethod

@@ -304,3 +304,101 @@ int orc_hconv2d_at(const double *f, const double *g, int64_t mx, int64_t my,
   /* (2mx-1, my) == (2mx-1, 2*1-1, my): reuse the 3D routine with my_c = 1 */
   return orc_hconv3d_at(f, g, mx, 1, my, out_idx, nout, out);
 }
+
+/* D7 at sampled outputs without materialising the extended array (for the
+ * full-size config 5b, where the extension would take 17 GB): the mirror
+ * U_{-p} = conj(U_p) and the kz = 0 projection are evaluated on the fly. */
+static inline void herm_val(const double *A, int64_t mx, int64_t my, int64_t mz, int64_t px, int64_t py,
+                            int64_t pz, double *re, double *im) {
+  const int64_t ny = 2 * my - 1;
+  if (pz > 0) {
+    const double *a = A + 2 * (((px + mx - 1) * ny + (py + my - 1)) * mz + pz);
+    *re = a[0]; *im = a[1];
+  } else if (pz < 0) {
+    const double *a = A + 2 * (((-px + mx - 1) * ny + (-py + my - 1)) * mz - pz);
+    *re = a[0]; *im = -a[1];
+  } else {
+    const double *a = A + 2 * (((px + mx - 1) * ny + (py + my - 1)) * mz);
+    const double *b = A + 2 * (((-px + mx - 1) * ny + (-py + my - 1)) * mz);
+    *re = 0.5 * (a[0] + b[0]); *im = 0.5 * (a[1] - b[1]);
+  }
+}
+
+int orc_hconv3d_at_mirror(const double *f, const double *g, int64_t mx, int64_t my, int64_t mz,
+                          const int64_t *out_idx, int64_t nout, double *out) {
+  if (mx < 1 || my < 1 || mz < 1 || nout < 0) return -2;
+  int64_t ny = 2 * my - 1;
+  if (over_cap((double)(2 * mx - 1) * (double)ny * (double)(2 * mz - 1) * (double)nout)) return -1;
+  for (int64_t o = 0; o < nout; ++o) {
+    int64_t lin = out_idx[o];
+    int64_t i = lin / (ny * mz), j = (lin / mz) % ny, l = lin % mz;
+    int64_t kx = i - (mx - 1), ky = j - (my - 1), kz = l;
+    double sre = 0, sim = 0, cre = 0, cim = 0;
+    /* parallel over px; per-thread compensated partial sums, combined exactly-ish below */
+    int64_t nth = 2 * mx - 1;
+    double *part = (double *)calloc((size_t)nth * 4, sizeof(double));
+    if (!part) return -2;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t pxi = 0; pxi < nth; ++pxi) {
+      int64_t px = pxi - (mx - 1), qx = kx - px;
+      if (qx < -(mx - 1) || qx > mx - 1) continue;
+      cacc_t a = {{0, 0}, {0, 0}};
+      for (int64_t py = -(my - 1); py <= my - 1; ++py) {
+        int64_t qy = ky - py;
+        if (qy < -(my - 1) || qy > my - 1) continue;
+        int64_t pz0 = kz - (mz - 1) > -(mz - 1) ? kz - (mz - 1) : -(mz - 1);
+        for (int64_t pz = pz0; pz <= mz - 1; ++pz) {
+          double xr, xi, yr, yi;
+          herm_val(f, mx, my, mz, px, py, pz, &xr, &xi);
+          herm_val(g, mx, my, mz, qx, qy, kz - pz, &yr, &yi);
+          cacc_addmul(&a, xr, xi, yr, yi);
+        }
+      }
+      part[4 * pxi] = a.re.s; part[4 * pxi + 1] = a.re.c;
+      part[4 * pxi + 2] = a.im.s; part[4 * pxi + 3] = a.im.c;
+    }
+    acc_t R = {0, 0}, I = {0, 0};
+    for (int64_t t = 0; t < nth; ++t) {
+      acc_add(&R, part[4 * t]); acc_add(&R, part[4 * t + 1]);
+      acc_add(&I, part[4 * t + 2]); acc_add(&I, part[4 * t + 3]);
+    }
+    free(part);
+    (void)sre; (void)sim; (void)cre; (void)cim;
+    out[2 * o] = acc_val(&R);
+    out[2 * o + 1] = acc_val(&I);
+  }
+  return 0;
+}
+
+/* D6 at sampled outputs, parallel inside each point (for the 512^3 config). */
+int orc_cconv3d_at_par(const double *f, const double *g, int64_t n0, int64_t n1, int64_t n2,
+                       const int64_t *out_idx, int64_t nout, double *out) {
+  if (n0 < 1 || n1 < 1 || n2 < 1 || nout < 0) return -2;
+  if (over_cap((double)n0 * (double)n1 * (double)n2 * (double)nout)) return -1;
+  for (int64_t o = 0; o < nout; ++o) {
+    int64_t lin = out_idx[o];
+    int64_t i = lin / (n1 * n2), j = (lin / n2) % n1, l = lin % n2;
+    double *part = (double *)calloc((size_t)(i + 1) * 4, sizeof(double));
+    if (!part) return -2;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t p = 0; p <= i; ++p) {
+      cacc_t a = {{0, 0}, {0, 0}};
+      for (int64_t q = 0; q <= j; ++q)
+        for (int64_t r = 0; r <= l; ++r) {
+          const double *F = f + 2 * ((p * n1 + q) * n2 + r);
+          const double *G = g + 2 * (((i - p) * n1 + (j - q)) * n2 + (l - r));
+          cacc_addmul(&a, F[0], F[1], G[0], G[1]);
+        }
+      part[4 * p] = a.re.s; part[4 * p + 1] = a.re.c; part[4 * p + 2] = a.im.s; part[4 * p + 3] = a.im.c;
+    }
+    acc_t R = {0, 0}, I = {0, 0};
+    for (int64_t t = 0; t <= i; ++t) {
+      acc_add(&R, part[4 * t]); acc_add(&R, part[4 * t + 1]);
+      acc_add(&I, part[4 * t + 2]); acc_add(&I, part[4 * t + 3]);
+    }
+    free(part);
+    out[2 * o] = acc_val(&R);
+    out[2 * o + 1] = acc_val(&I);
+  }
+  return 0;
+}

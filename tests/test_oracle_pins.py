@@ -430,3 +430,19 @@ def test_memory_formulas():
     rhs = 12 * m ** 3 - 6 * m * m + 2 * m * m + m + 2
     assert rhs == mw["hconv3d_512x512x512"]
     assert oracle.memory.hconv3d_implicit(m, m, m) - rhs == 2 * m
+
+
+def test_large_sampled_oracles_agree(rng):
+    """The mirror-on-the-fly / parallel sampled routines equal the plain ones."""
+    f, g = synthgen.hconv3d_inputs(4, 3, 5)
+    idx = np.arange(f.size)
+    assert rel_l2(direct.hconv3d_at_large(f, g, idx), direct.hconv3d_at(f, g, idx)) < 1e-15
+    a, b = crand(rng, 5, 4, 6), crand(rng, 5, 4, 6)
+    idx = np.arange(a.size)
+    assert rel_l2(direct.cconv3d_at_large(a, b, idx), direct.cconv_nd_at(a, b, idx)) < 1e-15
+
+
+def test_fast_generator_bitwise():
+    for aid, start, n in [(0, 0, 1000), (9, 77, 5000)]:
+        assert np.array_equal(synthgen.uniform_complex_fast(n, aid, start=start),
+                              synthgen.uniform_complex(n, aid, start=start))

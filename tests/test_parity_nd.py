@@ -146,3 +146,35 @@ def test_config4_hconv2d_2048(idc):
     idx = sample_idx((2 * mx - 1, my), 24, origin=(mx - 1, 0))
     out = F.cpu().numpy().reshape(-1)[idx]
     assert rel_l2(out, direct.hconv2d_at(f, g, idx)) < TOL
+
+
+def test_config5a_cconv3d_512(idc):
+    """C5a at full size (512^3, scaled 1/(1+|k|^2)); sampled outputs vs direct sums."""
+    m = 512
+    f, g = synthgen.cconv3d_inputs(m, m, m)
+    F, G = dev(f), dev(g)
+    idc.cconv3d(F, G)
+    idx = sample_idx((m, m, m), 6, origin=(0, 0, 0))
+    out = F.cpu().numpy().reshape(-1)[idx]
+    del F, G
+    torch.cuda.empty_cache()
+    assert rel_l2(out, direct.cconv3d_at_large(f, g, idx)) < TOL
+
+
+def test_config5b_hconv3d_512(idc):
+    """C5b at full size ((2*512-1)^2 x 512 Hermitian, scaled); sampled outputs."""
+    m = 512
+    f, g = synthgen.hconv3d_inputs(m, m, m)
+    F, G = dev(f), dev(g)
+    idc.hconv3d(F, G)
+    shape = f.shape
+    rs = np.random.default_rng(5)
+    idx = np.unique(np.concatenate([
+        [np.ravel_multi_index((m - 1, m - 1, 0), shape), np.ravel_multi_index((m - 1, m - 1, 1), shape),
+         np.ravel_multi_index((m, m - 2, 0), shape), np.ravel_multi_index((0, 0, 0), shape),
+         np.ravel_multi_index((2 * m - 2, 2 * m - 2, m - 1), shape)],
+        rs.choice(f.size, 3, replace=False)]).astype(np.int64))
+    out = F.cpu().numpy().reshape(-1)[idx]
+    del F, G
+    torch.cuda.empty_cache()
+    assert rel_l2(out, direct.hconv3d_at_large(f, g, idx)) < TOL
