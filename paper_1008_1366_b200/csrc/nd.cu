@@ -16,6 +16,7 @@
 // (SURVEY §8(a) a9), so only the slab read and the slab result write reach
 // HBM.  All launches are stream-ordered on the caller's stream.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "nd.cuh"
@@ -37,10 +38,38 @@ size_t l2_bytes() {
   return (size_t)l2;
 }
 
-// slabs per group: keep f/g slabs + U2/V2 of a group within ~half of L2
+// slabs per group: keep f/g slabs + U2/V2 of a group within a fraction of L2
+// (IDC_SLAB_L2_FRAC, percent, default 50; experiments only)
 long slab_group(size_t slab_bytes_all, long nslabs) {
-  long G = (long)((l2_bytes() / 2) / std::max<size_t>(slab_bytes_all, 1));
+  static long frac = -1;
+  if (frac < 0) {
+    const char* e = getenv("IDC_SLAB_L2_FRAC");
+    frac = e ? atol(e) : 50;
+  }
+  long G = (long)((l2_bytes() * frac / 100) / std::max<size_t>(slab_bytes_all, 1));
   return std::max<long>(1, std::min<long>(G, nslabs));
+}
+// Internal stream pool for concurrent slab groups (created once per device).
+constexpr int kSlabStreams = 4;
+struct Pool {
+  cudaStream_t s[kSlabStreams];
+  cudaEvent_t fork, done[kSlabStreams];
+  bool ok = false;
+};
+Pool& pool() {
+  static Pool p[16];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Pool& q = p[dev & 15];
+  if (!q.ok) {
+    for (int i = 0; i < kSlabStreams; ++i) {
+      cudaStreamCreateWithFlags(&q.s[i], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&q.done[i], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&q.fork, cudaEventDisableTiming);
+    q.ok = true;
+  }
+  return q;
 }
 }  // namespace
 
@@ -53,20 +82,24 @@ size_t hconv2d_work_bytes(size_t mx, size_t my) {
   if (!pow2ok(mx) || !pow2ok(my)) return 0;
   return 2 * (mx + 1) * my * W16 + hconv_rows_work_bytes((int)my);
 }
-static long c3_group(size_t mx, size_t my, size_t mz) { return slab_group(4 * my * mz * W16, 2 * (long)mx); }
+// slabs per group; kSlabStreams groups are in flight at once, so the L2
+// budget is shared between them
+static long c3_group(size_t mx, size_t my, size_t mz) {
+  return slab_group(kSlabStreams * 4 * my * mz * W16, 2 * (long)mx);
+}
 static long h3_group(size_t mx, size_t my, size_t mz) {
-  return slab_group(2 * ((2 * my - 1) + (my + 1)) * mz * W16, 3 * (long)mx);
+  return slab_group(kSlabStreams * 2 * ((2 * my - 1) + (my + 1)) * mz * W16, 3 * (long)mx);
 }
 size_t cconv3d_work_bytes(size_t mx, size_t my, size_t mz) {
   if (!pow2ok(mx) || !pow2ok(my) || !pow2ok(mz)) return 0;
   const long G = c3_group(mx, my, mz);
-  return 2 * mx * my * mz * W16 + 2 * (size_t)G * my * mz * W16 + cconv_rows_work_bytes((int)mz);
+  return 2 * mx * my * mz * W16 + kSlabStreams * (2 * (size_t)G * my * mz * W16 + cconv_rows_work_bytes((int)mz));
 }
 size_t hconv3d_work_bytes(size_t mx, size_t my, size_t mz) {
   if (!pow2ok(mx) || !pow2ok(my) || !pow2ok(mz)) return 0;
   const long G = h3_group(mx, my, mz);
-  return 2 * (mx + 1) * (2 * my - 1) * mz * W16 + 2 * (size_t)G * (my + 1) * mz * W16 +
-         hconv_rows_work_bytes((int)mz);
+  return 2 * (mx + 1) * (2 * my - 1) * mz * W16 +
+         kSlabStreams * (2 * (size_t)G * (my + 1) * mz * W16 + hconv_rows_work_bytes((int)mz));
 }
 
 // ------------------------------------------------------------------- 2D --
@@ -103,23 +136,34 @@ cudaError_t run_cconv3d(double2* f, double2* g, int mx, int my, int mz, double2*
   const long G = c3_group(mx, my, mz);
   double2* U = work;
   double2* V = U + n;
-  double2* U2 = V + n;
-  double2* V2 = U2 + G * slab;
-  double2* rw = V2 + G * slab;
+  double2* per = V + n;                                    // kSlabStreams x (U2, V2, row work)
+  const long per_elems = 2 * G * slab + (long)(cconv_rows_work_bytes(mz) / W16);
   IDC_TRY(launch_pad_bwd(f, g, U, V, mx, slab, 1, 0, 0, s));              // x: fftpadBackward over all (y,z)
+  Pool& P = pool();
+  IDC_TRY(cudaEventRecord(P.fork, s));
+  for (int i = 0; i < kSlabStreams; ++i) IDC_TRY(cudaStreamWaitEvent(P.s[i], P.fork, 0));
+  long gi = 0;
   for (int half = 0; half < 2; ++half) {                                   // x-residue slabs: f (even), U (odd)
     double2* A = half == 0 ? f : U;
     double2* B = half == 0 ? g : V;
-    for (long s0 = 0; s0 < mx; s0 += G) {
+    for (long s0 = 0; s0 < mx; s0 += G, ++gi) {
       const long gs = std::min<long>(G, mx - s0);
+      cudaStream_t st = P.s[gi % kSlabStreams];
+      double2* U2 = per + (gi % kSlabStreams) * per_elems;
+      double2* V2 = U2 + G * slab;
+      double2* rw = V2 + G * slab;
       double2* a = A + s0 * slab;
       double2* b = B + s0 * slab;
-      // cconv2 on the group's slabs, reusing U2/V2
-      IDC_TRY(launch_pad_bwd(a, b, U2, V2, my, mz, gs, slab, slab, s));
-      IDC_TRY(launch_cconv_rows(a, b, mz, gs * my, rw, s));
-      IDC_TRY(launch_cconv_rows(U2, V2, mz, gs * my, rw, s));
-      IDC_TRY(launch_pad_fwd(a, U2, my, mz, gs, slab, slab, s));
+      // cconv2 on the group's slabs, reusing this stream's U2/V2
+      IDC_TRY(launch_pad_bwd(a, b, U2, V2, my, mz, gs, slab, slab, st));
+      IDC_TRY(launch_cconv_rows(a, b, mz, gs * my, rw, st));
+      IDC_TRY(launch_cconv_rows(U2, V2, mz, gs * my, rw, st));
+      IDC_TRY(launch_pad_fwd(a, U2, my, mz, gs, slab, slab, st));
     }
+  }
+  for (int i = 0; i < kSlabStreams; ++i) {
+    IDC_TRY(cudaEventRecord(P.done[i], P.s[i]));
+    IDC_TRY(cudaStreamWaitEvent(s, P.done[i], 0));
   }
   return launch_pad_fwd(f, U, mx, slab, 1, 0, 0, s);                     // x: fftpadForward
 }
@@ -130,24 +174,35 @@ cudaError_t run_hconv3d(double2* f, double2* g, int mx, int my, int mz, double2*
   const long G = h3_group(mx, my, mz);
   double2* U = work;                                // (mx+1) slabs
   double2* V = U + (long)(mx + 1) * slab;
-  double2* U2 = V + (long)(mx + 1) * slab;
-  double2* V2 = U2 + G * uslab;
-  double2* rw = V2 + G * uslab;
+  double2* per = V + (long)(mx + 1) * slab;
+  const long per_elems = 2 * G * uslab + (long)(hconv_rows_work_bytes(mz) / W16);
   IDC_TRY(launch_pad0_bwd(f, g, U, V, mx, slab, 1, 0, 0, s));             // x: fft0padBackward
+  Pool& P = pool();
+  IDC_TRY(cudaEventRecord(P.fork, s));
+  for (int i = 0; i < kSlabStreams; ++i) IDC_TRY(cudaStreamWaitEvent(P.s[i], P.fork, 0));
+  long gi = 0;
   for (int half = 0; half < 2; ++half) {                                   // slabs: 2mx-1 in f, mx+1 in U
     double2* A = half == 0 ? f : U;
     double2* B = half == 0 ? g : V;
     const long ns = half == 0 ? 2L * mx - 1 : (long)mx + 1;
-    for (long s0 = 0; s0 < ns; s0 += G) {
+    for (long s0 = 0; s0 < ns; s0 += G, ++gi) {
       const long gs = std::min<long>(G, ns - s0);
+      cudaStream_t st = P.s[gi % kSlabStreams];
+      double2* U2 = per + (gi % kSlabStreams) * per_elems;
+      double2* V2 = U2 + G * uslab;
+      double2* rw = V2 + G * uslab;
       double2* a = A + s0 * slab;
       double2* b = B + s0 * slab;
-      // conv2 on the group's slabs, reusing U2/V2
-      IDC_TRY(launch_pad0_bwd(a, b, U2, V2, my, mz, gs, slab, uslab, s));
-      IDC_TRY(launch_hconv_rows(a, b, mz, gs * (2L * my - 1), rw, s));
-      IDC_TRY(launch_hconv_rows(U2, V2, mz, gs * ((long)my + 1), rw, s));
-      IDC_TRY(launch_pad0_fwd(a, U2, my, mz, gs, slab, uslab, s));
+      // conv2 on the group's slabs, reusing this stream's U2/V2
+      IDC_TRY(launch_pad0_bwd(a, b, U2, V2, my, mz, gs, slab, uslab, st));
+      IDC_TRY(launch_hconv_rows(a, b, mz, gs * (2L * my - 1), rw, st));
+      IDC_TRY(launch_hconv_rows(U2, V2, mz, gs * ((long)my + 1), rw, st));
+      IDC_TRY(launch_pad0_fwd(a, U2, my, mz, gs, slab, uslab, st));
     }
+  }
+  for (int i = 0; i < kSlabStreams; ++i) {
+    IDC_TRY(cudaEventRecord(P.done[i], P.s[i]));
+    IDC_TRY(cudaStreamWaitEvent(s, P.done[i], 0));
   }
   return launch_pad0_fwd(f, U, mx, slab, 1, 0, 0, s);                    // x: fft0padForward
 }
