@@ -404,6 +404,9 @@ size_t stash_bytes() {
     default: break;                      \
   }
 
+#ifndef IDC_V3_MIN_M
+#define IDC_V3_MIN_M 512
+#endif
 #ifndef IDC_V2_MAX_M
 #define IDC_V2_MAX_M 4096
 #endif
@@ -427,12 +430,28 @@ cudaError_t launch_cconv_rows(double2* f, double2* g, int m, long nrows, double2
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_hconv_rows(double2* f, double2* g, int m, long nrows, double2* work, cudaStream_t s) {
+  if (m >= IDC_V3_MIN_M && m <= 4096) {
+    switch (m) {
+      case 512: return hconv_rows3<512>(f, g, nrows, s);
+      case 1024: return hconv_rows3<1024>(f, g, nrows, s);
+      case 2048: return hconv_rows3<2048>(f, g, nrows, s);
+      case 4096: return hconv_rows3<4096>(f, g, nrows, s);
+    }
+  }
   if (m <= IDC_V2_MAX_M) { IDC_DISPATCH_M(m, return hconv_rows2<MM>(f, g, nrows, s)); }
   IDC_DISPATCH_M(m, return hconv_m<MM>(f, g, nrows, work, s));
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_tconv_rows(double2* f, double2* g, double2* h, int m, long nrows, double2* work,
                               cudaStream_t s) {
+  if (m >= IDC_V3_MIN_M && m <= 4096) {
+    switch (m) {
+      case 512: return tconv_rows3<512>(f, g, h, nrows, s);
+      case 1024: return tconv_rows3<1024>(f, g, h, nrows, s);
+      case 2048: return tconv_rows3<2048>(f, g, h, nrows, s);
+      case 4096: return tconv_rows3<4096>(f, g, h, nrows, s);
+    }
+  }
   if (m <= IDC_V2_MAX_M) { IDC_DISPATCH_M(m, return tconv_rows2<MM>(f, g, h, nrows, s)); }
   IDC_DISPATCH_M(m, return tconv_m<MM>(f, g, h, nrows, work, s));
   return cudaErrorInvalidValue;

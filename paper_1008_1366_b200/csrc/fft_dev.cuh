@@ -51,8 +51,14 @@ __device__ __forceinline__ double2 ldtw(const double2* p) {
   asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
 }
-// Stockham pass twiddles: read-only path (few per pass, kept in registers).
+// Stockham pass twiddles: read-only path (few per pass; ptxas keeps them in
+// registers across the row loop) unless a unit defines IDC_PASS_TW_COHERENT
+// (reloaded per pass from L1: fewer registers, more L1 traffic).
+#ifdef IDC_PASS_TW_COHERENT
+__device__ __forceinline__ double2 ldtw_pass(const double2* p) { return ldtw(p); }
+#else
 __device__ __forceinline__ double2 ldtw_pass(const double2* p) { return __ldg(p); }
+#endif
 // Data load that the compiler may not merge with an earlier load of the same
 // address (the residue loops re-read the row; keeping the first read live
 // across transforms would cost 4 registers per element).  L1-cached.

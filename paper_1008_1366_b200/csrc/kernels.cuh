@@ -27,6 +27,10 @@ template <int M> cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cud
 template <int M> cudaError_t hconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s);
 template <int M> cudaError_t tconv_rows2(double2* f, double2* g, double2* h, long nrows, cudaStream_t s);
 
+// TMA-staged Hermitian / ternary variants (rows3.cu), 512 <= m <= 4096.
+template <int M> cudaError_t hconv_rows3(double2* f, double2* g, long nrows, cudaStream_t s);
+template <int M> cudaError_t tconv_rows3(double2* f, double2* g, double2* h, long nrows, cudaStream_t s);
+
 // Number of SMs of the current device (cached).
 int num_sms();
 

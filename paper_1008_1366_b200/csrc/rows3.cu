@@ -1,0 +1,303 @@
+// rows3.cu -- Hermitian / ternary 1D row convolutions with TMA-staged rows.
+//
+// Same equations as conv1d.cu / rows2.cu (K3: centered Hermitian with three
+// residues; K4: ternary with four residues, P:1007-1034 and
+// DESIGN.md "tconv with four residues").  What changes is the data flow:
+//
+//   * each row group stages its f and g rows in shared memory with one TMA
+//     bulk copy per row (cp.async.bulk + mbarrier), so the residue split
+//     w_{k,r} = zeta^{rk}(U_k + c_r conj U_{m-k}) reads U_k and the mirror
+//     U_{m-k} from shared memory instead of re-reading L2 once per residue;
+//   * as soon as the last residue split of a row has read the staged row the
+//     group issues the bulk copy of its NEXT row, which then lands while the
+//     remaining transforms of the current row run;
+//   * the cross-transform state (p0 and the packed (p0, p1) spectrum Q of
+//     hconv; the f*g stream products of tconv) lives in registers; tconv
+//     parks the first residue pair's partial sum in the (already staged)
+//     global f row and finishes it with the second pair.
+#include "fft_dev.cuh"
+#include "kernels.cuh"
+#include "tables.cuh"
+#include "tma.cuh"
+
+namespace idc {
+
+namespace {
+
+template <int M>
+struct Cfg3 {
+  static constexpr int E = 16;
+  static constexpr int T = M / E;
+  static constexpr int G = T >= 256 ? 1 : 256 / T;     // row groups per CTA
+  static constexpr int THREADS = G * T;
+  static constexpr int XB = xbuf_elems<M, E>() > M ? xbuf_elems<M, E>() : M;
+  static constexpr int PER = 2 * M + XB;              // staged f, g + exchange buffer (double2)
+  static constexpr size_t SMEM = (size_t)G * PER * 16 + (size_t)G * 16;  // + one mbarrier per group
+  static constexpr bool NAMED = G > 1;
+};
+
+template <bool NAMED>
+struct Sync3;
+template <>
+struct Sync3<true> {
+  int id, n;
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+};
+template <>
+struct Sync3<false> {
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync 0;" ::: "memory"); }
+};
+
+template <int M>
+__device__ __forceinline__ Sync3<Cfg3<M>::NAMED> sync3(int grp) {
+  if constexpr (Cfg3<M>::NAMED) return Sync3<true>{1 + grp, Cfg3<M>::T};
+  else return Sync3<false>{};
+}
+
+// packed residue stream of the staged pair (f, g) at k >= 1:
+// Z = zr (P_k + c R_{m-k}),  P = f_k + i g_k,  R = conj f_{m-k} + i conj g_{m-k}
+__device__ __forceinline__ double2 zpair(const double2* F, const double2* Gs, int k, int mk, double2 zr, double2 c) {
+  const double2 fk = F[k], gk = Gs[k], fm = F[mk], gm = Gs[mk];
+  const double2 P = make_double2(fk.x - gk.y, fk.y + gk.x);
+  const double2 R = make_double2(fm.x + gm.y, gm.x - fm.y);
+  return cmul(zr, cadd(P, cmul(c, R)));
+}
+
+}  // namespace
+
+// ====================================================================== K3 ==
+template <int M>
+__global__ void __launch_bounds__(Cfg3<M>::THREADS, 1)
+k_hconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, long nrows, const double2* __restrict__ twM,
+              const double2* __restrict__ tw3M) {
+  using C = Cfg3<M>;
+  constexpr int E = C::E, T = C::T, G = C::G;
+  extern __shared__ __align__(128) double2 smem[];
+  const int grp = threadIdx.x / T, t = threadIdx.x - grp * T;
+  double2* F = smem + grp * C::PER;
+  double2* Gs = F + M;
+  double2* xb = Gs + M;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G * C::PER) + grp;
+  const auto sync = sync3<M>(grp);
+  const long stride = (long)gridDim.x * G;
+  long row = (long)blockIdx.x * G + grp;
+  if (t == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (t == 0 && row < nrows) {
+    mbar_arrive_expect_tx(bar, 2u * M * 16u);
+    tma_load_1d(F, f + row * (long)M, M * 16u, bar);
+    tma_load_1d(Gs, g + row * (long)M, M * 16u, bar);
+  }
+  const double inv = 1.0 / (3.0 * M);
+  const double s3 = 0.86602540378443864676372317075294;  // sqrt(3)/2
+  uint32_t phase = 0;
+  for (; row < nrows; row += stride) {
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    double2 v[E], Q[E];
+    double p0[E];
+#pragma unroll
+    for (int rr = 0; rr < 3; ++rr) {
+      const int r = rr == 0 ? 0 : (rr == 1 ? 1 : -1);
+      const double2 c = make_double2(r == 0 ? 1.0 : -0.5, r == 0 ? 0.0 : (r < 0 ? s3 : -s3));  // zeta_3^{-r}
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int k = t + T * i;
+        if (k == 0) {
+          v[i] = make_double2(F[0].x, Gs[0].x);                  // w_{0,r} = Re U_0 (AMB-7)
+        } else {
+          const double2 tz = ldtw(&tw3M[k]);
+          const double2 zr = r == 0 ? make_double2(1.0, 0.0) : (r > 0 ? tz : cconj(tz));
+          v[i] = zpair(F, Gs, k, M - k, zr, c);
+        }
+      }
+      if (r == -1) {  // last read of the staged row: prefetch the next one
+        sync();
+        if (t == 0 && row + stride < nrows) {
+          mbar_arrive_expect_tx(bar, 2u * M * 16u);
+          tma_load_1d(F, f + (row + stride) * (long)M, M * 16u, bar);
+          tma_load_1d(Gs, g + (row + stride) * (long)M, M * 16u, bar);
+        }
+      }
+      fft<M, E, +1>(v, t, xb, twM, sync);                      // two c2r in one complex FFT
+      if (r == 0) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) p0[i] = v[i].x * v[i].y;
+      } else if (r == 1) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) Q[i] = make_double2(p0[i], v[i].x * v[i].y);
+        fft<M, E, -1>(Q, t, xb, twM, sync);
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) v[i] = make_double2(v[i].x * v[i].y, 0.0);
+        fft<M, E, -1>(v, t, xb, twM, sync);
+      }
+    }
+    // P_0, P_1 from Q via Q_{m-k}; 3m h_k = P_0 + zeta^{k} P_{-1} + zeta^{-k} P_1 (Eq. fft0forwardB)
+#pragma unroll
+    for (int i = 0; i < E; ++i) xb[t + T * i] = Q[i];
+    sync();
+    double2* fw = f + row * (long)M;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int k = t + T * i;
+      const double2 a = Q[i], b = cconj(xb[(M - k) & (M - 1)]);
+      const double2 tz = ldtw(&tw3M[k]);
+      const double2 pp0 = cscale(cadd(a, b), 0.5);
+      const double2 d = csub(a, b);
+      const double2 pp1 = make_double2(0.5 * d.y, -0.5 * d.x);
+      fw[k] = cscale(cadd(cadd(pp0, cmul(v[i], tz)), cmulc(pp1, tz)), inv);
+    }
+    sync();
+  }
+}
+
+// ====================================================================== K4 ==
+template <int M>
+__global__ void __launch_bounds__(Cfg3<M>::THREADS, 1)
+k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const double2* __restrict__ h, long nrows,
+              const double2* __restrict__ twM, const double2* __restrict__ tw4M) {
+  using C = Cfg3<M>;
+  constexpr int E = C::E, T = C::T, G = C::G;
+  extern __shared__ __align__(128) double2 smem[];
+  const int grp = threadIdx.x / T, t = threadIdx.x - grp * T;
+  double2* F = smem + grp * C::PER;
+  double2* Gs = F + M;
+  double2* xb = Gs + M;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G * C::PER) + grp;
+  const auto sync = sync3<M>(grp);
+  const long stride = (long)gridDim.x * G;
+  long row = (long)blockIdx.x * G + grp;
+  if (t == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (t == 0 && row < nrows) {
+    mbar_arrive_expect_tx(bar, 2u * M * 16u);
+    tma_load_1d(F, f + row * (long)M, M * 16u, bar);
+    tma_load_1d(Gs, g + row * (long)M, M * 16u, bar);
+  }
+  const double inv = 1.0 / (4.0 * M);
+  uint32_t phase = 0;
+  for (; row < nrows; row += stride) {
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    const double2* hr = h + row * (long)M;
+    double2* fw = f + row * (long)M;   // staged: free to serve as the partial-sum scratch
+    double2 v[E];
+    double a0[E], a1[E];
+#pragma unroll 1
+    for (int r0 = 0; r0 < 4; r0 += 2) {
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int r = r0 + s;
+        const double2 c = r == 0 ? make_double2(1, 0) : r == 1 ? make_double2(0, -1) : r == 2 ? make_double2(-1, 0)
+                                                                                    : make_double2(0, 1);  // (-i)^r
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int k = t + T * i;
+          if (k == 0) v[i] = make_double2(F[0].x, Gs[0].x);
+          else v[i] = zpair(F, Gs, k, M - k, ldtw(&tw4M[r * k]), c);
+        }
+        if (r == 3) {  // last read of the staged row: prefetch the next one
+          sync();
+          if (t == 0 && row + stride < nrows) {
+            mbar_arrive_expect_tx(bar, 2u * M * 16u);
+            tma_load_1d(F, f + (row + stride) * (long)M, M * 16u, bar);
+            tma_load_1d(Gs, g + (row + stride) * (long)M, M * 16u, bar);
+          }
+        }
+        fft<M, E, +1>(v, t, xb, twM, sync);
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          if (s == 0) a0[i] = v[i].x * v[i].y;
+          else a1[i] = v[i].x * v[i].y;
+        }
+      }
+      {  // h packed across the residue pair: w^h_r + i w^h_{r+1}
+        const double2 c0 = r0 == 0 ? make_double2(1, 0) : make_double2(-1, 0);
+        const double2 c1 = r0 == 0 ? make_double2(0, -1) : make_double2(0, 1);
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int k = t + T * i;
+          if (k == 0) {
+            const double h0 = ldv(&hr[0]).x;
+            v[i] = make_double2(h0, h0);
+          } else {
+            const double2 hk = ldv(&hr[k]), hm = cconj(ldv(&hr[M - k]));
+            const double2 w0 = cmul(ldtw(&tw4M[r0 * k]), cadd(hk, cmul(c0, hm)));
+            const double2 w1 = cmul(ldtw(&tw4M[(r0 + 1) * k]), cadd(hk, cmul(c1, hm)));
+            v[i] = make_double2(w0.x - w1.y, w0.y + w1.x);
+          }
+        }
+      }
+      fft<M, E, +1>(v, t, xb, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) v[i] = make_double2(a0[i] * v[i].x, a1[i] * v[i].y);
+      fft<M, E, -1>(v, t, xb, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) xb[t + T * i] = v[i];
+      sync();
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int k = t + T * i;
+        const double2 a = v[i], b = cconj(xb[(M - k) & (M - 1)]);
+        const double2 pp0 = cscale(cadd(a, b), 0.5);
+        const double2 d = csub(a, b);
+        const double2 pp1 = make_double2(0.5 * d.y, -0.5 * d.x);
+        const double2 ct = cadd(cmulc(pp0, ldtw(&tw4M[r0 * k])), cmulc(pp1, ldtw(&tw4M[(r0 + 1) * k])));
+        if (r0 == 0) fw[k] = ct;                                   // partial sum of residues 0, 1
+        else fw[k] = cscale(cadd(ldv(&fw[k]), ct), inv);           // + residues 2, 3, then 1/(4m)
+      }
+      sync();
+    }
+  }
+}
+
+// ================================================================ launchers ==
+namespace {
+template <class K>
+cudaError_t launch3(K kernel, int threads, size_t smem, long nrows, int groups, cudaStream_t s, void** args) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  long need = (nrows + groups - 1) / groups;
+  long grid = num_sms();
+  if (need < grid) grid = need;
+  if (grid < 1) grid = 1;
+  return cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s);
+}
+}  // namespace
+
+template <int M>
+cudaError_t hconv_rows3(double2* f, double2* g, long nrows, cudaStream_t s) {
+  using C = Cfg3<M>;
+  const double2* twM = zeta_table(M);
+  const double2* tw3M = zeta_table(3 * M);
+  if (!twM || !tw3M) return cudaErrorMemoryAllocation;
+  void* args[] = {&f, &g, &nrows, &twM, &tw3M};
+  return launch3(k_hconv_rows3<M>, C::THREADS, C::SMEM, nrows, C::G, s, args);
+}
+
+template <int M>
+cudaError_t tconv_rows3(double2* f, double2* g, double2* h, long nrows, cudaStream_t s) {
+  using C = Cfg3<M>;
+  const double2* twM = zeta_table(M);
+  const double2* tw4M = zeta_table(4 * M);
+  if (!twM || !tw4M) return cudaErrorMemoryAllocation;
+  void* args[] = {&f, &g, &h, &nrows, &twM, &tw4M};
+  return launch3(k_tconv_rows3<M>, C::THREADS, C::SMEM, nrows, C::G, s, args);
+}
+
+#define IDC_INST3(M)                                                                        \
+  template cudaError_t hconv_rows3<M>(double2*, double2*, long, cudaStream_t);              \
+  template cudaError_t tconv_rows3<M>(double2*, double2*, double2*, long, cudaStream_t);
+IDC_INST3(512)
+IDC_INST3(1024)
+IDC_INST3(2048)
+IDC_INST3(4096)
+
+}  // namespace idc
