@@ -18,4 +18,18 @@ cudaError_t launch_pad0_bwd(double2* f, double2* g, double2* U, double2* V, int 
 cudaError_t launch_pad0_fwd(double2* f, const double2* U, int m, long ncols, long batch, long bstride, long ustride,
                             cudaStream_t s);
 
+// TMA-staged persistent variants (pencils2.cu), 64 <= m <= 4096.
+template <int N>
+cudaError_t pad_bwd_tma(double2* f, double2* g, double2* U, double2* V, long ncols, long batch, long bstride,
+                        long ustride, cudaStream_t s);
+template <int N>
+cudaError_t pad_fwd_tma(double2* f, const double2* U, long ncols, long batch, long bstride, long ustride,
+                        cudaStream_t s);
+template <int N>
+cudaError_t pad0_bwd_tma(double2* f, double2* g, double2* U, double2* V, long ncols, long batch, long bstride,
+                         long ustride, cudaStream_t s);
+template <int N>
+cudaError_t pad0_fwd_tma(double2* f, const double2* U, long ncols, long batch, long bstride, long ustride,
+                         cudaStream_t s);
+
 }  // namespace idc

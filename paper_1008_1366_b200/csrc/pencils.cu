@@ -321,23 +321,42 @@ cudaError_t pad0_fwd_n(double2* f, const double2* U, long ncols, long batch, lon
     default: break;                                         \
   }
 
+#ifndef IDC_PENCIL_TMA
+#define IDC_PENCIL_TMA 1
+#endif
+#define IDC_TDISPATCH(m, ...)                                       \
+  if (IDC_PENCIL_TMA) switch (m) {                                  \
+      case 64: { constexpr int NN = 64; __VA_ARGS__; }              \
+      case 128: { constexpr int NN = 128; __VA_ARGS__; }            \
+      case 256: { constexpr int NN = 256; __VA_ARGS__; }            \
+      case 512: { constexpr int NN = 512; __VA_ARGS__; }            \
+      case 1024: { constexpr int NN = 1024; __VA_ARGS__; }          \
+      case 2048: { constexpr int NN = 2048; __VA_ARGS__; }          \
+      case 4096: { constexpr int NN = 4096; __VA_ARGS__; }          \
+      default: break;                                               \
+    }
+
 cudaError_t launch_pad_bwd(double2* f, double2* g, double2* U, double2* V, int m, long ncols, long batch,
                            long bstride, long ustride, cudaStream_t s) {
+  IDC_TDISPATCH(m, return pad_bwd_tma<NN>(f, g, U, V, ncols, batch, bstride, ustride, s));
   IDC_PDISPATCH(m, return pad_bwd_n<NN>(f, g, U, V, ncols, batch, bstride, ustride, s));
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_pad_fwd(double2* f, const double2* U, int m, long ncols, long batch, long bstride, long ustride,
                            cudaStream_t s) {
+  IDC_TDISPATCH(m, return pad_fwd_tma<NN>(f, U, ncols, batch, bstride, ustride, s));
   IDC_PDISPATCH(m, return pad_fwd_n<NN>(f, U, ncols, batch, bstride, ustride, s));
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_pad0_bwd(double2* f, double2* g, double2* U, double2* V, int m, long ncols, long batch,
                             long bstride, long ustride, cudaStream_t s) {
+  IDC_TDISPATCH(m, return pad0_bwd_tma<NN>(f, g, U, V, ncols, batch, bstride, ustride, s));
   IDC_PDISPATCH(m, return pad0_bwd_n<NN>(f, g, U, V, ncols, batch, bstride, ustride, s));
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_pad0_fwd(double2* f, const double2* U, int m, long ncols, long batch, long bstride, long ustride,
                             cudaStream_t s) {
+  IDC_TDISPATCH(m, return pad0_fwd_tma<NN>(f, U, ncols, batch, bstride, ustride, s));
   IDC_PDISPATCH(m, return pad0_fwd_n<NN>(f, U, ncols, batch, bstride, ustride, s));
   return cudaErrorInvalidValue;
 }

@@ -1,0 +1,522 @@
+// pencils2.cu -- TMA-staged persistent pencil kernels (K5-K8), 64 <= m <= 4096.
+//
+// Same transforms as pencils.cu (Procedures fftpadBackward / fftpadForward,
+// P:325-349; Eqs. fft0backwardA/B and fft0forward, AMB-1 stream
+// layout).  B200 data movement: one CTA per SM loops over W-column pencil
+// tiles; each tile is brought into shared memory by 3D TMA tensor loads
+// (cp.async.bulk.tensor, boxes of W columns x <= 256 rows, completion on an
+// mbarrier).  As soon as every thread has copied its part of a staged tile
+// into registers, one thread issues the TMA loads of the CTA's next tile,
+// so the HBM traffic of tile n+1 overlaps the FFTs and stores of tile n.
+// The stage is read as [row][column]: thread (c, t) = c + W*t takes rows
+// t + T*i of column c -- consecutive lanes read consecutive 16-byte words.
+#include <cuda.h>
+
+#include "fft_dev.cuh"
+#include "kernels.cuh"
+#include "nd_internal.cuh"
+#include "tables.cuh"
+#include "tma.cuh"
+#include "tmap.cuh"
+
+namespace idc {
+
+namespace {
+
+#ifndef IDC_PENCIL_E
+#define IDC_PENCIL_E 8
+#endif
+#ifndef IDC_PENCIL_THREADS
+#define IDC_PENCIL_THREADS 512
+#endif
+#ifndef IDC_PENCIL_MINB
+#define IDC_PENCIL_MINB 1
+#endif
+template <int N>
+struct TCfg {
+  static constexpr int E = IDC_PENCIL_E;
+  static constexpr int T = N / E;
+  static constexpr int W = IDC_PENCIL_THREADS / T < 1 ? 1 : (IDC_PENCIL_THREADS / T > 16 ? 16 : IDC_PENCIL_THREADS / T);
+  static constexpr int THREADS = T * W;
+  static constexpr int BR = N < 256 ? N : 256;                     // TMA box rows
+  static constexpr int XB = (xbuf_elems<N, E>() > 0 ? xbuf_elems<N, E>() : 1) * W;
+};
+
+template <int W>
+struct Slot2 {
+  int c;
+  __device__ __forceinline__ int operator()(int i) const { return i * W + c; }
+};
+
+struct Tiles {
+  long ncols, nct;      // columns per item, column tiles per item
+  long batch;           // items per input
+  long per_input;       // nct * batch
+  long ntiles;          // per_input * inputs
+  long bstride, ustride;
+};
+
+// tile index -> (input, batch item, first column); tile counts fit in 32 bits
+__device__ __forceinline__ void tile_coords(const Tiles& tl, long tau, int W, int& input, long& item, long& col0) {
+  const unsigned tt = (unsigned)tau, per = (unsigned)tl.per_input, nct = (unsigned)tl.nct;
+  const unsigned in = tt / per;
+  const unsigned rest = tt - in * per;
+  const unsigned it = rest / nct;
+  input = (int)in;
+  item = it;
+  col0 = (long)(rest - it * nct) * W;
+}
+
+// issue the TMA boxes covering rows [row0, row0 + nrows) of a tile into `stage`
+template <int W, int BR>
+__device__ __forceinline__ void load_rows(const CUtensorMap* map, double2* stage, long col0, int row0, int nrows,
+                                          long item, uint64_t* bar) {
+  for (int b = 0; b < nrows; b += BR)
+    tma_load_3d(stage + (long)b * W, map, (int)(2 * col0), row0 + b, (int)item, bar);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------- K5 --
+template <int N>
+__global__ void __launch_bounds__(TCfg<N>::THREADS, IDC_PENCIL_MINB)
+k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mg, double2* __restrict__ f,
+              double2* __restrict__ g, double2* __restrict__ U, double2* __restrict__ V, Tiles tl,
+              const double2* __restrict__ twN, const double2* __restrict__ tw2N) {
+  using C = TCfg<N>;
+  constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
+  extern __shared__ __align__(128) double2 smem[];
+  double2* stage = smem;                       // N x W
+  double2* xb = stage + N * W;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(xb + C::XB);
+  const int c = threadIdx.x % W, t = threadIdx.x / W;
+  const Slot2<W> xs{c};
+  constexpr uint32_t BYTES = (uint32_t)N * W * 16;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  long tau = blockIdx.x;
+  if (threadIdx.x == 0 && tau < tl.ntiles) {
+    int in; long item, col0;
+    tile_coords(tl, tau, W, in, item, col0);
+    mbar_arrive_expect_tx(bar, BYTES);
+    load_rows<W, BR>(in == 0 ? &mf : &mg, stage, col0, 0, N, item, bar);
+  }
+  uint32_t phase = 0;
+  for (; tau < tl.ntiles; tau += gridDim.x) {
+    int in; long item, col0;
+    tile_coords(tl, tau, W, in, item, col0);
+    const long col = col0 + c;
+    const bool ok = col < tl.ncols;
+    double2* a = (in == 0 ? f : g) + item * tl.bstride + (ok ? col : 0);
+    double2* u = (in == 0 ? U : V) + item * tl.ustride + (ok ? col : 0);
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    double2 x0[E], v[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) x0[i] = stage[(t + T * i) * W + c];
+    __syncthreads();
+    const long nx = tau + gridDim.x;
+    if (threadIdx.x == 0 && nx < tl.ntiles) {
+      int in2; long item2, c2;
+      tile_coords(tl, nx, W, in2, item2, c2);
+      mbar_arrive_expect_tx(bar, BYTES);
+      load_rows<W, BR>(in2 == 0 ? &mf : &mg, stage, c2, 0, N, item2, bar);
+    }
+    // odd stream u_{2l+1} = sum_k zeta_m^{lk} zeta_{2m}^k U_k  (Eq. cconv1backward)
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = cmul(x0[i], ldtw(&tw2N[t + T * i]));
+    fft<N, E, +1>(v, t, xb, twN, CtaSync{}, xs);
+    const long rs = (long)T * tl.ncols;   // pointer step between a thread's rows
+    if (ok) {
+      double2* p = u + (long)t * tl.ncols;
+#pragma unroll
+      for (int i = 0; i < E; ++i, p += rs) *p = v[i];
+    }
+    fft<N, E, +1>(x0, t, xb, twN, CtaSync{}, xs);   // even stream, in place
+    if (ok) {
+      double2* p = a + (long)t * tl.ncols;
+#pragma unroll
+      for (int i = 0; i < E; ++i, p += rs) *p = x0[i];
+    }
+  }
+}
+
+// ------------------------------------------------------------------- K6 --
+template <int N>
+__global__ void __launch_bounds__(TCfg<N>::THREADS, IDC_PENCIL_MINB)
+k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mu, double2* __restrict__ f,
+              Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw2N) {
+  using C = TCfg<N>;
+  constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
+  extern __shared__ __align__(128) double2 smem[];
+  double2* sf = smem;
+  double2* su = sf + N * W;
+  double2* xb = su + N * W;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xb + C::XB);   // [0] = f stage, [1] = U stage
+  const int c = threadIdx.x % W, t = threadIdx.x / W;
+  const Slot2<W> xs{c};
+  constexpr uint32_t BYTES = (uint32_t)N * W * 16;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  long tau = blockIdx.x;
+  if (threadIdx.x == 0 && tau < tl.ntiles) {
+    int in; long item, col0;
+    tile_coords(tl, tau, W, in, item, col0);
+    mbar_arrive_expect_tx(&bars[1], BYTES);
+    load_rows<W, BR>(&mu, su, col0, 0, N, item, &bars[1]);
+    mbar_arrive_expect_tx(&bars[0], BYTES);
+    load_rows<W, BR>(&mf, sf, col0, 0, N, item, &bars[0]);
+  }
+  const double inv = 1.0 / (2.0 * N);
+  uint32_t phase = 0;
+  for (; tau < tl.ntiles; tau += gridDim.x) {
+    int in; long item, col0;
+    tile_coords(tl, tau, W, in, item, col0);
+    const long col = col0 + c;
+    const bool ok = col < tl.ncols;
+    double2* a = f + item * tl.bstride + (ok ? col : 0);
+    const long nx = tau + gridDim.x;
+    int in2 = 0; long item2 = 0, c2 = 0;
+    if (nx < tl.ntiles) tile_coords(tl, nx, W, in2, item2, c2);
+    double2 v[E], s[E];
+    mbar_wait(&bars[1], phase);
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = su[(t + T * i) * W + c];
+    __syncthreads();
+    if (threadIdx.x == 0 && nx < tl.ntiles) {
+      mbar_arrive_expect_tx(&bars[1], BYTES);
+      load_rows<W, BR>(&mu, su, c2, 0, N, item2, &bars[1]);
+    }
+    fft<N, E, -1>(v, t, xb, twN, CtaSync{}, xs);
+#pragma unroll
+    for (int i = 0; i < E; ++i) s[i] = cmulc(v[i], ldtw(&tw2N[t + T * i]));   // zeta_{2m}^{-k} U_k
+    mbar_wait(&bars[0], phase);
+    phase ^= 1;
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = sf[(t + T * i) * W + c];
+    __syncthreads();
+    if (threadIdx.x == 0 && nx < tl.ntiles) {
+      mbar_arrive_expect_tx(&bars[0], BYTES);
+      load_rows<W, BR>(&mf, sf, c2, 0, N, item2, &bars[0]);
+    }
+    fft<N, E, -1>(v, t, xb, twN, CtaSync{}, xs);
+    if (ok) {
+      double2* p = a + (long)t * tl.ncols;
+      const long rs = (long)T * tl.ncols;
+#pragma unroll
+      for (int i = 0; i < E; ++i, p += rs) *p = cscale(cadd(v[i], s[i]), inv);
+    }
+  }
+}
+
+// ------------------------------------------------------------------- K7 --
+// Centered column of 2N-1 rows staged whole (2N rows of stage, last one
+// padding), three streams written as in pencils.cu.
+template <int N>
+__global__ void __launch_bounds__(TCfg<N>::THREADS, IDC_PENCIL_MINB)
+k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mg,
+               double2* __restrict__ f, double2* __restrict__ g, double2* __restrict__ U, double2* __restrict__ V,
+               Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw3N) {
+  using C = TCfg<N>;
+  constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
+  constexpr int R2 = ((2 * N - 1 + BR - 1) / BR) * BR;              // staged rows
+  extern __shared__ __align__(128) double2 smem[];
+  double2* stage = smem;                                            // R2 x W
+  double2* xb = stage + R2 * W;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(xb + C::XB);
+  const int c = threadIdx.x % W, t = threadIdx.x / W;
+  const Slot2<W> xs{c};
+  constexpr uint32_t BYTES = (uint32_t)R2 * W * 16;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  long tau = blockIdx.x;
+  if (threadIdx.x == 0 && tau < tl.ntiles) {
+    int in; long item, col0;
+    tile_coords(tl, tau, W, in, item, col0);
+    mbar_arrive_expect_tx(bar, BYTES);
+    load_rows<W, BR>(in == 0 ? &mf : &mg, stage, col0, 0, 2 * N - 1, item, bar);
+  }
+  const double s3 = 0.86602540378443864676372317075294;
+  uint32_t phase = 0;
+  for (; tau < tl.ntiles; tau += gridDim.x) {
+    int in; long item, col0;
+    tile_coords(tl, tau, W, in, item, col0);
+    const long col = col0 + c;
+    const bool ok = col < tl.ncols;
+    double2* a = (in == 0 ? f : g) + item * tl.bstride + (ok ? col : 0);
+    double2* u = (in == 0 ? U : V) + item * tl.ustride + (ok ? col : 0);
+    const long S = tl.ncols;
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    double2 up[E], un[E], v[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int k = t + T * i;
+      up[i] = stage[(N - 1 + k) * W + c];                              // U_k
+      un[i] = k > 0 ? stage[(k - 1) * W + c] : make_double2(0, 0);     // U_{k-m}
+    }
+    __syncthreads();
+    const long nx = tau + gridDim.x;
+    if (threadIdx.x == 0 && nx < tl.ntiles) {
+      int in2; long item2, c2;
+      tile_coords(tl, nx, W, in2, item2, c2);
+      mbar_arrive_expect_tx(bar, BYTES);
+      load_rows<W, BR>(in2 == 0 ? &mf : &mg, stage, c2, 0, 2 * N - 1, item2, bar);
+    }
+#pragma unroll 1
+    for (int rr = 0; rr < 3; ++rr) {
+      const int r = rr - 1;
+      const double2 z3 = make_double2(r == 0 ? 1.0 : -0.5, r == 0 ? 0.0 : (r < 0 ? s3 : -s3));  // zeta_3^{-r}
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int k = t + T * i;
+        if (k == 0) {
+          v[i] = up[i];
+        } else {
+          const double2 tz = ldtw(&tw3N[k]);
+          const double2 zr = r == 0 ? make_double2(1, 0) : (r > 0 ? tz : cconj(tz));
+          v[i] = cmul(zr, cadd(up[i], cmul(z3, un[i])));
+        }
+      }
+      fft<N, E, +1>(v, t, xb, twN, CtaSync{}, xs);
+      if (ok) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+          const int l = t + T * i;
+          double2* dst = r == 1 ? a + (long)(N - 1 + l) * S
+                       : r == -1 ? u + (long)l * S
+                                 : (l < N - 1 ? a + (long)l * S : u + (long)N * S);
+          *dst = v[i];
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------- K8 --
+// Streams staged one at a time (double buffered): q = 0 (r = -1: U rows
+// 0..N-1), q = 1 (r = 0: f rows 0..N-2 and U row N, the latter through a
+// one-row box into a separate tail slot), q = 2 (r = +1: f rows N-1..2N-2).
+template <int N>
+__global__ void __launch_bounds__(TCfg<N>::THREADS, IDC_PENCIL_MINB)
+k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mu,
+               const __grid_constant__ CUtensorMap mu1, double2* __restrict__ f, Tiles tl,
+               const double2* __restrict__ twN, const double2* __restrict__ tw3N) {
+  using C = TCfg<N>;
+  constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
+  extern __shared__ __align__(128) double2 smem[];
+  double2* st[2] = {smem, smem + N * W};
+  // one-row tail slots, 128-byte aligned (TMA tensor destinations): 16 double2 each
+  double2* tail[2] = {smem + 2 * N * W, smem + 2 * N * W + 16};
+  double2* xb = smem + 2 * N * W + 32;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xb + C::XB);
+  const int c = threadIdx.x % W, t = threadIdx.x / W;
+  const Slot2<W> xs{c};
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // stream q of tile tau -> buffer b
+  auto issue = [&](long tau, int q, int b) {
+    int in; long item, col0;
+    tile_coords(tl, tau, W, in, item, col0);
+    if (q == 0) {
+      mbar_arrive_expect_tx(&bars[b], (uint32_t)N * W * 16);
+      load_rows<W, BR>(&mu, st[b], col0, 0, N, item, &bars[b]);
+    } else if (q == 1) {
+      mbar_arrive_expect_tx(&bars[b], (uint32_t)N * W * 16 + (uint32_t)W * 16);
+      load_rows<W, BR>(&mf, st[b], col0, 0, N, item, &bars[b]);          // row N-1 unused (belongs to r = +1)
+      tma_load_3d(tail[b], &mu1, (int)(2 * col0), N, (int)item, &bars[b]);  // U row N = stream r = 0, l = N-1
+    } else {
+      mbar_arrive_expect_tx(&bars[b], (uint32_t)N * W * 16);
+      load_rows<W, BR>(&mf, st[b], col0, N - 1, N, item, &bars[b]);
+    }
+  };
+  long tau = blockIdx.x;
+  if (threadIdx.x == 0 && tau < tl.ntiles) {
+    issue(tau, 0, 0);
+    issue(tau, 1, 1);
+  }
+  const double s3 = 0.86602540378443864676372317075294;
+  const double inv = 1.0 / (3.0 * N);
+  uint32_t ph[2] = {0, 0};
+  int b = 0;
+  for (; tau < tl.ntiles; tau += gridDim.x) {
+    int in; long item, col0;
+    tile_coords(tl, tau, W, in, item, col0);
+    const long col = col0 + c;
+    const bool ok = col < tl.ncols;
+    double2* a = f + item * tl.bstride + (ok ? col : 0);
+    const long S = tl.ncols;
+    double2 v[E], ap[E], an[E];
+#pragma unroll 1
+    for (int q = 0; q < 3; ++q) {
+      const int r = q - 1;
+      mbar_wait(&bars[b], ph[b]);
+      ph[b] ^= 1;
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int l = t + T * i;
+        v[i] = (q == 1 && l == N - 1) ? tail[b][c] : st[b][l * W + c];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {  // refill this buffer with the stream two steps ahead
+        const int q2 = q + 2;
+        if (q2 < 3) issue(tau, q2, b);
+        else if (tau + gridDim.x < tl.ntiles) issue(tau + gridDim.x, q2 - 3, b);
+      }
+      b ^= 1;
+      fft<N, E, -1>(v, t, xb, twN, CtaSync{}, xs);
+      // 3m U_k = sum_r zeta_{3m}^{-rk} S_r(k); 3m U_{k-m} = sum_r zeta_{3m}^{-rk} zeta_3^{r} S_r(k)
+      const double2 z3 = make_double2(r == 0 ? 1.0 : -0.5, r == 0 ? 0.0 : (r > 0 ? s3 : -s3));  // zeta_3^{r}
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int k = t + T * i;
+        const double2 tz = ldtw(&tw3N[k]);
+        const double2 zr = r == 0 ? make_double2(1, 0) : (r > 0 ? cconj(tz) : tz);  // zeta_{3m}^{-rk}
+        const double2 p = cmul(zr, v[i]);
+        if (q == 0) {
+          ap[i] = p;
+          an[i] = cmul(z3, p);
+        } else {
+          ap[i] = cadd(ap[i], p);
+          an[i] = cadd(an[i], cmul(z3, p));
+        }
+      }
+    }
+    if (ok) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int k = t + T * i;
+        a[(long)(N - 1 + k) * S] = cscale(ap[i], inv);
+        if (k > 0) a[(long)(k - 1) * S] = cscale(an[i], inv);
+      }
+    }
+  }
+}
+
+// ================================================================ launchers ==
+namespace {
+
+template <class K>
+cudaError_t launch_t(K kernel, int threads, size_t smem, long ntiles, cudaStream_t s, void** args) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  if (per_sm < 1) per_sm = 1;
+  long grid = (long)num_sms() * per_sm;
+  if (ntiles < grid) grid = ntiles;
+  if (grid < 1) grid = 1;
+  return cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s);
+}
+
+template <int N>
+Tiles make_tiles(long ncols, long batch, int inputs, long bstride, long ustride) {
+  constexpr int W = TCfg<N>::W;
+  Tiles tl;
+  tl.ncols = ncols;
+  tl.nct = (ncols + W - 1) / W;
+  tl.batch = batch;
+  tl.per_input = tl.nct * batch;
+  tl.ntiles = tl.per_input * inputs;
+  tl.bstride = bstride;
+  tl.ustride = ustride;
+  return tl;
+}
+
+}  // namespace
+
+template <int N>
+cudaError_t pad_bwd_tma(double2* f, double2* g, double2* U, double2* V, long ncols, long batch, long bstride,
+                        long ustride, cudaStream_t s) {
+  using C = TCfg<N>;
+  const double2* twN = zeta_table(N);
+  const double2* tw2N = zeta_table(2 * N);
+  if (!twN || !tw2N) return cudaErrorMemoryAllocation;
+  CUtensorMap mf, mg;
+  if (!encode_pencil_map(&mf, f, ncols, N, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
+  if (!encode_pencil_map(&mg, g ? g : f, ncols, N, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
+  Tiles tl = make_tiles<N>(ncols, batch, g ? 2 : 1, bstride, ustride);
+  void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw2N};
+  const size_t smem = ((size_t)N * C::W + C::XB) * 16 + 16;
+  return launch_t(k_pad_bwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
+}
+
+template <int N>
+cudaError_t pad_fwd_tma(double2* f, const double2* U, long ncols, long batch, long bstride, long ustride,
+                        cudaStream_t s) {
+  using C = TCfg<N>;
+  const double2* twN = zeta_table(N);
+  const double2* tw2N = zeta_table(2 * N);
+  if (!twN || !tw2N) return cudaErrorMemoryAllocation;
+  CUtensorMap mf, mu;
+  if (!encode_pencil_map(&mf, f, ncols, N, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
+  if (!encode_pencil_map(&mu, U, ncols, N, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
+  Tiles tl = make_tiles<N>(ncols, batch, 1, bstride, ustride);
+  void* args[] = {&mf, &mu, &f, &tl, &twN, &tw2N};
+  const size_t smem = (2 * (size_t)N * C::W + C::XB) * 16 + 32;
+  return launch_t(k_pad_fwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
+}
+
+template <int N>
+cudaError_t pad0_bwd_tma(double2* f, double2* g, double2* U, double2* V, long ncols, long batch, long bstride,
+                         long ustride, cudaStream_t s) {
+  using C = TCfg<N>;
+  constexpr int R2 = ((2 * N - 1 + C::BR - 1) / C::BR) * C::BR;
+  const double2* twN = zeta_table(N);
+  const double2* tw3N = zeta_table(3 * N);
+  if (!twN || !tw3N) return cudaErrorMemoryAllocation;
+  CUtensorMap mf, mg;
+  if (!encode_pencil_map(&mf, f, ncols, 2 * N - 1, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
+  if (!encode_pencil_map(&mg, g ? g : f, ncols, 2 * N - 1, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
+  Tiles tl = make_tiles<N>(ncols, batch, g ? 2 : 1, bstride, ustride);
+  void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw3N};
+  const size_t smem = ((size_t)R2 * C::W + C::XB) * 16 + 16;
+  return launch_t(k_pad0_bwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
+}
+
+template <int N>
+cudaError_t pad0_fwd_tma(double2* f, const double2* U, long ncols, long batch, long bstride, long ustride,
+                         cudaStream_t s) {
+  using C = TCfg<N>;
+  const double2* twN = zeta_table(N);
+  const double2* tw3N = zeta_table(3 * N);
+  if (!twN || !tw3N) return cudaErrorMemoryAllocation;
+  CUtensorMap mf, mu, mu1;
+  if (!encode_pencil_map(&mf, f, ncols, 2 * N - 1, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
+  if (!encode_pencil_map(&mu, U, ncols, N + 1, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
+  if (!encode_pencil_map(&mu1, U, ncols, N + 1, batch, ustride, C::W, 1)) return cudaErrorNotSupported;
+  Tiles tl = make_tiles<N>(ncols, batch, 1, bstride, ustride);
+  void* args[] = {&mf, &mu, &mu1, &f, &tl, &twN, &tw3N};
+  const size_t smem = (2 * (size_t)N * C::W + 32 + C::XB) * 16 + 32;
+  return launch_t(k_pad0_fwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
+}
+
+#define IDC_INST_T(N)                                                                                           \
+  template cudaError_t pad_bwd_tma<N>(double2*, double2*, double2*, double2*, long, long, long, long, cudaStream_t); \
+  template cudaError_t pad_fwd_tma<N>(double2*, const double2*, long, long, long, long, cudaStream_t);              \
+  template cudaError_t pad0_bwd_tma<N>(double2*, double2*, double2*, double2*, long, long, long, long,             \
+                                       cudaStream_t);                                                            \
+  template cudaError_t pad0_fwd_tma<N>(double2*, const double2*, long, long, long, long, cudaStream_t);
+IDC_INST_T(64)
+IDC_INST_T(128)
+IDC_INST_T(256)
+IDC_INST_T(512)
+IDC_INST_T(1024)
+IDC_INST_T(2048)
+IDC_INST_T(4096)
+
+}  // namespace idc
