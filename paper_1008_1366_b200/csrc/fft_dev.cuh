@@ -77,46 +77,105 @@ __device__ __forceinline__ double2 cmul_dir(double2 a, double2 w) {
 }
 
 // ------------------------------------------------- compile-time twiddles --
-// cos(pi j / 16), j = 0..8
-__host__ __device__ constexpr double cos16tab(int j) {
-  return j == 0 ? 1.0
-       : j == 1 ? 0.98078528040323044912618223613424
-       : j == 2 ? 0.92387953251128675612818318939679
-       : j == 3 ? 0.83146961230254523707878837761791
-       : j == 4 ? 0.70710678118654752440084436210485
-       : j == 5 ? 0.55557023301960222474283081394853
-       : j == 6 ? 0.38268343236508977172845998403040
-       : j == 7 ? 0.19509032201612826784828486847702
+// cos(2 pi j / 192), j = 0..48 (first quadrant; 192 = lcm of the 32-, 48-
+// and 64-point roots the kernels need as immediates), 35 significant digits
+__host__ __device__ constexpr double cos192tab(int j) {
+  return j == 0  ? 1.00000000000000000000000000000000000
+       : j == 1  ? 0.99946458747636564442983644624285995
+       : j == 2  ? 0.99785892323860350673806979127277760
+       : j == 3  ? 0.99518472667219688624483695310947992
+       : j == 4  ? 0.99144486137381041114455752692856287
+       : j == 5  ? 0.98664333208487900474692393298420604
+       : j == 6  ? 0.98078528040323044912618223613423904
+       : j == 7  ? 0.97387697927733364814968997013355039
+       : j == 8  ? 0.96592582628906828674974319972889737
+       : j == 9  ? 0.95694033573220886493579788698026997
+       : j == 10 ? 0.94693012949510566425580427485398368
+       : j == 11 ? 0.93590592675732570029170724946673536
+       : j == 12 ? 0.92387953251128675612818318939678829
+       : j == 13 ? 0.91086382492117581857329170716055065
+       : j == 14 ? 0.89687274153268830389410393639308120
+       : j == 15 ? 0.88192126434835502971275686366038835
+       : j == 16 ? 0.86602540378443864676372317075293618
+       : j == 17 ? 0.84920218152657888764909693734310022
+       : j == 18 ? 0.83146961230254523707878837761790576
+       : j == 19 ? 0.81284668459161521657909614327190880
+       : j == 20 ? 0.79335334029123516457977696150129928
+       : j == 21 ? 0.77301045336273696081090660975846980
+       : j == 22 ? 0.75183980747897739640751940637696144
+       : j == 23 ? 0.72986407269783565735010119440318188
+       : j == 24 ? 0.70710678118654752440084436210484904
+       : j == 25 ? 0.68359230202287128051349759431615512
+       : j == 26 ? 0.65934581510006886842512461205533745
+       : j == 27 ? 0.63439328416364549821517161322549337
+       : j == 28 ? 0.60876142900872063941609754289816400
+       : j == 29 ? 0.58247769686780214919713476703611245
+       : j == 30 ? 0.55557023301960222474283081394853287
+       : j == 31 ? 0.52806785065036799587344882033760557
+       : j == 32 ? 0.50000000000000000000000000000000000
+       : j == 33 ? 0.47139673682599764855638762590525438
+       : j == 34 ? 0.44228869021900128199523897732424473
+       : j == 35 ? 0.41270702980439473704770218607336747
+       : j == 36 ? 0.38268343236508977172845998403039887
+       : j == 37 ? 0.35225004792123350653175231975871267
+       : j == 38 ? 0.32143946530316158070105762407890159
+       : j == 39 ? 0.29028467725446236763619237581739527
+       : j == 40 ? 0.25881904510252076234889883762404833
+       : j == 41 ? 0.22707626303437320758569669257708809
+       : j == 42 ? 0.19509032201612826784828486847702224
+       : j == 43 ? 0.16289547339458873948080063970826556
+       : j == 44 ? 0.13052619222005159154840622789548901
+       : j == 45 ? 0.09801714032956060199419556388864185
+       : j == 46 ? 0.06540312923014306681531555877517544
+       : j == 47 ? 0.03271908282177614206365992631728813
        : 0.0;
 }
-// cos(2 pi j / 32) for any integer j
-__host__ __device__ constexpr double cos32(int j) {
-  return ((j & 31) <= 8)  ? cos16tab(j & 31)
-       : ((j & 31) <= 16) ? -cos16tab(16 - (j & 31))
-       : ((j & 31) <= 24) ? -cos16tab((j & 31) - 16)
-                          : cos16tab(32 - (j & 31));
+// cos(2 pi j / 192) for any integer j
+__host__ __device__ constexpr int mod192(int j) { return (j % 192 + 192) % 192; }
+__host__ __device__ constexpr double cos192(int j) {
+  return (mod192(j) <= 48)  ? cos192tab(mod192(j))
+       : (mod192(j) <= 96)  ? -cos192tab(96 - mod192(j))
+       : (mod192(j) <= 144) ? -cos192tab(mod192(j) - 96)
+                            : cos192tab(192 - mod192(j));
 }
-__host__ __device__ constexpr double sin32(int j) { return cos32(j - 8); }
+__host__ __device__ constexpr double sin192(int j) { return cos192(j - 48); }
 
-// a * exp(SIGN * 2 pi i K / L), L | 32, resolved at compile time
+// a * exp(SIGN * 2 pi i K / L), L | 192, resolved at compile time; the
+// trivial roots (1, +-i, -1) cost no arithmetic
 template <int K, int L, int SIGN>
 __device__ __forceinline__ double2 twc(double2 a) {
-  constexpr int j = ((K * (32 / L)) % 32 + 32) % 32;
+  static_assert(192 % L == 0, "compile-time roots need L | 192");
+  constexpr int j = mod192(K * (192 / L));
   if constexpr (j == 0) {
     return a;
-  } else if constexpr (j == 8) {            // * (SIGN i)
+  } else if constexpr (j == 48) {           // * (SIGN i)
     if constexpr (SIGN > 0) return make_double2(-a.y, a.x);
     else return make_double2(a.y, -a.x);
-  } else if constexpr (j == 16) {
+  } else if constexpr (j == 96) {
     return make_double2(-a.x, -a.y);
-  } else if constexpr (j == 24) {           // * (-SIGN i)
+  } else if constexpr (j == 144) {          // * (-SIGN i)
     if constexpr (SIGN > 0) return make_double2(a.y, -a.x);
     else return make_double2(-a.y, a.x);
   } else {
-    constexpr double c = cos32(j);
-    constexpr double s = SIGN > 0 ? sin32(j) : -sin32(j);
+    constexpr double c = cos192(j);
+    constexpr double s = SIGN > 0 ? sin192(j) : -sin192(j);
     return make_double2(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
   }
+}
+
+// Per-element roots of the residue split / recombination: element i of a
+// lane (k = t + T i, T = M / E) needs zeta_{QM}^{R k} = zeta_{QM}^{R t} *
+// zeta_{QE}^{R i}.  The lane loads zt = zeta_{QM}^{R t} once; the second
+// factor is a compile-time root.  f(i, w_i) is called for i = 0..E-1 with
+// w_i = zt * zeta_{QE}^{SIGN R i} (4 fp64 instructions instead of one
+// 16-byte table load per element).
+template <int QE, int R, int SIGN, class F, int... I>
+__device__ __forceinline__ void roots_apply(double2 zt, F& f, std::integer_sequence<int, I...>) {
+  (f(I, twc<R * I, QE, SIGN>(zt)), ...);
+}
+template <int QE, int R, int SIGN, int E, class F>
+__device__ __forceinline__ void for_roots(double2 zt, F&& f) {
+  roots_apply<QE, R, SIGN>(zt, f, std::make_integer_sequence<int, E>{});
 }
 
 // ----------------------------------------------- in-register DFT_R (R<=32) --
@@ -186,17 +245,31 @@ __device__ __forceinline__ void pass_compute(double2 (&v)[E], int t, const doubl
       // w^{Qa} (a < R/Q), one complex product for the mixed terms
       const int jm = (t + T * b) & (NS - 1);
       constexpr int STEP = N / (NS * R);
+      {
       constexpr int Q = R >= 16 ? 4 : (R >= 4 ? 2 : 1);
       double2 lo[Q], hi[R / Q];
 #pragma unroll
       for (int c = 1; c < Q; ++c) lo[c] = ldtw_pass(&tw[c * jm * STEP]);
 #pragma unroll
       for (int a = 1; a < R / Q; ++a) hi[a] = ldtw_pass(&tw[Q * a * jm * STEP]);
+#ifndef IDC_PASS_TW_PRODUCT
+      // x[Qa + c] * w^c * w^{Qa}: two multiplies per element instead of
+      // forming every w^r = w^{Qa} w^c first (same multiply count, but no
+      // R-element twiddle set live in registers: -7% time at m = 4096)
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const int a = r / Q, c = r % Q;
+        if (c != 0) x[r] = cmul_dir<SIGN>(x[r], lo[c]);
+        if (a != 0) x[r] = cmul_dir<SIGN>(x[r], hi[a]);
+      }
+#else
 #pragma unroll
       for (int r = 1; r < R; ++r) {
         const int a = r / Q, c = r % Q;
         const double2 w = a == 0 ? lo[c] : (c == 0 ? hi[a] : cmul(hi[a], lo[c]));
         x[r] = cmul_dir<SIGN>(x[r], w);
+      }
+#endif
       }
     }
     dft<R, SIGN>(x);

@@ -68,9 +68,13 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
   constexpr int T = C::T;
   extern __shared__ __align__(16) double2 smem[];
   const int grp = threadIdx.x / T, t = threadIdx.x - grp * T;
+#ifndef IDC_CCONV_SMEM_STASH
+  double2* xb = smem + grp * C::XB;
+#else
   double2* xb = smem + grp * (C::XB + 2 * M);
   double2* S = xb + C::XB;
   double2* P = S + M;
+#endif
   const auto sync = row_sync<M, E, G>(grp);
   const double inv = 1.0 / (2.0 * M);
   for (long row0 = (long)blockIdx.x * G; row0 < nrows; row0 += (long)gridDim.x * G) {
@@ -81,6 +85,38 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
     const bool ok = row < nrows;
     const double2* fr = f + (ok ? row : 0) * (long)M;
     const double2* gr = g + (ok ? row : 0) * (long)M;
+#ifndef IDC_CCONV_SMEM_STASH
+    // Every intermediate in registers (at most three E-vectors live): no
+    // shared-memory stash traffic, only the FFT exchanges.
+    double2 x[E], y[E], z[E];
+    // r = 0: u = fft^{-1} f ; v = fft^{-1} g ; u*v
+#pragma unroll
+    for (int i = 0; i < E; ++i) x[i] = ldv(&fr[t + T * i]);
+    fft<M, E, +1>(x, t, xb, twM, sync);
+#pragma unroll
+    for (int i = 0; i < E; ++i) y[i] = ldv(&gr[t + T * i]);
+    fft<M, E, +1>(y, t, xb, twM, sync);
+#pragma unroll
+    for (int i = 0; i < E; ++i) x[i] = cmul(x[i], y[i]);
+    // r = 1: zeta_{2m}^k-shifted streams
+    // zeta_{2m}^k, k = t + T i: zeta_{2m}^t (one table value) x zeta_{2E}^i (immediate)
+    const double2 zt = ldtw(&tw2M[t]);
+    for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { y[i] = cmul(ldv(&fr[t + T * i]), w); });
+    fft<M, E, +1>(y, t, xb, twM, sync);
+    for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { z[i] = cmul(ldv(&gr[t + T * i]), w); });
+    fft<M, E, +1>(z, t, xb, twM, sync);
+#pragma unroll
+    for (int i = 0; i < E; ++i) y[i] = cmul(y[i], z[i]);
+    // forward transforms, recombination and 1/(2m)
+    fft<M, E, -1>(y, t, xb, twM, sync);
+    fft<M, E, -1>(x, t, xb, twM, sync);
+    if (ok) {
+      double2* fw = f + row * (long)M;
+      for_roots<2 * E, 1, -1, E>(cconj(zt), [&](int i, double2 w) {       // zeta_{2m}^{-k}
+        fw[t + T * i] = cscale(cadd(x[i], cmul(y[i], w)), inv);
+      });
+    }
+#else
     double2 v[E];
     // r = 0: u = fft^{-1} f ; v = fft^{-1} g ; u*v
 #pragma unroll
@@ -116,6 +152,8 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
 #pragma unroll
       for (int i = 0; i < E; ++i) fw[t + T * i] = cscale(cadd(v[i], S[t + T * i]), inv);
     }
+
+#endif
   }
 }
 
@@ -329,7 +367,12 @@ cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s) {
   const double2* tw2M = zeta_table(2 * M);
   if (!twM || !tw2M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw2M};
-  return launch2(k_cconv_rows2<M, E, G>, C::THREADS, (size_t)G * (C::XB + 2 * M) * 16, nrows, G, s, args);
+#ifndef IDC_CCONV_SMEM_STASH
+  const size_t per = C::XB;               // exchange buffer only (intermediates in registers)
+#else
+  const size_t per = C::XB + 2 * M;
+#endif
+  return launch2(k_cconv_rows2<M, E, G>, C::THREADS, (size_t)G * per * 16, nrows, G, s, args);
 }
 
 template <int M>

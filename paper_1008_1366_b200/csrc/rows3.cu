@@ -103,6 +103,23 @@ k_hconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, long nrows
     for (int rr = 0; rr < 3; ++rr) {
       const int r = rr == 0 ? 0 : (rr == 1 ? 1 : -1);
       const double2 c = make_double2(r == 0 ? 1.0 : -0.5, r == 0 ? 0.0 : (r < 0 ? s3 : -s3));  // zeta_3^{-r}
+#ifndef IDC_ROOTS_TABLE
+      // zeta_{3m}^{rk}, k = t + T i: zeta_{3m}^{rt} x zeta_{3E}^{ri} (immediate)
+      const double2 zt = r == 0 ? make_double2(1.0, 0.0) : (r > 0 ? ldtw(&tw3M[t]) : cconj(ldtw(&tw3M[t])));
+      auto split = [&](int i, double2 zr) {
+        const int k = t + T * i;
+        if (i == 0 && t == 0) v[i] = make_double2(F[0].x, Gs[0].x);       // w_{0,r} = Re U_0 (AMB-7)
+        else v[i] = zpair(F, Gs, k, M - k, zr, c);
+      };
+      if (r == 0) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) split(i, zt);
+      } else if (r > 0) {
+        for_roots<3 * E, 1, +1, E>(zt, split);
+      } else {
+        for_roots<3 * E, 1, -1, E>(zt, split);
+      }
+#else
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const int k = t + T * i;
@@ -114,6 +131,7 @@ k_hconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, long nrows
           v[i] = zpair(F, Gs, k, M - k, zr, c);
         }
       }
+#endif
       if (r == -1) {  // last read of the staged row: prefetch the next one
         sync();
         if (t == 0 && row + stride < nrows) {
@@ -141,16 +159,20 @@ k_hconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, long nrows
     for (int i = 0; i < E; ++i) xb[t + T * i] = Q[i];
     sync();
     double2* fw = f + row * (long)M;
-#pragma unroll
-    for (int i = 0; i < E; ++i) {
+    auto recombine = [&](int i, double2 tz) {
       const int k = t + T * i;
       const double2 a = Q[i], b = cconj(xb[(M - k) & (M - 1)]);
-      const double2 tz = ldtw(&tw3M[k]);
       const double2 pp0 = cscale(cadd(a, b), 0.5);
       const double2 d = csub(a, b);
       const double2 pp1 = make_double2(0.5 * d.y, -0.5 * d.x);
       fw[k] = cscale(cadd(cadd(pp0, cmul(v[i], tz)), cmulc(pp1, tz)), inv);
-    }
+    };
+#ifndef IDC_ROOTS_TABLE
+    for_roots<3 * E, 1, +1, E>(ldtw(&tw3M[t]), recombine);
+#else
+#pragma unroll
+    for (int i = 0; i < E; ++i) recombine(i, ldtw(&tw3M[t + T * i]));
+#endif
     sync();
   }
 }
@@ -197,12 +219,26 @@ k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const doub
         const int r = r0 + s;
         const double2 c = r == 0 ? make_double2(1, 0) : r == 1 ? make_double2(0, -1) : r == 2 ? make_double2(-1, 0)
                                                                                     : make_double2(0, 1);  // (-i)^r
+#ifndef IDC_ROOTS_TABLE
+        {  // zeta_{4m}^{rk} = zeta_{4m}^{rt} x zeta_{4E}^{ri}
+          auto split = [&](int i, double2 zr) {
+            if (i == 0 && t == 0) v[i] = make_double2(F[0].x, Gs[0].x);
+            else v[i] = zpair(F, Gs, t + T * i, M - t - T * i, zr, c);
+          };
+          const double2 zt = ldtw(&tw4M[r * t]);
+          if (r == 0) for_roots<4 * E, 0, +1, E>(zt, split);
+          else if (r == 1) for_roots<4 * E, 1, +1, E>(zt, split);
+          else if (r == 2) for_roots<4 * E, 2, +1, E>(zt, split);
+          else for_roots<4 * E, 3, +1, E>(zt, split);
+        }
+#else
 #pragma unroll
         for (int i = 0; i < E; ++i) {
           const int k = t + T * i;
           if (k == 0) v[i] = make_double2(F[0].x, Gs[0].x);
           else v[i] = zpair(F, Gs, k, M - k, ldtw(&tw4M[r * k]), c);
         }
+#endif
         if (r == 3) {  // last read of the staged row: prefetch the next one
           sync();
           if (t == 0 && row + stride < nrows) {
