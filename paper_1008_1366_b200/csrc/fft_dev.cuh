@@ -26,6 +26,7 @@
 // no arithmetic.
 #pragma once
 #include <cuda_runtime.h>
+#include <type_traits>
 #include <utility>
 
 namespace idc {
@@ -176,6 +177,16 @@ __device__ __forceinline__ void roots_apply(double2 zt, F& f, std::integer_seque
 template <int QE, int R, int SIGN, int E, class F>
 __device__ __forceinline__ void for_roots(double2 zt, F&& f) {
   roots_apply<QE, R, SIGN>(zt, f, std::make_integer_sequence<int, E>{});
+}
+
+// f(std::integral_constant<int, I>{}) for I = 0..N-1 (compile-time element index)
+template <class F, int... I>
+__device__ __forceinline__ void static_for_impl(F& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
 }
 
 // ----------------------------------------------- in-register DFT_R (R<=32) --

@@ -99,61 +99,45 @@ k_hconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, long nrows
     phase ^= 1;
     double2 v[E], Q[E];
     double p0[E];
-#pragma unroll
-    for (int rr = 0; rr < 3; ++rr) {
-      const int r = rr == 0 ? 0 : (rr == 1 ? 1 : -1);
-      const double2 c = make_double2(r == 0 ? 1.0 : -0.5, r == 0 ? 0.0 : (r < 0 ? s3 : -s3));  // zeta_3^{-r}
-#ifndef IDC_ROOTS_TABLE
-      // zeta_{3m}^{rk}, k = t + T i: zeta_{3m}^{rt} x zeta_{3E}^{ri} (immediate)
-      const double2 zt = r == 0 ? make_double2(1.0, 0.0) : (r > 0 ? ldtw(&tw3M[t]) : cconj(ldtw(&tw3M[t])));
-      auto split = [&](int i, double2 zr) {
-        const int k = t + T * i;
-        if (i == 0 && t == 0) v[i] = make_double2(F[0].x, Gs[0].x);       // w_{0,r} = Re U_0 (AMB-7)
-        else v[i] = zpair(F, Gs, k, M - k, zr, c);
-      };
-      if (r == 0) {
-#pragma unroll
-        for (int i = 0; i < E; ++i) split(i, zt);
-      } else if (r > 0) {
-        for_roots<3 * E, 1, +1, E>(zt, split);
+    // residues r = 0 and r = 1 from ONE read of the staged pair:
+    // P_k = f_k + i g_k, R_k = conj f_{m-k} + i conj g_{m-k};
+    // v = P + R (r = 0), Q = zeta_{3m}^{k} (P + zeta_3^{-1} R) (r = 1)
+    const double2 c1 = make_double2(-0.5, -s3);                 // zeta_3^{-1}
+    for_roots<3 * E, 1, +1, E>(ldtw(&tw3M[t]), [&](int i, double2 zr) {
+      const int k = t + T * i;
+      if (i == 0 && t == 0) {
+        v[i] = Q[i] = make_double2(F[0].x, Gs[0].x);              // w_{0,r} = Re U_0 (AMB-7)
       } else {
-        for_roots<3 * E, 1, -1, E>(zt, split);
+        const double2 fk = F[k], gk = Gs[k], fm = F[M - k], gm = Gs[M - k];
+        const double2 P = make_double2(fk.x - gk.y, fk.y + gk.x);
+        const double2 R = make_double2(fm.x + gm.y, gm.x - fm.y);
+        v[i] = cadd(P, R);
+        Q[i] = cmul(zr, cadd(P, cmul(c1, R)));
       }
-#else
+    });
+    fft<M, E, +1>(v, t, xb, twM, sync);                         // two c2r in one complex FFT
 #pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const int k = t + T * i;
-        if (k == 0) {
-          v[i] = make_double2(F[0].x, Gs[0].x);                  // w_{0,r} = Re U_0 (AMB-7)
-        } else {
-          const double2 tz = ldtw(&tw3M[k]);
-          const double2 zr = r == 0 ? make_double2(1.0, 0.0) : (r > 0 ? tz : cconj(tz));
-          v[i] = zpair(F, Gs, k, M - k, zr, c);
-        }
-      }
-#endif
-      if (r == -1) {  // last read of the staged row: prefetch the next one
-        sync();
-        if (t == 0 && row + stride < nrows) {
-          mbar_arrive_expect_tx(bar, 2u * M * 16u);
-          tma_load_1d(F, f + (row + stride) * (long)M, M * 16u, bar);
-          tma_load_1d(Gs, g + (row + stride) * (long)M, M * 16u, bar);
-        }
-      }
-      fft<M, E, +1>(v, t, xb, twM, sync);                      // two c2r in one complex FFT
-      if (r == 0) {
+    for (int i = 0; i < E; ++i) p0[i] = v[i].x * v[i].y;
+    fft<M, E, +1>(Q, t, xb, twM, sync);
 #pragma unroll
-        for (int i = 0; i < E; ++i) p0[i] = v[i].x * v[i].y;
-      } else if (r == 1) {
-#pragma unroll
-        for (int i = 0; i < E; ++i) Q[i] = make_double2(p0[i], v[i].x * v[i].y);
-        fft<M, E, -1>(Q, t, xb, twM, sync);
-      } else {
-#pragma unroll
-        for (int i = 0; i < E; ++i) v[i] = make_double2(v[i].x * v[i].y, 0.0);
-        fft<M, E, -1>(v, t, xb, twM, sync);
-      }
+    for (int i = 0; i < E; ++i) Q[i] = make_double2(p0[i], Q[i].x * Q[i].y);
+    fft<M, E, -1>(Q, t, xb, twM, sync);                         // Q = fft(p_0 + i p_1)
+    // r = -1: the last read of the staged row, then the next row's bulk copy
+    const double2 cm = make_double2(-0.5, s3);                  // zeta_3^{+1}
+    for_roots<3 * E, 1, -1, E>(cconj(ldtw(&tw3M[t])), [&](int i, double2 zr) {
+      if (i == 0 && t == 0) v[i] = make_double2(F[0].x, Gs[0].x);
+      else v[i] = zpair(F, Gs, t + T * i, M - t - T * i, zr, cm);
+    });
+    sync();
+    if (t == 0 && row + stride < nrows) {
+      mbar_arrive_expect_tx(bar, 2u * M * 16u);
+      tma_load_1d(F, f + (row + stride) * (long)M, M * 16u, bar);
+      tma_load_1d(Gs, g + (row + stride) * (long)M, M * 16u, bar);
     }
+    fft<M, E, +1>(v, t, xb, twM, sync);
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = make_double2(v[i].x * v[i].y, 0.0);
+    fft<M, E, -1>(v, t, xb, twM, sync);                         // P_{-1}
     // P_0, P_1 from Q via Q_{m-k}; 3m h_k = P_0 + zeta^{k} P_{-1} + zeta^{-k} P_1 (Eq. fft0forwardB)
 #pragma unroll
     for (int i = 0; i < E; ++i) xb[t + T * i] = Q[i];
@@ -167,12 +151,7 @@ k_hconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, long nrows
       const double2 pp1 = make_double2(0.5 * d.y, -0.5 * d.x);
       fw[k] = cscale(cadd(cadd(pp0, cmul(v[i], tz)), cmulc(pp1, tz)), inv);
     };
-#ifndef IDC_ROOTS_TABLE
     for_roots<3 * E, 1, +1, E>(ldtw(&tw3M[t]), recombine);
-#else
-#pragma unroll
-    for (int i = 0; i < E; ++i) recombine(i, ldtw(&tw3M[t + T * i]));
-#endif
     sync();
   }
 }
@@ -210,87 +189,87 @@ k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const doub
     phase ^= 1;
     const double2* hr = h + row * (long)M;
     double2* fw = f + row * (long)M;   // staged: free to serve as the partial-sum scratch
-    double2 v[E];
+    if (t == 0 && row + stride < nrows) prefetch_l2(h + (row + stride) * (long)M, M * 16u);
     double a0[E], a1[E];
-#pragma unroll 1
-    for (int r0 = 0; r0 < 4; r0 += 2) {
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int r = r0 + s;
-        const double2 c = r == 0 ? make_double2(1, 0) : r == 1 ? make_double2(0, -1) : r == 2 ? make_double2(-1, 0)
-                                                                                    : make_double2(0, 1);  // (-i)^r
-#ifndef IDC_ROOTS_TABLE
-        {  // zeta_{4m}^{rk} = zeta_{4m}^{rt} x zeta_{4E}^{ri}
-          auto split = [&](int i, double2 zr) {
-            if (i == 0 && t == 0) v[i] = make_double2(F[0].x, Gs[0].x);
-            else v[i] = zpair(F, Gs, t + T * i, M - t - T * i, zr, c);
-          };
-          const double2 zt = ldtw(&tw4M[r * t]);
-          if (r == 0) for_roots<4 * E, 0, +1, E>(zt, split);
-          else if (r == 1) for_roots<4 * E, 1, +1, E>(zt, split);
-          else if (r == 2) for_roots<4 * E, 2, +1, E>(zt, split);
-          else for_roots<4 * E, 3, +1, E>(zt, split);
+    // one residue pair (r0, r0 + 1), r0 = 0 or 2, with compile-time roots
+    // zeta_{4m}^{rk} = zeta_{4m}^{rt} x zeta_{4E}^{ri} and c_r = (-i)^r
+    auto pair = [&](auto R0) {
+      constexpr int r0 = decltype(R0)::value;
+      const double2 ca = r0 == 0 ? make_double2(1, 0) : make_double2(-1, 0);   // (-i)^{r0}
+      const double2 cb = r0 == 0 ? make_double2(0, -1) : make_double2(0, 1);   // (-i)^{r0+1}
+      // (za, zb are re-loaded per stage -- volatile loads -- so that the
+      // derived per-element roots are recomputed, not kept live across FFTs)
+      double2 v[E], w[E];
+      double2 za = ldtw(&tw4M[r0 * t]), zb = ldtw(&tw4M[(r0 + 1) * t]);
+      // both f/g residue streams of the pair from one read of the staged row
+      static_for<E>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        const int k = t + T * i;
+        if (i == 0 && t == 0) {
+          v[i] = w[i] = make_double2(F[0].x, Gs[0].x);            // w_{0,r} = Re U_0 (AMB-7)
+        } else {
+          const double2 fk = F[k], gk = Gs[k], fm = F[M - k], gm = Gs[M - k];
+          const double2 P = make_double2(fk.x - gk.y, fk.y + gk.x);
+          const double2 R = make_double2(fm.x + gm.y, gm.x - fm.y);
+          v[i] = cmul(twc<r0 * i, 4 * E, +1>(za), cadd(P, cmul(ca, R)));
+          w[i] = cmul(twc<(r0 + 1) * i, 4 * E, +1>(zb), cadd(P, cmul(cb, R)));
         }
-#else
-#pragma unroll
-        for (int i = 0; i < E; ++i) {
-          const int k = t + T * i;
-          if (k == 0) v[i] = make_double2(F[0].x, Gs[0].x);
-          else v[i] = zpair(F, Gs, k, M - k, ldtw(&tw4M[r * k]), c);
-        }
-#endif
-        if (r == 3) {  // last read of the staged row: prefetch the next one
-          sync();
-          if (t == 0 && row + stride < nrows) {
-            mbar_arrive_expect_tx(bar, 2u * M * 16u);
-            tma_load_1d(F, f + (row + stride) * (long)M, M * 16u, bar);
-            tma_load_1d(Gs, g + (row + stride) * (long)M, M * 16u, bar);
-          }
-        }
-        fft<M, E, +1>(v, t, xb, twM, sync);
-#pragma unroll
-        for (int i = 0; i < E; ++i) {
-          if (s == 0) a0[i] = v[i].x * v[i].y;
-          else a1[i] = v[i].x * v[i].y;
-        }
-      }
-      {  // h packed across the residue pair: w^h_r + i w^h_{r+1}
-        const double2 c0 = r0 == 0 ? make_double2(1, 0) : make_double2(-1, 0);
-        const double2 c1 = r0 == 0 ? make_double2(0, -1) : make_double2(0, 1);
-#pragma unroll
-        for (int i = 0; i < E; ++i) {
-          const int k = t + T * i;
-          if (k == 0) {
-            const double h0 = ldv(&hr[0]).x;
-            v[i] = make_double2(h0, h0);
-          } else {
-            const double2 hk = ldv(&hr[k]), hm = cconj(ldv(&hr[M - k]));
-            const double2 w0 = cmul(ldtw(&tw4M[r0 * k]), cadd(hk, cmul(c0, hm)));
-            const double2 w1 = cmul(ldtw(&tw4M[(r0 + 1) * k]), cadd(hk, cmul(c1, hm)));
-            v[i] = make_double2(w0.x - w1.y, w0.y + w1.x);
-          }
+      });
+      if constexpr (r0 == 2) {  // last read of the staged row: prefetch the next one
+        sync();
+        if (t == 0 && row + stride < nrows) {
+          mbar_arrive_expect_tx(bar, 2u * M * 16u);
+          tma_load_1d(F, f + (row + stride) * (long)M, M * 16u, bar);
+          tma_load_1d(Gs, g + (row + stride) * (long)M, M * 16u, bar);
         }
       }
       fft<M, E, +1>(v, t, xb, twM, sync);
 #pragma unroll
+      for (int i = 0; i < E; ++i) a0[i] = v[i].x * v[i].y;
+      fft<M, E, +1>(w, t, xb, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) a1[i] = w[i].x * w[i].y;
+      // h packed across the residue pair: w^h_{r0} + i w^h_{r0+1}
+      za = ldtw(&tw4M[r0 * t]);
+      zb = ldtw(&tw4M[(r0 + 1) * t]);
+      static_for<E>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        const int k = t + T * i;
+        if (i == 0 && t == 0) {
+          const double h0 = ldv(&hr[0]).x;
+          v[i] = make_double2(h0, h0);
+        } else {
+          const double2 hk = ldv(&hr[k]), hm = cconj(ldv(&hr[M - k]));
+          const double2 w0 = cmul(twc<r0 * i, 4 * E, +1>(za), cadd(hk, cmul(ca, hm)));
+          const double2 w1 = cmul(twc<(r0 + 1) * i, 4 * E, +1>(zb), cadd(hk, cmul(cb, hm)));
+          v[i] = make_double2(w0.x - w1.y, w0.y + w1.x);
+        }
+      });
+      fft<M, E, +1>(v, t, xb, twM, sync);
+#pragma unroll
       for (int i = 0; i < E; ++i) v[i] = make_double2(a0[i] * v[i].x, a1[i] * v[i].y);
       fft<M, E, -1>(v, t, xb, twM, sync);
+      // separate the pair's real-data spectra through v_{m-k}, recombine
 #pragma unroll
       for (int i = 0; i < E; ++i) xb[t + T * i] = v[i];
       sync();
-#pragma unroll
-      for (int i = 0; i < E; ++i) {
+      za = ldtw(&tw4M[r0 * t]);
+      zb = ldtw(&tw4M[(r0 + 1) * t]);
+      static_for<E>([&](auto I) {
+        constexpr int i = decltype(I)::value;
         const int k = t + T * i;
         const double2 a = v[i], b = cconj(xb[(M - k) & (M - 1)]);
         const double2 pp0 = cscale(cadd(a, b), 0.5);
         const double2 d = csub(a, b);
         const double2 pp1 = make_double2(0.5 * d.y, -0.5 * d.x);
-        const double2 ct = cadd(cmulc(pp0, ldtw(&tw4M[r0 * k])), cmulc(pp1, ldtw(&tw4M[(r0 + 1) * k])));
-        if (r0 == 0) fw[k] = ct;                                   // partial sum of residues 0, 1
+        const double2 ct = cadd(cmulc(pp0, twc<r0 * i, 4 * E, +1>(za)), cmulc(pp1, twc<(r0 + 1) * i, 4 * E, +1>(zb)));
+        if constexpr (r0 == 0) fw[k] = ct;                         // partial sum of residues 0, 1
         else fw[k] = cscale(cadd(ldv(&fw[k]), ct), inv);           // + residues 2, 3, then 1/(4m)
-      }
+      });
       sync();
-    }
+    };
+    pair(std::integral_constant<int, 0>{});
+    pair(std::integral_constant<int, 2>{});
   }
 }
 

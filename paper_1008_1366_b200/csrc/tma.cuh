@@ -48,6 +48,11 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src
       : "memory");
 }
 
+// bulk prefetch of a global range into L2 (no destination, no completion)
+__device__ __forceinline__ void prefetch_l2(const void* gmem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem_src), "r"(bytes) : "memory");
+}
+
 }  // namespace idc
 
 namespace idc {
