@@ -163,10 +163,26 @@ IDC_API size_t idc_dist_workspace_bytes(idc_kind k, size_t mx, size_t my, size_t
 IDC_API idc_status idc_cconv3d_dist(void* comm, idc_c128* f, idc_c128* g, size_t mx, size_t my, size_t mz,
                             void* work, size_t work_bytes, idc_stream stream);
 
+/* Distributed hconv3d (centered Hermitian 3D, P:891-897 with AMB-9; the
+ * decomposition is ours, AMB-19).  The global (2mx-1) x (2my-1) x mz arrays
+ * are padded to 2mx x-planes (the extra last plane is never read and its
+ * output is unspecified); rank r holds planes [r*2mx/P, (r+1)*2mx/P) --
+ * result in place, same layout.  Requires P a power of two dividing 2mx and
+ * 3my, and mx, my, mz >= 2.  Internally: fft0padBackward along the locally
+ * complete centered y axis (3my y-residues), ncclAlltoAll, Function conv2
+ * on the (x, z) plane of every owned y-residue, ncclAlltoAll
+ * back, fft0padForward along y.  Workspace: idc_dist_workspace_bytes(
+ * IDC_HCONV3D, ...).  Errors as idc_cconv3d_dist. */
+IDC_API idc_status idc_hconv3d_dist(void* comm, idc_c128* f, idc_c128* g, size_t mx, size_t my, size_t mz,
+                            void* work, size_t work_bytes, idc_stream stream);
+
 /* Host-side plan of the decomposition (no GPU needed): out[0..5] =
  * {local x planes nx, y-residues per rank nres, elements per peer block,
  * first local plane x0, first owned residue q0, elements per y-stream S}. */
 IDC_API idc_status idc_dist_plan(size_t mx, size_t my, size_t mz, int nranks, int rank, long long* out);
+/* Same for k = IDC_CCONV3D or IDC_HCONV3D (idc_dist_plan == IDC_CCONV3D). */
+IDC_API idc_status idc_dist_plan_kind(idc_kind k, size_t mx, size_t my, size_t mz, int nranks, int rank,
+                                      long long* out);
 
 /* Single-GPU emulation of nranks ranks (validation of the P > 1 path without
  * P GPUs): f_slabs[r], g_slabs[r] are device pointers to rank r's x-slabs;
@@ -174,6 +190,9 @@ IDC_API idc_status idc_dist_plan(size_t mx, size_t my, size_t mz, int nranks, in
  * compute phases are exactly those of idc_cconv3d_dist. */
 IDC_API size_t idc_dist_emulated_workspace_bytes(size_t mx, size_t my, size_t mz, int nranks);
 IDC_API idc_status idc_cconv3d_dist_emulated(int nranks, idc_c128** f_slabs, idc_c128** g_slabs, size_t mx,
+                                             size_t my, size_t mz, void* work, size_t work_bytes, idc_stream stream);
+IDC_API size_t idc_dist_emulated_workspace_bytes_kind(idc_kind k, size_t mx, size_t my, size_t mz, int nranks);
+IDC_API idc_status idc_hconv3d_dist_emulated(int nranks, idc_c128** f_slabs, idc_c128** g_slabs, size_t mx,
                                              size_t my, size_t mz, void* work, size_t work_bytes, idc_stream stream);
 
 /* ---- synthetic inputs (not part of the method) -------------------------- */

@@ -48,6 +48,11 @@ SIGNATURES = {
     "idc_dist_emulated_workspace_bytes": ([_S, _S, _S, _I], _S),
     "idc_cconv3d_dist_emulated": ([_I, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), _S, _S, _S,
                                    _P, _S, _P], _I),
+    "idc_hconv3d_dist": ([_P, _P, _P, _S, _S, _S, _P, _S, _P], _I),
+    "idc_dist_plan_kind": ([_I, _S, _S, _S, _I, _I, ctypes.POINTER(ctypes.c_longlong)], _I),
+    "idc_dist_emulated_workspace_bytes_kind": ([_I, _S, _S, _S, _I], _S),
+    "idc_hconv3d_dist_emulated": ([_I, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), _S, _S, _S,
+                                   _P, _S, _P], _I),
 }
 
 _lib = None
@@ -230,10 +235,12 @@ def fill_uniform(out, array_id: int, seed: int, start: int = 0, stream=None):
 
 # ------------------------------------------------------ distributed 3D --
 
-def dist_plan(mx: int, my: int, mz: int, nranks: int, rank: int) -> dict:
-    """Host-side decomposition plan (pure logic in the C library, no GPU)."""
+def dist_plan(mx: int, my: int, mz: int, nranks: int, rank: int, kind: int = None) -> dict:
+    """Host-side decomposition plan (pure logic in the C library, no GPU).
+    kind = CCONV3D (default) or HCONV3D."""
     out = (ctypes.c_longlong * 6)()
-    _check(lib().idc_dist_plan(mx, my, mz, nranks, rank, out), "idc_dist_plan")
+    k = CCONV3D if kind is None else kind
+    _check(lib().idc_dist_plan_kind(k, mx, my, mz, nranks, rank, out), "idc_dist_plan_kind")
     return dict(nx=out[0], nres=out[1], blk=out[2], x0=out[3], q0=out[4], S=out[5])
 
 
@@ -267,29 +274,47 @@ class Comm:
             self.handle = ctypes.c_void_p()
 
 
+def _dist(kind, name, comm, f, g, mx, my, mz, work, stream):
+    _prep([f, g])
+    nb = int(lib().idc_dist_workspace_bytes(kind, mx, my, mz, comm.size))
+    if nb == 0:
+        raise IdcError(ERR_UNSUPPORTED, name)
+    w, wb = _workspace(nb, f.device, work)
+    _check(getattr(lib(), name)(comm.handle, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(g.data_ptr()),
+                                mx, my, mz, ctypes.c_void_p(w.data_ptr()), wb, _stream_ptr(stream, f.device)), name)
+    return f
+
+
 def cconv3d_dist(comm: Comm, f, g, mx: int, my: int, mz: int, work=None, stream=None):
     """Distributed cconv3d on this rank's x-slab f, g (shape (mx/P, my, mz))."""
-    _prep([f, g])
-    nb = int(lib().idc_dist_workspace_bytes(CCONV3D, mx, my, mz, comm.size))
+    return _dist(CCONV3D, "idc_cconv3d_dist", comm, f, g, mx, my, mz, work, stream)
+
+
+def hconv3d_dist(comm: Comm, f, g, mx: int, my: int, mz: int, work=None, stream=None):
+    """Distributed hconv3d on this rank's x-slab f, g (shape (2mx/P, 2my-1, mz)
+    of the global array padded to 2mx x-planes; the padding plane is never read)."""
+    return _dist(HCONV3D, "idc_hconv3d_dist", comm, f, g, mx, my, mz, work, stream)
+
+
+def _emulated(kind, name, f_slabs, g_slabs, mx, my, mz, stream):
+    P = len(f_slabs)
+    _prep(list(f_slabs) + list(g_slabs))
+    nb = int(lib().idc_dist_emulated_workspace_bytes_kind(kind, mx, my, mz, P))
     if nb == 0:
-        raise IdcError(ERR_UNSUPPORTED, "idc_cconv3d_dist")
-    w, wb = _workspace(nb, f.device, work)
-    _check(lib().idc_cconv3d_dist(comm.handle, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(g.data_ptr()),
-                                  mx, my, mz, ctypes.c_void_p(w.data_ptr()), wb, _stream_ptr(stream, f.device)),
-           "idc_cconv3d_dist")
-    return f
+        raise IdcError(ERR_UNSUPPORTED, name)
+    w = torch.empty(nb, dtype=torch.uint8, device=f_slabs[0].device)
+    fp = (ctypes.c_void_p * P)(*[a.data_ptr() for a in f_slabs])
+    gp = (ctypes.c_void_p * P)(*[a.data_ptr() for a in g_slabs])
+    _check(getattr(lib(), name)(P, fp, gp, mx, my, mz, ctypes.c_void_p(w.data_ptr()), nb,
+                                _stream_ptr(stream, f_slabs[0].device)), name)
+    return f_slabs
 
 
 def cconv3d_dist_emulated(f_slabs, g_slabs, mx: int, my: int, mz: int, stream=None):
     """Single-GPU emulation of len(f_slabs) ranks (validation of the P > 1 path)."""
-    P = len(f_slabs)
-    _prep(list(f_slabs) + list(g_slabs))
-    nb = int(lib().idc_dist_emulated_workspace_bytes(mx, my, mz, P))
-    if nb == 0:
-        raise IdcError(ERR_UNSUPPORTED, "idc_cconv3d_dist_emulated")
-    w = torch.empty(nb, dtype=torch.uint8, device=f_slabs[0].device)
-    fp = (ctypes.c_void_p * P)(*[a.data_ptr() for a in f_slabs])
-    gp = (ctypes.c_void_p * P)(*[a.data_ptr() for a in g_slabs])
-    _check(lib().idc_cconv3d_dist_emulated(P, fp, gp, mx, my, mz, ctypes.c_void_p(w.data_ptr()), nb,
-                                           _stream_ptr(stream, f_slabs[0].device)), "idc_cconv3d_dist_emulated")
-    return f_slabs
+    return _emulated(CCONV3D, "idc_cconv3d_dist_emulated", f_slabs, g_slabs, mx, my, mz, stream)
+
+
+def hconv3d_dist_emulated(f_slabs, g_slabs, mx: int, my: int, mz: int, stream=None):
+    """Single-GPU emulation of the distributed hconv3d (slabs of 2mx/P planes)."""
+    return _emulated(HCONV3D, "idc_hconv3d_dist_emulated", f_slabs, g_slabs, mx, my, mz, stream)

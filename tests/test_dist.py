@@ -32,6 +32,30 @@ def test_decomposition_gloo(tmp_path, world, shape):
     assert rel_l2(res, direct.cconv3d(f, g)) < 1e-13
 
 
+@pytest.mark.parametrize("world,shape", [(2, (2, 2, 4)), (2, (4, 2, 2)), (4, (4, 4, 2))])
+def test_hermitian_decomposition_gloo(tmp_path, world, shape):
+    port = 29900 + (os.getpid() % 50) * 8 + world
+    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "dist_worker.py"), str(r), str(world), str(port),
+                               ",".join(map(str, shape)), str(tmp_path), "herm"]) for r in range(world)]
+    for p in procs:
+        assert p.wait(timeout=300) == 0
+    res = np.concatenate([np.load(tmp_path / f"rank{r}.npy") for r in range(world)], axis=0)[:-1]  # drop padding plane
+    f, g = synthgen.hconv3d_inputs(*shape)
+    assert rel_l2(res, direct.hconv3d(f, g)) < 1e-13
+
+
+def test_hermitian_plan_properties():
+    from paper_1008_1366_b200 import idconv
+    for (mx, my, mz, P) in [(512, 512, 512, 8), (4, 8, 4, 8), (2, 2, 2, 2)]:
+        plans = [idconv.dist_plan(mx, my, mz, P, r, kind=idconv.HCONV3D) for r in range(P)]
+        assert sum(p["nx"] for p in plans) == 2 * mx                 # 2mx-1 planes + 1 padding plane
+        assert sum(p["nres"] for p in plans) == 3 * my               # every centered y-residue once
+        assert all(p["S"] == p["nx"] * (2 * my - 1) * mz for p in plans)
+    with pytest.raises(Exception):
+        idconv.dist_plan(8, 2, 8, 4, 0, kind=idconv.HCONV3D)         # P must divide 3my
+    assert idconv.workspace_bytes(idconv.HCONV3D, 4, 4, 4) > 0
+
+
 def test_plan_properties():
     from paper_1008_1366_b200 import idconv
     for (mx, my, mz, P) in [(512, 512, 512, 8), (16, 8, 4, 4), (8, 8, 8, 1)]:
@@ -85,6 +109,55 @@ def test_nccl_single_rank_gpu():
         idconv.cconv3d_dist(comm, F, G, *shape)
         torch.cuda.synchronize()
         assert rel_l2(F.cpu().numpy(), direct.cconv3d(f, g)) < 1e-14
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def _herm_slabs(f, P):
+    fp = np.concatenate([f, np.zeros_like(f[:1])], axis=0)           # 2mx planes (last = padding)
+    nx = fp.shape[0] // P
+    return [np.ascontiguousarray(fp[r * nx:(r + 1) * nx]) for r in range(P)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P,shape", [(1, (4, 4, 4)), (2, (4, 2, 8)), (4, (4, 4, 4)), (8, (4, 8, 4)),
+                                     (8, (32, 16, 16))])
+def test_hermitian_emulated_ranks_gpu(P, shape):
+    import torch
+    from paper_1008_1366_b200 import idconv
+    mx, my, mz = shape
+    f, g = synthgen.hconv3d_inputs(*shape)
+    F = [torch.from_numpy(a).cuda() for a in _herm_slabs(f, P)]
+    G = [torch.from_numpy(a).cuda() for a in _herm_slabs(g, P)]
+    idconv.hconv3d_dist_emulated(F, G, mx, my, mz)
+    res = np.concatenate([a.cpu().numpy() for a in F], axis=0)[:-1]
+    if f.size <= 4096:
+        assert rel_l2(res, direct.hconv3d(f, g)) < 1e-14
+    else:
+        idx = np.random.default_rng(5).choice(res.size, 64, replace=False)
+        assert rel_l2(res.reshape(-1)[idx], direct.hconv3d_at(f, g, idx)) < 1e-14
+    F1, G1 = torch.from_numpy(f.copy()).cuda(), torch.from_numpy(g.copy()).cuda()
+    idconv.hconv3d(F1, G1)
+    assert rel_l2(res, F1.cpu().numpy()) < 1e-14
+
+
+@pytest.mark.gpu
+def test_hermitian_nccl_single_rank_gpu():
+    import torch
+    import torch.distributed as dist
+    from paper_1008_1366_b200 import idconv
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = "29733"
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = idconv.Comm()
+        shape = (8, 4, 16)
+        f, g = synthgen.hconv3d_inputs(*shape)
+        F, G = [torch.from_numpy(a).cuda() for a in _herm_slabs(f, 1)], [torch.from_numpy(a).cuda() for a in _herm_slabs(g, 1)]
+        idconv.hconv3d_dist(comm, F[0], G[0], *shape)
+        torch.cuda.synchronize()
+        assert rel_l2(F[0].cpu().numpy()[:-1], direct.hconv3d(f, g)) < 1e-14
         comm.close()
     finally:
         dist.destroy_process_group()
