@@ -12,6 +12,7 @@
 #include "fft_dev.cuh"
 #include "kernels.cuh"
 #include "tables.cuh"
+#include "tma.cuh"
 
 namespace idc {
 
@@ -25,6 +26,9 @@ struct Cfg2 {
   static constexpr bool NAMED = (T % 32 == 0) && G > 1;
   // cap registers at 128 per thread: 16 warps per SM for 512-thread CTAs,
   // two 256-thread CTAs per SM otherwise
+#ifndef IDC_ROWS_PREFETCH
+#define IDC_ROWS_PREFETCH 1
+#endif
 #ifndef IDC_ROWS_REGS
 #define IDC_ROWS_REGS 255
 #endif
@@ -86,6 +90,12 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
     const double2* fr = f + (ok ? row : 0) * (long)M;
     const double2* gr = g + (ok ? row : 0) * (long)M;
 #ifndef IDC_CCONV_SMEM_STASH
+    // the next rows of this group: bulk prefetch into L2 (hides the HBM
+    // latency of the first loads of the next iteration)
+    if (IDC_ROWS_PREFETCH && t == 0 && row + (long)gridDim.x * G < nrows) {
+      prefetch_l2(f + (row + (long)gridDim.x * G) * (long)M, M * 16u);
+      prefetch_l2(g + (row + (long)gridDim.x * G) * (long)M, M * 16u);
+    }
     // Every intermediate in registers (at most three E-vectors live): no
     // shared-memory stash traffic, only the FFT exchanges.
     double2 x[E], y[E], z[E];

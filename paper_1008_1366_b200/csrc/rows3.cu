@@ -191,17 +191,19 @@ k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const doub
     double2* fw = f + row * (long)M;   // staged: free to serve as the partial-sum scratch
     if (t == 0 && row + stride < nrows) prefetch_l2(h + (row + stride) * (long)M, M * 16u);
     double a0[E], a1[E];
-    // one residue pair (r0, r0 + 1), r0 = 0 or 2, with compile-time roots
-    // zeta_{4m}^{rk} = zeta_{4m}^{rt} x zeta_{4E}^{ri} and c_r = (-i)^r
-    auto pair = [&](auto R0) {
+    // Residue pairs (r0, r0 + 1), r0 = 0, 2, in a runtime loop so that the
+    // four transforms of a pair are instantiated once (instruction-cache
+    // footprint); only the small split / pack / recombine stages are
+    // specialised on r0 for their compile-time roots
+    // zeta_{4m}^{rk} = zeta_{4m}^{rt} x zeta_{4E}^{ri}, c_r = (-i)^r.
+    // (za, zb are re-loaded per stage -- volatile loads -- so that the derived
+    // per-element roots are recomputed, not kept live across transforms.)
+    double2 v[E], w[E];
+    auto split = [&](auto R0) {   // both f/g residue streams of the pair, one read of the staged row
       constexpr int r0 = decltype(R0)::value;
       const double2 ca = r0 == 0 ? make_double2(1, 0) : make_double2(-1, 0);   // (-i)^{r0}
       const double2 cb = r0 == 0 ? make_double2(0, -1) : make_double2(0, 1);   // (-i)^{r0+1}
-      // (za, zb are re-loaded per stage -- volatile loads -- so that the
-      // derived per-element roots are recomputed, not kept live across FFTs)
-      double2 v[E], w[E];
-      double2 za = ldtw(&tw4M[r0 * t]), zb = ldtw(&tw4M[(r0 + 1) * t]);
-      // both f/g residue streams of the pair from one read of the staged row
+      const double2 za = ldtw(&tw4M[r0 * t]), zb = ldtw(&tw4M[(r0 + 1) * t]);
       static_for<E>([&](auto I) {
         constexpr int i = decltype(I)::value;
         const int k = t + T * i;
@@ -215,23 +217,12 @@ k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const doub
           w[i] = cmul(twc<(r0 + 1) * i, 4 * E, +1>(zb), cadd(P, cmul(cb, R)));
         }
       });
-      if constexpr (r0 == 2) {  // last read of the staged row: prefetch the next one
-        sync();
-        if (t == 0 && row + stride < nrows) {
-          mbar_arrive_expect_tx(bar, 2u * M * 16u);
-          tma_load_1d(F, f + (row + stride) * (long)M, M * 16u, bar);
-          tma_load_1d(Gs, g + (row + stride) * (long)M, M * 16u, bar);
-        }
-      }
-      fft<M, E, +1>(v, t, xb, twM, sync);
-#pragma unroll
-      for (int i = 0; i < E; ++i) a0[i] = v[i].x * v[i].y;
-      fft<M, E, +1>(w, t, xb, twM, sync);
-#pragma unroll
-      for (int i = 0; i < E; ++i) a1[i] = w[i].x * w[i].y;
-      // h packed across the residue pair: w^h_{r0} + i w^h_{r0+1}
-      za = ldtw(&tw4M[r0 * t]);
-      zb = ldtw(&tw4M[(r0 + 1) * t]);
+    };
+    auto hpack = [&](auto R0) {   // h packed across the pair: w^h_{r0} + i w^h_{r0+1}
+      constexpr int r0 = decltype(R0)::value;
+      const double2 ca = r0 == 0 ? make_double2(1, 0) : make_double2(-1, 0);
+      const double2 cb = r0 == 0 ? make_double2(0, -1) : make_double2(0, 1);
+      const double2 za = ldtw(&tw4M[r0 * t]), zb = ldtw(&tw4M[(r0 + 1) * t]);
       static_for<E>([&](auto I) {
         constexpr int i = decltype(I)::value;
         const int k = t + T * i;
@@ -245,16 +236,10 @@ k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const doub
           v[i] = make_double2(w0.x - w1.y, w0.y + w1.x);
         }
       });
-      fft<M, E, +1>(v, t, xb, twM, sync);
-#pragma unroll
-      for (int i = 0; i < E; ++i) v[i] = make_double2(a0[i] * v[i].x, a1[i] * v[i].y);
-      fft<M, E, -1>(v, t, xb, twM, sync);
-      // separate the pair's real-data spectra through v_{m-k}, recombine
-#pragma unroll
-      for (int i = 0; i < E; ++i) xb[t + T * i] = v[i];
-      sync();
-      za = ldtw(&tw4M[r0 * t]);
-      zb = ldtw(&tw4M[(r0 + 1) * t]);
+    };
+    auto recombine = [&](auto R0) {   // separate the pair's real-data spectra via v_{m-k}
+      constexpr int r0 = decltype(R0)::value;
+      const double2 za = ldtw(&tw4M[r0 * t]), zb = ldtw(&tw4M[(r0 + 1) * t]);
       static_for<E>([&](auto I) {
         constexpr int i = decltype(I)::value;
         const int k = t + T * i;
@@ -266,10 +251,38 @@ k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const doub
         if constexpr (r0 == 0) fw[k] = ct;                         // partial sum of residues 0, 1
         else fw[k] = cscale(cadd(ldv(&fw[k]), ct), inv);           // + residues 2, 3, then 1/(4m)
       });
-      sync();
     };
-    pair(std::integral_constant<int, 0>{});
-    pair(std::integral_constant<int, 2>{});
+#pragma unroll 1
+    for (int r0 = 0; r0 < 4; r0 += 2) {
+      if (r0 == 0) split(std::integral_constant<int, 0>{});
+      else split(std::integral_constant<int, 2>{});
+      if (r0 == 2) {  // last read of the staged row: prefetch the next one
+        sync();
+        if (t == 0 && row + stride < nrows) {
+          mbar_arrive_expect_tx(bar, 2u * M * 16u);
+          tma_load_1d(F, f + (row + stride) * (long)M, M * 16u, bar);
+          tma_load_1d(Gs, g + (row + stride) * (long)M, M * 16u, bar);
+        }
+      }
+      fft<M, E, +1>(v, t, xb, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) a0[i] = v[i].x * v[i].y;
+      fft<M, E, +1>(w, t, xb, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) a1[i] = w[i].x * w[i].y;
+      if (r0 == 0) hpack(std::integral_constant<int, 0>{});
+      else hpack(std::integral_constant<int, 2>{});
+      fft<M, E, +1>(v, t, xb, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) v[i] = make_double2(a0[i] * v[i].x, a1[i] * v[i].y);
+      fft<M, E, -1>(v, t, xb, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) xb[t + T * i] = v[i];
+      sync();
+      if (r0 == 0) recombine(std::integral_constant<int, 0>{});
+      else recombine(std::integral_constant<int, 2>{});
+      sync();
+    }
   }
 }
 
