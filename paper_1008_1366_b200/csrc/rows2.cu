@@ -109,13 +109,12 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
 #pragma unroll
     for (int i = 0; i < E; ++i) x[i] = cmul(x[i], y[i]);
     // r = 1: zeta_{2m}^k-shifted streams
-    // (per-element zeta_{2m}^k table loads measured faster here than the
-    // compile-time root products: this kernel is closer to fp64-bound)
-#pragma unroll
-    for (int i = 0; i < E; ++i) y[i] = cmul(ldv(&fr[t + T * i]), ldtw(&tw2M[t + T * i]));
+    // zeta_{2m}^k, k = t + T i: zeta_{2m}^t (one table value) x zeta_{2E}^i
+    // (immediate); zt is shared by both splits and the recombination
+    const double2 zt = ldtw(&tw2M[t]);
+    for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { y[i] = cmul(ldv(&fr[t + T * i]), w); });
     fft<M, E, +1>(y, t, xb, twM, sync);
-#pragma unroll
-    for (int i = 0; i < E; ++i) z[i] = cmul(ldv(&gr[t + T * i]), ldtw(&tw2M[t + T * i]));
+    for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { z[i] = cmul(ldv(&gr[t + T * i]), w); });
     fft<M, E, +1>(z, t, xb, twM, sync);
 #pragma unroll
     for (int i = 0; i < E; ++i) y[i] = cmul(y[i], z[i]);
@@ -124,8 +123,9 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
     fft<M, E, -1>(x, t, xb, twM, sync);
     if (ok) {
       double2* fw = f + row * (long)M;
-#pragma unroll
-      for (int i = 0; i < E; ++i) fw[t + T * i] = cscale(cadd(x[i], cmulc(y[i], ldtw(&tw2M[t + T * i]))), inv);
+      for_roots<2 * E, 1, -1, E>(cconj(zt), [&](int i, double2 w) {       // zeta_{2m}^{-k}
+        fw[t + T * i] = cscale(cadd(x[i], cmul(y[i], w)), inv);
+      });
     }
 #else
     double2 v[E];
