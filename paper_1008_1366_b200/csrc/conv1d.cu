@@ -348,7 +348,7 @@ template <int M>
 cudaError_t cconv_m(double2* f, double2* g, long nrows, double2* work, cudaStream_t s) {
   using C = RowCfg<M>;
   using SC = StashCfg<M, kCconvStash<M>>;
-  const double2* twM = zeta_table(M);
+  const double2* twM = pass_table(M, RowCfg<M>::E);
   const double2* tw2M = zeta_table(2 * M);
   if (!twM || !tw2M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw2M, &work};
@@ -359,7 +359,7 @@ template <int M>
 cudaError_t hconv_m(double2* f, double2* g, long nrows, double2* work, cudaStream_t s) {
   using C = RowCfg<M>;
   using SC = StashCfg<M, kHconvStash<M>>;
-  const double2* twM = zeta_table(M);
+  const double2* twM = pass_table(M, RowCfg<M>::E);
   const double2* tw3M = zeta_table(3 * M);
   if (!twM || !tw3M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw3M, &work};
@@ -370,7 +370,7 @@ template <int M>
 cudaError_t tconv_m(double2* f, double2* g, double2* h, long nrows, double2* work, cudaStream_t s) {
   using C = RowCfg<M>;
   using SC = StashCfg<M, kTconvStash<M>>;
-  const double2* twM = zeta_table(M);
+  const double2* twM = pass_table(M, RowCfg<M>::E);
   const double2* tw4M = zeta_table(4 * M);
   if (!twM || !tw4M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &h, &nrows, &twM, &tw4M, &work};

@@ -242,6 +242,26 @@ __device__ __forceinline__ int xpad(int pos) {
 template <int N, int E>
 __host__ __device__ constexpr int xbuf_elems() { return N <= E ? 0 : N + N / E; }
 
+// Pass twiddle tables (one per (N, E), built on the host by pass_table()):
+// for every pass with NS > 1 (radix R, Q = 4, 2 or 1 as below), a block of
+// (Q - 1 + R/Q - 1) rows of NS entries: row c - 1 (c = 1..Q-1) holds
+// w^c and row Q - 2 + a (a = 1..R/Q-1) holds w^{Qa}, w = zeta_N^{j N/(NS R)},
+// at column j.  Lanes read consecutive j: contiguous 16-byte loads (a gather
+// from the full zeta_N table touched up to 32 cache lines per warp load).
+__host__ __device__ constexpr int pass_q(int R) { return R >= 16 ? 4 : (R >= 4 ? 2 : 1); }
+__host__ __device__ constexpr int pass_radix(int N, int E, int NS) { return (NS * E <= N) ? E : N / NS; }
+template <int N, int E>
+__host__ __device__ constexpr int pass_tab_offset(int ns_target) {
+  int off = 0;
+  for (int NS = 1; NS < N;) {
+    const int R = pass_radix(N, E, NS);
+    if (NS == ns_target) return off;
+    if (NS > 1) off += (pass_q(R) - 1 + R / pass_q(R) - 1) * NS;
+    NS *= R;
+  }
+  return off;
+}
+
 // One Stockham radix-R pass; twiddles then DFT_R, data stays in registers.
 template <int N, int E, int R, int NS, int SIGN>
 __device__ __forceinline__ void pass_compute(double2 (&v)[E], int t, const double2* __restrict__ tw) {
@@ -253,16 +273,16 @@ __device__ __forceinline__ void pass_compute(double2 (&v)[E], int t, const doubl
     for (int r = 0; r < R; ++r) x[r] = v[b + r * B];
     if constexpr (NS > 1) {
       // w^r, w = exp(2 pi i jm/(NS R)), r = Q a + c: load w^c (c < Q) and
-      // w^{Qa} (a < R/Q), one complex product for the mixed terms
+      // w^{Qa} (a < R/Q) from the pass table
       const int jm = (t + T * b) & (NS - 1);
-      constexpr int STEP = N / (NS * R);
       {
-      constexpr int Q = R >= 16 ? 4 : (R >= 4 ? 2 : 1);
+      constexpr int Q = pass_q(R);
+      const double2* tp = tw + pass_tab_offset<N, E>(NS) + jm;
       double2 lo[Q], hi[R / Q];
 #pragma unroll
-      for (int c = 1; c < Q; ++c) lo[c] = ldtw_pass(&tw[c * jm * STEP]);
+      for (int c = 1; c < Q; ++c) lo[c] = ldtw_pass(&tp[(c - 1) * NS]);
 #pragma unroll
-      for (int a = 1; a < R / Q; ++a) hi[a] = ldtw_pass(&tw[Q * a * jm * STEP]);
+      for (int a = 1; a < R / Q; ++a) hi[a] = ldtw_pass(&tp[(Q - 2 + a) * NS]);
 #ifndef IDC_PASS_TW_PRODUCT
       // x[Qa + c] * w^c * w^{Qa}: two multiplies per element instead of
       // forming every w^r = w^{Qa} w^c first (same multiply count, but no

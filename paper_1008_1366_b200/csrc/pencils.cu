@@ -249,7 +249,7 @@ cudaError_t pad_bwd_n(double2* f, double2* g, double2* U, double2* V, long ncols
                       long ustride, cudaStream_t s) {
   constexpr int E = PTune<N>::E, W = PTune<N>::W;
   using C = PCfg<N, E, W>;
-  const double2* twN = zeta_table(N);
+  const double2* twN = pass_table(N, PTune<N>::E);
   const double2* tw2N = zeta_table(2 * N);
   if (!twN || !tw2N) return cudaErrorMemoryAllocation;
   Pencil pc{ncols, bstride, ustride};
@@ -263,7 +263,7 @@ cudaError_t pad_fwd_n(double2* f, const double2* U, long ncols, long batch, long
                       cudaStream_t s) {
   constexpr int E = PTune<N>::E, W = PTune<N>::W;
   using C = PCfg<N, E, W>;
-  const double2* twN = zeta_table(N);
+  const double2* twN = pass_table(N, PTune<N>::E);
   const double2* tw2N = zeta_table(2 * N);
   if (!twN || !tw2N) return cudaErrorMemoryAllocation;
   Pencil pc{ncols, bstride, ustride};
@@ -277,7 +277,7 @@ cudaError_t pad0_bwd_n(double2* f, double2* g, double2* U, double2* V, long ncol
                        long ustride, cudaStream_t s) {
   constexpr int E = PTune<N>::E, W = PTune<N>::W;
   using C = PCfg<N, E, W>;
-  const double2* twN = zeta_table(N);
+  const double2* twN = pass_table(N, PTune<N>::E);
   const double2* tw3N = zeta_table(3 * N);
   if (!twN || !tw3N) return cudaErrorMemoryAllocation;
   Pencil pc{ncols, bstride, ustride};
@@ -291,7 +291,7 @@ cudaError_t pad0_fwd_n(double2* f, const double2* U, long ncols, long batch, lon
                        cudaStream_t s) {
   constexpr int E = PTune<N>::E, W = PTune<N>::W;
   using C = PCfg<N, E, W>;
-  const double2* twN = zeta_table(N);
+  const double2* twN = pass_table(N, PTune<N>::E);
   const double2* tw3N = zeta_table(3 * N);
   if (!twN || !tw3N) return cudaErrorMemoryAllocation;
   Pencil pc{ncols, bstride, ustride};

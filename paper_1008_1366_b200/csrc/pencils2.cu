@@ -443,7 +443,7 @@ template <int N>
 cudaError_t pad_bwd_tma(double2* f, double2* g, double2* U, double2* V, long ncols, long batch, long bstride,
                         long ustride, cudaStream_t s) {
   using C = TCfg<N>;
-  const double2* twN = zeta_table(N);
+  const double2* twN = pass_table(N, TCfg<N>::E);
   const double2* tw2N = zeta_table(2 * N);
   if (!twN || !tw2N) return cudaErrorMemoryAllocation;
   CUtensorMap mf, mg;
@@ -459,7 +459,7 @@ template <int N>
 cudaError_t pad_fwd_tma(double2* f, const double2* U, long ncols, long batch, long bstride, long ustride,
                         cudaStream_t s) {
   using C = TCfg<N>;
-  const double2* twN = zeta_table(N);
+  const double2* twN = pass_table(N, TCfg<N>::E);
   const double2* tw2N = zeta_table(2 * N);
   if (!twN || !tw2N) return cudaErrorMemoryAllocation;
   CUtensorMap mf, mu;
@@ -476,7 +476,7 @@ cudaError_t pad0_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nc
                          long ustride, cudaStream_t s) {
   using C = TCfg<N>;
   constexpr int R2 = ((2 * N - 1 + C::BR - 1) / C::BR) * C::BR;
-  const double2* twN = zeta_table(N);
+  const double2* twN = pass_table(N, TCfg<N>::E);
   const double2* tw3N = zeta_table(3 * N);
   if (!twN || !tw3N) return cudaErrorMemoryAllocation;
   CUtensorMap mf, mg;
@@ -492,7 +492,7 @@ template <int N>
 cudaError_t pad0_fwd_tma(double2* f, const double2* U, long ncols, long batch, long bstride, long ustride,
                          cudaStream_t s) {
   using C = TCfg<N>;
-  const double2* twN = zeta_table(N);
+  const double2* twN = pass_table(N, TCfg<N>::E);
   const double2* tw3N = zeta_table(3 * N);
   if (!twN || !tw3N) return cudaErrorMemoryAllocation;
   CUtensorMap mf, mu, mu1;

@@ -374,7 +374,7 @@ template <int M>
 cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s) {
   constexpr int E = Tune<M>::E, G = Tune<M>::G;
   using C = Cfg2<M, E, G>;
-  const double2* twM = zeta_table(M);
+  const double2* twM = pass_table(M, Tune<M>::E);
   const double2* tw2M = zeta_table(2 * M);
   if (!twM || !tw2M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw2M};
@@ -390,7 +390,7 @@ template <int M>
 cudaError_t hconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s) {
   constexpr int E = Tune<M>::E, G = Tune<M>::G;
   using C = Cfg2<M, E, G>;
-  const double2* twM = zeta_table(M);
+  const double2* twM = pass_table(M, Tune<M>::E);
   const double2* tw3M = zeta_table(3 * M);
   if (!twM || !tw3M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw3M};
@@ -402,7 +402,7 @@ template <int M>
 cudaError_t tconv_rows2(double2* f, double2* g, double2* h, long nrows, cudaStream_t s) {
   constexpr int E = Tune<M>::E, G = Tune<M>::G;
   using C = Cfg2<M, E, G>;
-  const double2* twM = zeta_table(M);
+  const double2* twM = pass_table(M, Tune<M>::E);
   const double2* tw4M = zeta_table(4 * M);
   if (!twM || !tw4M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &h, &nrows, &twM, &tw4M};

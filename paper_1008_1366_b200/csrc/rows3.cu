@@ -303,7 +303,7 @@ cudaError_t launch3(K kernel, int threads, size_t smem, long nrows, int groups, 
 template <int M>
 cudaError_t hconv_rows3(double2* f, double2* g, long nrows, cudaStream_t s) {
   using C = Cfg3<M>;
-  const double2* twM = zeta_table(M);
+  const double2* twM = pass_table(M, Cfg3<M>::E);
   const double2* tw3M = zeta_table(3 * M);
   if (!twM || !tw3M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw3M};
@@ -313,7 +313,7 @@ cudaError_t hconv_rows3(double2* f, double2* g, long nrows, cudaStream_t s) {
 template <int M>
 cudaError_t tconv_rows3(double2* f, double2* g, double2* h, long nrows, cudaStream_t s) {
   using C = Cfg3<M>;
-  const double2* twM = zeta_table(M);
+  const double2* twM = pass_table(M, Cfg3<M>::E);
   const double2* tw4M = zeta_table(4 * M);
   if (!twM || !tw4M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &h, &nrows, &twM, &tw4M};

@@ -1,6 +1,8 @@
 // tables.cu -- twiddle-table cache, see tables.cuh.
 #include "tables.cuh"
 
+#include "fft_dev.cuh"
+
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -12,6 +14,7 @@ namespace idc {
 namespace {
 std::mutex g_mu;
 std::map<std::pair<int, int>, double2*> g_tables;  // (device, N) -> table
+std::map<std::pair<int, long>, double2*> g_ptables;  // (device, N * 65536 + E) -> pass table
 
 // exp(2 pi i k / N) with k reduced to the first octant so that cosl/sinl see
 // arguments in [0, pi/4] (symmetries are exact).
@@ -78,6 +81,43 @@ const double2* zeta_table(int N) {
     return nullptr;
   }
   g_tables[key] = d;
+  return d;
+}
+
+const double2* pass_table(int N, int E) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  if (E > N) E = N;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_pair(dev, (long)N * 65536 + E);
+  auto it = g_ptables.find(key);
+  if (it != g_ptables.end()) return it->second;
+  std::vector<double2> h;
+  for (int NS = 1; NS < N;) {
+    const int R = pass_radix(N, E, NS);
+    if (NS > 1) {
+      const int Q = pass_q(R);
+      const long STEP = N / ((long)NS * R);
+      auto put = [&](long mult) {
+        for (int j = 0; j < NS; ++j) {
+          double c, s;
+          root(mult * j * STEP, N, &c, &s);
+          h.push_back(make_double2(c, s));
+        }
+      };
+      for (int c = 1; c < Q; ++c) put(c);
+      for (int a = 1; a < R / Q; ++a) put((long)Q * a);
+    }
+    NS *= R;
+  }
+  if (h.empty()) h.push_back(make_double2(1.0, 0.0));
+  double2* d = nullptr;
+  if (cudaMalloc(&d, sizeof(double2) * h.size()) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, h.data(), sizeof(double2) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  g_ptables[key] = d;
   return d;
 }
 

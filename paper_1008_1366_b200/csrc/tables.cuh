@@ -17,4 +17,9 @@ namespace idc {
 // Returns nullptr on failure (allocation / copy error).
 const double2* zeta_table(int N);
 
+// Device pointer to the Stockham pass-twiddle table of an N-point FFT with E
+// elements per thread (layout: fft_dev.cuh, pass_tab_offset).  Same roots as
+// zeta_table(N), regrouped so that a warp's twiddle loads are contiguous.
+const double2* pass_table(int N, int E);
+
 }  // namespace idc
