@@ -38,13 +38,17 @@ size_t l2_bytes() {
   return (size_t)l2;
 }
 
-// slabs per group: keep f/g slabs + U2/V2 of a group within a fraction of L2
-// (IDC_SLAB_L2_FRAC, percent, default 50; experiments only)
+// slabs per group = (IDC_SLAB_L2_FRAC percent of L2) / (per-slab bytes of all
+// streams in flight).  Measured on B200 (profiles/): an
+// L2-resident group (50%: one 512^2 slab per stream, 512-row launches) is
+// 17% slower than groups of ~10-20 slabs whose launches fill the GPU several
+// times over -- launch granularity matters more than L2 residency here, so
+// the default budget is 10x L2 (frac 1000).
 long slab_group(size_t slab_bytes_all, long nslabs) {
   static long frac = -1;
   if (frac < 0) {
     const char* e = getenv("IDC_SLAB_L2_FRAC");
-    frac = e ? atol(e) : 50;
+    frac = e ? atol(e) : 1000;
   }
   long G = (long)((l2_bytes() * frac / 100) / std::max<size_t>(slab_bytes_all, 1));
   return std::max<long>(1, std::min<long>(G, nslabs));
