@@ -82,6 +82,11 @@ IDC_API const char* idc_status_string(idc_status s);
 /* Library version string, e.g. "idconv 0.1 sm_100a". */
 IDC_API const char* idc_version(void);
 
+/* Number of hot-path kernels this library has launched so far in this
+ * process (all devices, all calls; monotonic).  Instrumentation only: lets a
+ * caller count the kernels inside a timed region. */
+IDC_API long long idc_launch_count(void);
+
 /* Bytes of device workspace `work` the call of kind k needs for the given
  * sizes (unused sizes are ignored; pass 1).  1D: m0 = m.  2D: (m0, m1) =
  * (mx, my).  3D: (m0, m1, m2) = (mx, my, mz).  Returns 0 for unsupported

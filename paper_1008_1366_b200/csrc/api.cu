@@ -62,6 +62,8 @@ const char* idc_status_string(idc_status s) {
 
 const char* idc_version(void) { return "idconv 0.1 sm_100a fp64"; }
 
+long long idc_launch_count(void) { return idc::launch_count(); }
+
 size_t idc_workspace_bytes(idc_kind k, size_t m0, size_t m1, size_t m2, size_t batch) {
   switch (k) {
     case IDC_CCONV1D: return size_ok(m0, 1, 8192) ? idc::cconv_rows_work_bytes((int)m0) : 0;

@@ -9,6 +9,8 @@
 // P:1079-1083) live in registers / shared memory ("stash"), never in HBM,
 // except for m = 8192 where the stash spills to the caller's workspace
 // (L2-resident).
+#include <atomic>
+
 #include "fft_dev.cuh"
 #include "kernels.cuh"
 #include "tables.cuh"
@@ -42,6 +44,10 @@ template <int M> constexpr int kTconvStash = 2 * M;  // acc (M) + (a_r, a_r') pa
 int g_sms = 0;
 
 }  // namespace
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 int num_sms() {
   if (g_sms == 0) {
@@ -336,6 +342,7 @@ cudaError_t launch_persistent(K kernel, int threads, size_t smem, long nrows, in
   long grid = (long)num_sms() * per_sm;
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
+  count_launch();
   return cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s);
 }
 

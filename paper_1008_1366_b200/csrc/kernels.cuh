@@ -31,6 +31,12 @@ template <int M> cudaError_t tconv_rows2(double2* f, double2* g, double2* h, lon
 template <int M> cudaError_t hconv_rows3(double2* f, double2* g, long nrows, cudaStream_t s);
 template <int M> cudaError_t tconv_rows3(double2* f, double2* g, double2* h, long nrows, cudaStream_t s);
 
+// Count of hot-path kernel launches issued by this library (every launcher
+// calls count_launch() right before cudaLaunchKernel); read through the ABI
+// as idc_launch_count() so a benchmark can report its own kernel launches.
+void count_launch();
+long long launch_count();
+
 // Number of SMs of the current device (cached).
 int num_sms();
 

@@ -241,6 +241,7 @@ template <class K>
 cudaError_t launchp(K kernel, int threads, size_t smem, dim3 grid, cudaStream_t s, void** args) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  count_launch();
   return cudaLaunchKernel((const void*)kernel, grid, dim3(threads), args, smem, s);
 }
 

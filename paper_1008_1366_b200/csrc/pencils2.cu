@@ -420,6 +420,7 @@ cudaError_t launch_t(K kernel, int threads, size_t smem, long ntiles, cudaStream
   long grid = (long)num_sms() * per_sm;
   if (ntiles < grid) grid = ntiles;
   if (grid < 1) grid = 1;
+  count_launch();
   return cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s);
 }
 

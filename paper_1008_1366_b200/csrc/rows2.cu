@@ -354,6 +354,7 @@ cudaError_t launch2(K kernel, int threads, size_t smem, long nrows, int groups, 
   long grid = (long)num_sms() * per_sm;
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
+  count_launch();
   return cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s);
 }
 

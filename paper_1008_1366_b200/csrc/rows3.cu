@@ -296,6 +296,7 @@ cudaError_t launch3(K kernel, int threads, size_t smem, long nrows, int groups, 
   long grid = num_sms();
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
+  count_launch();
   return cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s);
 }
 }  // namespace

@@ -30,6 +30,7 @@ _P, _S, _I, _U64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint
 SIGNATURES = {
     "idc_status_string": ([_I], ctypes.c_char_p),
     "idc_version": ([], ctypes.c_char_p),
+    "idc_launch_count": ([], ctypes.c_longlong),
     "idc_workspace_bytes": ([_I, _S, _S, _S, _S], _S),
     "idc_cconv1d": ([_P, _P, _S, _S, _P, _S, _P], _I),
     "idc_hconv1d": ([_P, _P, _S, _S, _P, _S, _P], _I),
@@ -231,6 +232,11 @@ def fill_uniform(out, array_id: int, seed: int, start: int = 0, stream=None):
     _check(lib().idc_fill_uniform(ctypes.c_void_p(out.data_ptr()), out.numel(), seed, array_id, start,
                                   _stream_ptr(stream, out.device)), "idc_fill_uniform")
     return out
+
+
+def launch_count() -> int:
+    """Hot-path kernels launched by the library so far (idc_launch_count)."""
+    return int(lib().idc_launch_count())
 
 
 # ------------------------------------------------------ distributed 3D --

@@ -101,3 +101,23 @@ def test_no_cpu_fallback():
     f = torch.zeros(4, dtype=torch.complex128)
     with pytest.raises(Exception):
         idconv.cconv1d(f, f.clone())
+
+
+def test_launch_count_is_monotonic_without_gpu():
+    n0 = idconv.launch_count()
+    assert n0 >= 0 and idconv.launch_count() == n0          # no launches without calls
+
+
+@pytest.mark.gpu
+def test_launch_count_counts_hot_path_kernels():
+    import torch
+    f = torch.zeros((3, 64), dtype=torch.complex128, device="cuda")
+    g = torch.zeros_like(f)
+    n0 = idconv.launch_count()
+    idconv.cconv1d(f, g)                                     # one fused row kernel
+    assert idconv.launch_count() - n0 == 1
+    a = torch.zeros((16, 16), dtype=torch.complex128, device="cuda")
+    b = torch.zeros_like(a)
+    n1 = idconv.launch_count()
+    idconv.cconv2d(a, b)                                     # K5, K2 (x2), K6
+    assert idconv.launch_count() - n1 == 4
