@@ -361,6 +361,51 @@ __device__ __forceinline__ void fft(double2 (&v)[E], int t, double2* __restrict_
   fft_passes<N, E, 1, SIGN>(v, tl, xb, tw, sync, xs);
 }
 
+// Two independent N-point FFTs (same sign) in lockstep: each pass computes
+// both vectors' butterflies, then both are exchanged (v through xb, w through
+// xb2) under one pair of barriers -- half the barriers of two fft() calls and
+// twice the independent work between them.
+template <int N, int E, int NS, int SIGN, class Sync, class XS>
+__device__ __forceinline__ void fft2_passes(double2 (&v)[E], double2 (&w)[E], int t, double2* __restrict__ xb,
+                                            double2* __restrict__ xb2, const double2* __restrict__ tw, Sync sync,
+                                            XS xs) {
+  if constexpr (NS < N) {
+    constexpr int R = (NS * E <= N) ? E : N / NS;
+    pass_compute<N, E, R, NS, SIGN>(v, t, tw);
+    pass_compute<N, E, R, NS, SIGN>(w, t, tw);
+    if constexpr (NS * R < N) {
+      constexpr int T = N / E, B = E / R;
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const int j = t + T * b;
+        const int base = (j / NS) * NS * R + (j & (NS - 1));
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          xb[xs(xpad<NS, R>(base + r * NS))] = v[b + r * B];
+          xb2[xs(xpad<NS, R>(base + r * NS))] = w[b + r * B];
+        }
+      }
+      sync();
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        v[i] = xb[xs(xpad<NS, R>(t + T * i))];
+        w[i] = xb2[xs(xpad<NS, R>(t + T * i))];
+      }
+      sync();
+      fft2_passes<N, E, NS * R, SIGN>(v, w, t, xb, xb2, tw, sync, xs);
+    }
+  }
+}
+
+template <int N, int E, int SIGN, class Sync, class XS = IdentitySlot>
+__device__ __forceinline__ void fft2(double2 (&v)[E], double2 (&w)[E], int t, double2* __restrict__ xb,
+                                     double2* __restrict__ xb2, const double2* __restrict__ tw, Sync sync,
+                                     XS xs = XS{}) {
+  int tl;
+  asm volatile("mov.b32 %0, %1;" : "=r"(tl) : "r"(t));
+  fft2_passes<N, E, 1, SIGN>(v, w, tl, xb, xb2, tw, sync, xs);
+}
+
 // CTA barrier as volatile asm: it keeps its order relative to the volatile
 // table loads (ldtw), so the next pass's twiddles are not hoisted above it.
 struct CtaSync {

@@ -73,7 +73,9 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
   extern __shared__ __align__(16) double2 smem[];
   const int grp = threadIdx.x / T, t = threadIdx.x - grp * T;
 #ifndef IDC_CCONV_SMEM_STASH
-  double2* xb = smem + grp * C::XB;
+  constexpr bool FFT2 = E <= 8;
+  double2* xb = smem + grp * (FFT2 ? 2 : 1) * C::XB;   // one exchange buffer per vector in flight
+  double2* xb2 = xb + C::XB;
 #else
   double2* xb = smem + grp * (C::XB + 2 * M);
   double2* S = xb + C::XB;
@@ -97,30 +99,48 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
       prefetch_l2(g + (row + (long)gridDim.x * G) * (long)M, M * 16u);
     }
     // Every intermediate in registers (at most three E-vectors live): no
-    // shared-memory stash traffic, only the FFT exchanges.
+    // shared-memory stash traffic, only the FFT exchanges.  With E = 8 the
+    // independent transforms run pairwise in lockstep (fft2: one barrier pair
+    // per pass; 2-7% faster at m <= 512); with E = 16 the second vector's
+    // codelet registers spill, so the transforms run one at a time.
     double2 x[E], y[E], z[E];
-    // r = 0: u = fft^{-1} f ; v = fft^{-1} g ; u*v
+    double2 zt;   // zeta_{2m}^t; zeta_{2m}^k = zeta_{2m}^t zeta_{2E}^i (immediate), k = t + T i
+    if constexpr (FFT2) {
 #pragma unroll
-    for (int i = 0; i < E; ++i) x[i] = ldv(&fr[t + T * i]);
-    fft<M, E, +1>(x, t, xb, twM, sync);
+      for (int i = 0; i < E; ++i) x[i] = ldv(&fr[t + T * i]);
 #pragma unroll
-    for (int i = 0; i < E; ++i) y[i] = ldv(&gr[t + T * i]);
-    fft<M, E, +1>(y, t, xb, twM, sync);
+      for (int i = 0; i < E; ++i) y[i] = ldv(&gr[t + T * i]);
+      fft2<M, E, +1>(x, y, t, xb, xb2, twM, sync);                        // r = 0
 #pragma unroll
-    for (int i = 0; i < E; ++i) x[i] = cmul(x[i], y[i]);
-    // r = 1: zeta_{2m}^k-shifted streams
-    // zeta_{2m}^k, k = t + T i: zeta_{2m}^t (one table value) x zeta_{2E}^i
-    // (immediate); zt is shared by both splits and the recombination
-    const double2 zt = ldtw(&tw2M[t]);
-    for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { y[i] = cmul(ldv(&fr[t + T * i]), w); });
-    fft<M, E, +1>(y, t, xb, twM, sync);
-    for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { z[i] = cmul(ldv(&gr[t + T * i]), w); });
-    fft<M, E, +1>(z, t, xb, twM, sync);
+      for (int i = 0; i < E; ++i) x[i] = cmul(x[i], y[i]);
+      // r = 1: zeta_{2m}^k-shifted streams
+      zt = ldtw(&tw2M[t]);
+      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { y[i] = cmul(ldv(&fr[t + T * i]), w); });
+      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { z[i] = cmul(ldv(&gr[t + T * i]), w); });
+      fft2<M, E, +1>(y, z, t, xb, xb2, twM, sync);
 #pragma unroll
-    for (int i = 0; i < E; ++i) y[i] = cmul(y[i], z[i]);
-    // forward transforms, recombination and 1/(2m)
-    fft<M, E, -1>(y, t, xb, twM, sync);
-    fft<M, E, -1>(x, t, xb, twM, sync);
+      for (int i = 0; i < E; ++i) y[i] = cmul(y[i], z[i]);
+      fft2<M, E, -1>(x, y, t, xb, xb2, twM, sync);                        // forward
+    } else {
+#pragma unroll
+      for (int i = 0; i < E; ++i) x[i] = ldv(&fr[t + T * i]);
+      fft<M, E, +1>(x, t, xb, twM, sync);                                 // r = 0
+#pragma unroll
+      for (int i = 0; i < E; ++i) y[i] = ldv(&gr[t + T * i]);
+      fft<M, E, +1>(y, t, xb, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) x[i] = cmul(x[i], y[i]);
+      zt = ldtw(&tw2M[t]);
+      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { y[i] = cmul(ldv(&fr[t + T * i]), w); });
+      fft<M, E, +1>(y, t, xb, twM, sync);                                 // r = 1
+      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { z[i] = cmul(ldv(&gr[t + T * i]), w); });
+      fft<M, E, +1>(z, t, xb, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) y[i] = cmul(y[i], z[i]);
+      fft<M, E, -1>(y, t, xb, twM, sync);                                 // forward
+      fft<M, E, -1>(x, t, xb, twM, sync);
+    }
+    // recombination and 1/(2m)
     if (ok) {
       double2* fw = f + row * (long)M;
       for_roots<2 * E, 1, -1, E>(cconj(zt), [&](int i, double2 w) {       // zeta_{2m}^{-k}
@@ -382,7 +402,7 @@ cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s) {
   if (!twM || !tw2M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw2M};
 #ifndef IDC_CCONV_SMEM_STASH
-  const size_t per = C::XB;               // exchange buffer only (intermediates in registers)
+  const size_t per = (E <= 8 ? 2 : 1) * C::XB;   // exchange buffer(s) only (intermediates in registers)
 #else
   const size_t per = C::XB + 2 * M;
 #endif
