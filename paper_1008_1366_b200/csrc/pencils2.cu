@@ -258,21 +258,12 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
     const long S = tl.ncols;
     mbar_wait(bar, phase);
     phase ^= 1;
-    double2 up[E], un[E], v[E];
-#pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const int k = t + T * i;
-      up[i] = stage[(N - 1 + k) * W + c];                              // U_k
-      un[i] = k > 0 ? stage[(k - 1) * W + c] : make_double2(0, 0);     // U_{k-m}
-    }
-    __syncthreads();
+    // U_k and U_{k-m} are re-read from the stage for every residue (keeping
+    // them in registers across the three transforms spilled at 128 registers:
+    // 1.4x the shared loads in local-memory loads); the next tile's copy is
+    // issued after the last residue's read.
+    double2 v[E];
     const long nx = tau + gridDim.x;
-    if (threadIdx.x == 0 && nx < tl.ntiles) {
-      int in2; long item2, c2;
-      tile_coords(tl, nx, W, in2, item2, c2);
-      mbar_arrive_expect_tx(bar, BYTES);
-      load_rows<W, BR>(in2 == 0 ? &mf : &mg, stage, c2, 0, 2 * N - 1, item2, bar);
-    }
 #pragma unroll 1
     for (int rr = 0; rr < 3; ++rr) {
       const int r = rr - 1;
@@ -280,12 +271,23 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const int k = t + T * i;
+        const double2 up = stage[(N - 1 + k) * W + c];                    // U_k
         if (k == 0) {
-          v[i] = up[i];
+          v[i] = up;
         } else {
+          const double2 un = stage[(k - 1) * W + c];                      // U_{k-m}
           const double2 tz = ldtw(&tw3N[k]);
           const double2 zr = r == 0 ? make_double2(1, 0) : (r > 0 ? tz : cconj(tz));
-          v[i] = cmul(zr, cadd(up[i], cmul(z3, un[i])));
+          v[i] = cmul(zr, cadd(up, cmul(z3, un)));
+        }
+      }
+      if (rr == 2) {
+        __syncthreads();
+        if (threadIdx.x == 0 && nx < tl.ntiles) {
+          int in2; long item2, c2;
+          tile_coords(tl, nx, W, in2, item2, c2);
+          mbar_arrive_expect_tx(bar, BYTES);
+          load_rows<W, BR>(in2 == 0 ? &mf : &mg, stage, c2, 0, 2 * N - 1, item2, bar);
         }
       }
       fft<N, E, +1>(v, t, xb, twN, CtaSync{}, xs);
