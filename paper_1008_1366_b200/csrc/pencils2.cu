@@ -126,8 +126,8 @@ k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
       load_rows<W, BR>(in2 == 0 ? &mf : &mg, stage, c2, 0, N, item2, bar);
     }
     // odd stream u_{2l+1} = sum_k zeta_m^{lk} zeta_{2m}^k U_k  (Eq. cconv1backward)
-#pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = cmul(x0[i], ldtw(&tw2N[t + T * i]));
+    // zeta_{2m}^k, k = t + T i: zeta_{2m}^t x zeta_{2E}^i (immediate)
+    for_roots<2 * E, 1, +1, E>(ldtw(&tw2N[t]), [&](int i, double2 w) { v[i] = cmul(x0[i], w); });
     fft<N, E, +1>(v, t, xb, twN, CtaSync{}, xs);
     const long rs = (long)T * tl.ncols;   // pointer step between a thread's rows
     if (ok) {
@@ -195,8 +195,7 @@ k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
       load_rows<W, BR>(&mu, su, c2, 0, N, item2, &bars[1]);
     }
     fft<N, E, -1>(v, t, xb, twN, CtaSync{}, xs);
-#pragma unroll
-    for (int i = 0; i < E; ++i) s[i] = cmulc(v[i], ldtw(&tw2N[t + T * i]));   // zeta_{2m}^{-k} U_k
+    for_roots<2 * E, 1, -1, E>(cconj(ldtw(&tw2N[t])), [&](int i, double2 w) { s[i] = cmul(v[i], w); });  // zeta_{2m}^{-k} U_k
     mbar_wait(&bars[0], phase);
     phase ^= 1;
 #pragma unroll
@@ -268,18 +267,25 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
     for (int rr = 0; rr < 3; ++rr) {
       const int r = rr - 1;
       const double2 z3 = make_double2(r == 0 ? 1.0 : -0.5, r == 0 ? 0.0 : (r < 0 ? s3 : -s3));  // zeta_3^{-r}
-#pragma unroll
-      for (int i = 0; i < E; ++i) {
+      // zeta_{3m}^{rk}, k = t + T i: zeta_{3m}^{rt} x zeta_{3E}^{ri} (immediate)
+      auto split = [&](int i, double2 zr) {
         const int k = t + T * i;
         const double2 up = stage[(N - 1 + k) * W + c];                    // U_k
-        if (k == 0) {
+        if (i == 0 && t == 0) {
           v[i] = up;
         } else {
           const double2 un = stage[(k - 1) * W + c];                      // U_{k-m}
-          const double2 tz = ldtw(&tw3N[k]);
-          const double2 zr = r == 0 ? make_double2(1, 0) : (r > 0 ? tz : cconj(tz));
           v[i] = cmul(zr, cadd(up, cmul(z3, un)));
         }
+      };
+      const double2 zt = ldtw(&tw3N[t]);
+      if (r == 0) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) split(i, make_double2(1, 0));
+      } else if (r > 0) {
+        for_roots<3 * E, 1, +1, E>(zt, split);
+      } else {
+        for_roots<3 * E, 1, -1, E>(cconj(zt), split);
       }
       if (rr == 2) {
         __syncthreads();
@@ -383,11 +389,7 @@ k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
       fft<N, E, -1>(v, t, xb, twN, CtaSync{}, xs);
       // 3m U_k = sum_r zeta_{3m}^{-rk} S_r(k); 3m U_{k-m} = sum_r zeta_{3m}^{-rk} zeta_3^{r} S_r(k)
       const double2 z3 = make_double2(r == 0 ? 1.0 : -0.5, r == 0 ? 0.0 : (r > 0 ? s3 : -s3));  // zeta_3^{r}
-#pragma unroll
-      for (int i = 0; i < E; ++i) {
-        const int k = t + T * i;
-        const double2 tz = ldtw(&tw3N[k]);
-        const double2 zr = r == 0 ? make_double2(1, 0) : (r > 0 ? cconj(tz) : tz);  // zeta_{3m}^{-rk}
+      auto acc = [&](int i, double2 zr) {                                 // zr = zeta_{3m}^{-rk}
         const double2 p = cmul(zr, v[i]);
         if (q == 0) {
           ap[i] = p;
@@ -396,6 +398,15 @@ k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
           ap[i] = cadd(ap[i], p);
           an[i] = cadd(an[i], cmul(z3, p));
         }
+      };
+      const double2 zt = ldtw(&tw3N[t]);
+      if (r == 0) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) acc(i, make_double2(1, 0));
+      } else if (r > 0) {
+        for_roots<3 * E, 1, -1, E>(cconj(zt), acc);
+      } else {
+        for_roots<3 * E, 1, +1, E>(zt, acc);
       }
     }
     if (ok) {
