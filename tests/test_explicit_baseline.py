@@ -1,0 +1,43 @@
+"""The explicitly padded comparison baseline (tools/cufft_explicit.py, SURVEY
+8(f) NEXT-4) computes the same dealiased convolutions: checked against the
+oracle's direct sums on small inputs (torch.fft on the CPU here; the same
+functions run on cuFFT in the comparison run)."""
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import synthgen
+from oracle import direct, rel_l2
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+import cufft_explicit as ex  # noqa: E402
+
+
+def T(a):
+    return torch.from_numpy(np.ascontiguousarray(a))
+
+
+def test_explicit_1d():
+    f, g, h = synthgen.hconv1d_inputs(32, 3, roles=(0, 1, 2))
+    assert rel_l2(ex.cconv1d(T(f), T(g)).numpy(), direct.cconv1d(f, g)) < 1e-14
+    assert rel_l2(ex.hconv1d(T(f), T(g)).numpy(), direct.hconv1d(f, g)) < 1e-14
+    assert rel_l2(ex.tconv1d(T(f), T(g), T(h)).numpy(), direct.tconv1d(f, g, h)) < 1e-14
+
+
+@pytest.mark.parametrize("shape", [(8, 16), (16, 4)])
+def test_explicit_2d(shape):
+    f, g = synthgen.cconv2d_inputs(*shape, 2)
+    ref = np.stack([direct.cconv2d(f[b], g[b]) for b in range(2)])
+    assert rel_l2(ex.cconv2d(T(f), T(g)).numpy(), ref) < 1e-14
+    f, g = synthgen.hconv2d_inputs(*shape)
+    assert rel_l2(ex.hconv2d(T(f), T(g)).numpy(), direct.hconv2d(f, g)) < 1e-14
+
+
+def test_explicit_3d():
+    f, g = synthgen.cconv3d_inputs(4, 8, 4)
+    assert rel_l2(ex.cconv3d(T(f), T(g)).numpy(), direct.cconv3d(f, g)) < 1e-14
+    f, g = synthgen.hconv3d_inputs(4, 4, 4)
+    assert rel_l2(ex.hconv3d(T(f), T(g)).numpy(), direct.hconv3d(f, g)) < 1e-14
