@@ -248,6 +248,8 @@ __host__ __device__ constexpr int xbuf_elems() { return N <= E ? 0 : N + N / E; 
 // w^c and row Q - 2 + a (a = 1..R/Q-1) holds w^{Qa}, w = zeta_N^{j N/(NS R)},
 // at column j.  Lanes read consecutive j: contiguous 16-byte loads (a gather
 // from the full zeta_N table touched up to 32 cache lines per warp load).
+// (storing every w^r instead -- one multiply per element, R - 1 loads per
+// butterfly -- measured 6-12% slower: more L1 wavefronts)
 __host__ __device__ constexpr int pass_q(int R) { return R >= 16 ? 4 : (R >= 4 ? 2 : 1); }
 __host__ __device__ constexpr int pass_radix(int N, int E, int NS) { return (NS * E <= N) ? E : N / NS; }
 template <int N, int E>
