@@ -80,6 +80,8 @@ WORKLOADS = {
         dict(kind="cconv2d", m=(256, 256), batch=64, narr=2)]),
     "c4": dict(desc="configs[3]: hconv2d mx=my=2048 ((2mx-1) x my)", parts=[
         dict(kind="hconv2d", m=(2048, 2048), batch=1, narr=2)]),
+    "c4adv": dict(desc="NEXT-1: 2D Euler advective term (M=2 dot-product conv2, P:867-876), mx=my=2048", parts=[
+        dict(kind="advection2d", m=(2048, 2048), batch=1, narr=2)]),
     "c5a": dict(desc="configs[4]: cconv3d 512^3", parts=[
         dict(kind="cconv3d", m=(512, 512, 512), batch=1, narr=2)]),
     "c5b": dict(desc="configs[4]: hconv3d 512^3 modes ((2m-1)^2 x m)", parts=[
@@ -93,7 +95,7 @@ def shape_of(p):
         return (p["batch"], m)
     if k == "cconv2d":
         return (p["batch"],) + tuple(m)
-    if k == "hconv2d":
+    if k in ("hconv2d", "advection2d"):
         return (2 * m[0] - 1, m[1])
     if k == "cconv3d":
         return tuple(m)
@@ -122,6 +124,12 @@ def part_model(p):
         mx, my = m
         fl = 9 * my * flops_cfft(mx) + 3 * mx * 9 * flops_rfft(my)
         return W * (3 * (2 * mx - 1) * my + 18 * mx * my), fl
+    if kind == "advection2d":
+        # input build (read w, write 4 arrays), M = 2 dot-product conv2 (x pass over
+        # 4 arrays, rows over 2 pairs, x-forward of one), copy out
+        mx, my = m
+        fl = 15 * my * flops_cfft(mx) + 3 * mx * 15 * flops_rfft(my)
+        return W * (12 * (2 * mx - 1) * my + 30 * mx * my), fl
     if kind == "cconv3d":
         mx, my, mz = m
         fl = 6 * my * mz * flops_cfft(mx) + 2 * mx * (6 * mz * flops_cfft(my) + 2 * my * 6 * flops_cfft(mz))
@@ -206,17 +214,17 @@ def make_inputs(idc, torch, p, rank, dev):
             idc.fill_uniform(a, synthgen.array_id(role, rank), synthgen.SEED)
         if kind in ("hconv1d", "tconv1d"):
             a[:, 0] = a[:, 0].real.to(torch.complex128)   # Im U_0 := 0 (config 2)
-        elif kind in ("hconv2d", "cconv3d", "hconv3d"):
+        elif kind in ("hconv2d", "advection2d", "cconv3d", "hconv3d"):
             axes = []
             for d, n in enumerate(shp):
                 k = torch.arange(n, device=dev, dtype=torch.float64)
-                centered = (kind == "hconv2d" and d == 0) or (kind == "hconv3d" and d < 2)
+                centered = (kind in ("hconv2d", "advection2d") and d == 0) or (kind == "hconv3d" and d < 2)
                 if centered:
                     k = k - (n - 1) // 2
                 axes.append(k)
             k2 = sum((ax ** 2).reshape([-1 if i == j else 1 for i in range(len(shp))]) for j, ax in enumerate(axes))
             a /= (1.0 + k2)
-            if kind == "hconv2d":                      # ky = 0 line conjugate-symmetric, U_00 real
+            if kind in ("hconv2d", "advection2d"):     # ky = 0 line conjugate-symmetric, U_00 real
                 c = (shp[0] - 1) // 2
                 a[:c, 0] = torch.conj(torch.flip(a[c + 1:, 0], dims=(0,)))
                 a[c, 0] = a[c, 0].real.to(torch.complex128)
@@ -231,6 +239,12 @@ def make_inputs(idc, torch, p, rank, dev):
 
 
 def call(idc, p, arrs):
+    if p["kind"] == "advection2d":                      # (w, out); device-only call
+        if arrs[0].is_cuda:
+            return idc.advection2d(arrs[0], out=arrs[1])
+        out = idc.advection2d(arrs[0].to("cuda", non_blocking=True))
+        arrs[0].copy_(out, non_blocking=True)            # result back to the host buffer
+        return arrs[0]
     return getattr(idc, p["kind"])(*arrs)
 
 
@@ -367,7 +381,8 @@ def run_e2e(args, idc, torch, parts, pristine, dev, ws):
     host_f0 = [arrs[0].clone() for arrs in host]
     stream = torch.cuda.current_stream(dev)
     steps = max(1, min(args.steps, args.e2e_steps))
-    bi = sum(a.numel() * 16 for arrs in host for a in arrs)
+    bi = sum(a.numel() * 16 for p, arrs in zip(parts, host)
+             for a in (arrs[:1] if p["kind"] == "advection2d" else arrs))
     bo = sum(arrs[0].numel() * 16 for arrs in host)
     # warm-up once
     for p, arrs in zip(parts, host):

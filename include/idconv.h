@@ -200,6 +200,43 @@ IDC_API size_t idc_dist_emulated_workspace_bytes_kind(idc_kind k, size_t mx, siz
 IDC_API idc_status idc_hconv3d_dist_emulated(int nranks, idc_c128** f_slabs, idc_c128** g_slabs, size_t mx,
                                              size_t my, size_t mz, void* work, size_t work_bytes, idc_stream stream);
 
+/* ---- multivector dot-product convolutions ---------- */
+
+/* "we allow the convolution inputs to be arrays of vectors, f_i
+ * and g_i (i = 1..M), interpreting ... the product f * g as the
+ * element-by-element dot product sum_i f_i * g_i".  The M = npairs backward
+ * transforms of each residue are followed by ONE set of forward transforms.
+ *
+ * idc_hconv1d_dot: f, g hold npairs stacked (batch x m) arrays (pair i at
+ * f + i*batch*m, centered Hermitian rows as idc_hconv1d, 2 <= m <= 4096);
+ * f[0..batch*m) <- sum_i conv(f_i, g_i) (D2 summed over i).  The other pairs
+ * of f and all of g are unspecified on return.  No workspace. */
+IDC_API idc_status idc_hconv1d_dot(idc_c128* f, idc_c128* g, size_t npairs, size_t m, size_t batch,
+                                   idc_stream stream);
+/* idc_hconv2d_dot: npairs stacked (2mx-1) x my centered Hermitian arrays
+ * (layout of idc_hconv2d, my <= 4096); pair 0 <- sum_i hconv2d(f_i, g_i).
+ * Workspace idc_dot_workspace_bytes(IDC_HCONV2D, npairs, mx, my)
+ * = 2 npairs (mx+1) my words (the x-stream work arrays of Function conv2,
+ * P:829-834, per pair). */
+IDC_API size_t idc_dot_workspace_bytes(idc_kind k, size_t npairs, size_t m0, size_t m1);
+IDC_API idc_status idc_hconv2d_dot(idc_c128* f, idc_c128* g, size_t npairs, size_t mx, size_t my, void* work,
+                                   size_t work_bytes, idc_stream stream);
+/* Hermitian projection of the stored ky = 0 line of batch (2mx-1) x my
+ * arrays, in place (AMB-7): U_{kx,0} <- (U_{kx,0} +
+ * conj U_{-kx,0})/2, so U_{0,0} becomes real.  Idempotent. */
+IDC_API idc_status idc_enforce_symmetry_2d(idc_c128* a, size_t mx, size_t my, size_t batch, idc_stream stream);
+/* 2D pseudospectral Euler application: out <- the call
+ * conv2(i kx w, i ky w, i ky w/k^2, -i kx w/k^2) of the paper with M = 2,
+ * i.e. sum_p (p_y k_x - p_x k_y)/|k-p|^2 w_p w_{k-p} = u.grad(w) for
+ * u = zhat x grad(inverse Laplacian of w) (1/k^2 := 0 at k = 0; AMB-22: the
+ * paper calls this "the advective term -u.grad(w)" and prints the sum with
+ * the opposite sign; the call as written computes +u.grad(w)).  w, out:
+ * (2mx-1) x my centered Hermitian (w is not modified; may alias out).
+ * Workspace idc_advection2d_workspace_bytes(mx, my). */
+IDC_API size_t idc_advection2d_workspace_bytes(size_t mx, size_t my);
+IDC_API idc_status idc_advection2d(const idc_c128* w, idc_c128* out, size_t mx, size_t my, void* work,
+                                   size_t work_bytes, idc_stream stream);
+
 /* ---- synthetic inputs (not part of the method) -------------------------- */
 
 /* Fill n complex values with the counter-based splitmix64 generator of

@@ -27,6 +27,9 @@ Layers:
   (P:891-897, AMB-9).
 * O4 ``closed.*`` -- the paper's exact test families
   and their derived 2D/3D/ternary analogues.
+* O5 ``application.*`` -- the 2D pseudospectral Euler sum of P:867-876
+  written out (pinned by a two-mode closed form and by its decomposition into
+  D5 direct sums).
 
 Parity status: every function here is pinned by tests/test_oracle_*.py
 against closed forms, library routines (numpy.convolve), brute force or the
@@ -602,6 +605,47 @@ class implicit:
             res = np.stack([implicit.hconv2d(a[l], b[l]) for l in range(mx)], axis=0)
             out[r] = np.moveaxis(res, 0, -1)
         return np.moveaxis(implicit.fft0pad_forward(out, mx), -1, 0)
+
+
+# ================================================ O5 pseudospectral application ==
+
+class application:
+    """The 2D pseudospectral use case of P:859-876 written out as sums."""
+
+    @staticmethod
+    def hermitian_full2d(A):
+        """(2mx-1, my) centered Hermitian storage -> (2mx-1, 2my-1) full array,
+        ky = 0 line projected (AMB-7), U_{kx,-ky} = conj(U_{-kx,ky})."""
+        A = _c(A).copy()
+        nx, my = A.shape
+        A[:, 0] = 0.5 * (A[:, 0] + np.conj(A[::-1, 0]))
+        full = np.zeros((nx, 2 * my - 1), dtype=np.complex128)
+        full[:, my - 1:] = A
+        full[:, :my - 1] = np.conj(A[::-1, :0:-1])
+        return full
+
+    @staticmethod
+    def euler_sum(w):
+        """S_k = sum_p (p_x k_y - p_y k_x) / |k-p|^2 w_p w_{k-p}, p and
+        k-p over the full centered range, 1/|q|^2 := 0 at q = 0 (no mean flow,
+        S:398); output kx in [-mx+1, mx-1], ky in [0, my-1] (AMB-6).  Plain loops
+        over k, numpy over p: small sizes only."""
+        W = application.hermitian_full2d(w)
+        nx, ny = W.shape
+        mx, my = (nx + 1) // 2, (ny + 1) // 2
+        px = np.arange(-(mx - 1), mx)[:, None]
+        py = np.arange(-(my - 1), my)[None, :]
+        out = np.zeros((nx, my), dtype=np.complex128)
+        for kx in range(-(mx - 1), mx):
+            for ky in range(0, my):
+                qx, qy = kx - px, ky - py                       # k - p
+                ok = (np.abs(qx) <= mx - 1) & (np.abs(qy) <= my - 1)
+                q2 = (qx * qx + qy * qy).astype(np.float64)
+                inv = np.where((q2 > 0) & ok, 1.0 / np.where(q2 > 0, q2, 1.0), 0.0)
+                Wq = np.where(ok, W[np.clip(qx + mx - 1, 0, nx - 1), np.clip(qy + my - 1, 0, ny - 1)], 0.0)
+                term = (px * ky - py * kx) * inv * W * Wq
+                out[kx + mx - 1, ky] = term.sum()
+        return out
 
 
 # ======================================================== O4 closed forms ==

@@ -167,4 +167,69 @@ idc_status idc_hconv3d(idc_c128* f, idc_c128* g, size_t mx, size_t my, size_t mz
                                     (int)mz, reinterpret_cast<double2*>(work), (cudaStream_t)stream));
 }
 
+// ---- multivector dot-product convolutions (NEXT-1) ----------
+
+size_t idc_dot_workspace_bytes(idc_kind k, size_t npairs, size_t m0, size_t m1) {
+  if (npairs == 0) return 0;
+  if (k == IDC_HCONV1D) return 0;
+  if (k == IDC_HCONV2D) return idc::hconv2d_dot_work_bytes(npairs, m0, m1);
+  return 0;
+}
+
+idc_status idc_hconv1d_dot(idc_c128* f, idc_c128* g, size_t npairs, size_t m, size_t batch, idc_stream stream) {
+  if (m == 0 || batch == 0 || npairs == 0) return IDC_ERR_INVALID;
+  if (!size_ok(m, 2, 4096)) return IDC_ERR_UNSUPPORTED;
+  const void* arrs[] = {f, g};
+  idc_status st = check_arrays(arrs, 2, npairs * m * batch * sizeof(idc_c128), nullptr, 0, 0);
+  if (st != IDC_OK) return st;
+  return from_cuda(idc::launch_hconv_dot_rows(reinterpret_cast<double2*>(f), reinterpret_cast<double2*>(g),
+                                              (int)npairs, (long)(m * batch), (int)m, (long)batch,
+                                              (cudaStream_t)stream));
+}
+
+idc_status idc_hconv2d_dot(idc_c128* f, idc_c128* g, size_t npairs, size_t mx, size_t my, void* work,
+                           size_t work_bytes, idc_stream stream) {
+  if (mx == 0 || my == 0 || npairs == 0) return IDC_ERR_INVALID;
+  if (!size_ok(mx, 1, 8192) || !size_ok(my, 2, 4096)) return IDC_ERR_UNSUPPORTED;
+  size_t need = idc::hconv2d_dot_work_bytes(npairs, mx, my);
+  if (need == 0) return IDC_ERR_UNSUPPORTED;
+  const void* arrs[] = {f, g};
+  idc_status st = check_arrays(arrs, 2, npairs * (2 * mx - 1) * my * sizeof(idc_c128), work, work_bytes, need);
+  if (st != IDC_OK) return st;
+  return from_cuda(idc::run_hconv2d_dot(reinterpret_cast<double2*>(f), reinterpret_cast<double2*>(g), (int)npairs,
+                                        (int)mx, (int)my, reinterpret_cast<double2*>(work), (cudaStream_t)stream));
+}
+
+idc_status idc_enforce_symmetry_2d(idc_c128* a, size_t mx, size_t my, size_t batch, idc_stream stream) {
+  if (!a || !aligned16(a) || mx == 0 || my == 0 || batch == 0) return IDC_ERR_INVALID;
+  return from_cuda(idc::launch_enforce_symmetry_2d(reinterpret_cast<double2*>(a), (int)mx, (int)my, (long)batch,
+                                                   (cudaStream_t)stream));
+}
+
+size_t idc_advection2d_workspace_bytes(size_t mx, size_t my) {
+  const size_t conv = idc::hconv2d_dot_work_bytes(2, mx, my);
+  if (conv == 0) return 0;
+  return conv + 3 * 2 * (2 * mx - 1) * my * sizeof(idc_c128);   // f (2 arrays), g (2 arrays), alignment slack
+}
+
+idc_status idc_advection2d(const idc_c128* w, idc_c128* out, size_t mx, size_t my, void* work, size_t work_bytes,
+                           idc_stream stream) {
+  if (!w || !out || mx == 0 || my == 0) return IDC_ERR_INVALID;
+  if (!aligned16(w) || !aligned16(out) || (work && !aligned16(work))) return IDC_ERR_INVALID;
+  if (!size_ok(mx, 1, 8192) || !size_ok(my, 2, 4096)) return IDC_ERR_UNSUPPORTED;
+  const size_t need = idc_advection2d_workspace_bytes(mx, my);
+  if (!work) return IDC_ERR_WORKSPACE;
+  if (work_bytes < need) return IDC_ERR_WORKSPACE;
+  const size_t n = (2 * mx - 1) * my;
+  double2* F = reinterpret_cast<double2*>(work);
+  double2* G = F + 2 * n;
+  double2* cw = G + 2 * n;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = idc::launch_advection2d_inputs(reinterpret_cast<const double2*>(w), F, G, (int)mx, (int)my, s);
+  if (e != cudaSuccess) return IDC_ERR_CUDA;
+  e = idc::run_hconv2d_dot(F, G, 2, (int)mx, (int)my, cw, s);
+  if (e != cudaSuccess) return IDC_ERR_CUDA;
+  return from_cuda(cudaMemcpyAsync(out, F, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+}
+
 }  // extern "C"

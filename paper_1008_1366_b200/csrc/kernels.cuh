@@ -31,6 +31,15 @@ template <int M> cudaError_t tconv_rows2(double2* f, double2* g, double2* h, lon
 template <int M> cudaError_t hconv_rows3(double2* f, double2* g, long nrows, cudaStream_t s);
 template <int M> cudaError_t tconv_rows3(double2* f, double2* g, double2* h, long nrows, cudaStream_t s);
 
+// K3d (rows_dot.cu): centered Hermitian dot-product convolution of npairs
+// row pairs (pair i at f + i*istride, g + i*istride), result in pair 0.
+cudaError_t launch_hconv_dot_rows(double2* f, const double2* g, int npairs, long istride, int m, long nrows,
+                                  cudaStream_t s);
+// Hermitian projection of the ky = 0 lines of batch (2mx-1) x my arrays.
+cudaError_t launch_enforce_symmetry_2d(double2* a, int mx, int my, long batch, cudaStream_t s);
+// The four M = 2 inputs of the 2D Euler advective term from w.
+cudaError_t launch_advection2d_inputs(const double2* w, double2* f, double2* g, int mx, int my, cudaStream_t s);
+
 // Count of hot-path kernel launches issued by this library (every launcher
 // calls count_launch() right before cudaLaunchKernel); read through the ABI
 // as idc_launch_count() so a benchmark can report its own kernel launches.

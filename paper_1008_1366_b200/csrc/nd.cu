@@ -134,6 +134,25 @@ cudaError_t run_hconv2d(double2* f, double2* g, int mx, int my, double2* work, c
   return launch_pad0_fwd(f, U, mx, my, 1, 0, 0, s);                       // fft0padForward on columns
 }
 
+// Multivector dot product: sum_i f_i * g_i of npairs Hermitian
+// 2D pairs (pair i at f + i (2mx-1) my), result in pair 0.  Function conv2
+// with the product stage summed over the pairs: K7 along x on all 2*npairs
+// arrays, K3d on the rows of the three x-streams, K8 on pair 0 only.
+size_t hconv2d_dot_work_bytes(size_t npairs, size_t mx, size_t my) {
+  if (!pow2ok(mx) || !pow2ok(my) || my > 4096 || npairs == 0) return 0;
+  return 2 * npairs * (mx + 1) * my * W16;
+}
+
+cudaError_t run_hconv2d_dot(double2* f, double2* g, int npairs, int mx, int my, double2* work, cudaStream_t s) {
+  const long fs = (2L * mx - 1) * my, us = ((long)mx + 1) * my;
+  double2* U = work;
+  double2* V = work + (long)npairs * us;
+  IDC_TRY(launch_pad0_bwd(f, g, U, V, mx, my, npairs, fs, us, s));       // fft0padBackward on every column
+  IDC_TRY(launch_hconv_dot_rows(f, g, npairs, fs, my, 2L * mx - 1, s));   // dot-product conv, f-stream rows
+  IDC_TRY(launch_hconv_dot_rows(U, V, npairs, us, my, (long)mx + 1, s));  // dot-product conv, U-stream rows
+  return launch_pad0_fwd(f, U, mx, my, 1, 0, 0, s);                      // fft0padForward, pair 0
+}
+
 // ------------------------------------------------------------------- 3D --
 cudaError_t run_cconv3d(double2* f, double2* g, int mx, int my, int mz, double2* work, cudaStream_t s) {
   const long slab = (long)my * mz, n = (long)mx * slab;

@@ -1,0 +1,245 @@
+// rows_dot.cu -- multivector dot-product centered Hermitian convolutions
+// and the small elementwise helpers of the 2D
+// pseudospectral application.
+//
+// "we allow the convolution inputs to be arrays of vectors, f_i
+// and g_i (i = 1..M), interpreting in Functions cconv, conv and tconv the
+// product f * g as the element-by-element dot product sum_i f_i * g_i".
+// K3d below is K3 (centered Hermitian, three residues) with the
+// product stage summed over the M pairs before the forward transforms: per
+// residue r the M packed streams w^{f_i}_r + i w^{g_i}_r are backward
+// transformed (two c2r each) and their real products summed,
+// p_r = sum_i (Re * Im); the forward transforms and the recombination
+// 3m h_k = P_0 + zeta_{3m}^{k} P_{-1} + zeta_{3m}^{-k} P_1 (Eq. fft0forwardB)
+// run once.  For M = 2 that is the paper's "five Fourier transforms" per
+// input-pair set at the 1D level: 4 c2r + 1 r2c per residue.
+//
+// Layout: pair i's rows start at f + i * istride (g likewise); row j of pair
+// i is f + i * istride + j * m.  The result goes to pair 0's rows (f).
+#include "fft_dev.cuh"
+#include "kernels.cuh"
+#include "tables.cuh"
+#include "tma.cuh"
+
+namespace idc {
+
+namespace {
+
+template <int M>
+struct DCfg {
+  static constexpr int E = M < 8 ? M : (M <= 512 ? 8 : 16);
+  static constexpr int T = M / E;
+  static constexpr int G = T >= 256 ? 1 : 256 / T;          // rows per CTA
+  static constexpr int THREADS = G * T;
+  static constexpr int XB = xbuf_elems<M, E>() > M ? xbuf_elems<M, E>() : M;
+  static constexpr bool NAMED = (T % 32 == 0) && G > 1;
+};
+
+template <bool NAMED>
+struct DSync;
+template <>
+struct DSync<true> {
+  int id, n;
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+};
+template <>
+struct DSync<false> {
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync 0;" ::: "memory"); }
+};
+
+template <int M>
+__device__ __forceinline__ DSync<DCfg<M>::NAMED> dsync(int grp) {
+  if constexpr (DCfg<M>::NAMED) return DSync<true>{1 + grp, DCfg<M>::T};
+  else return DSync<false>{};
+}
+
+}  // namespace
+
+// ===================================================================== K3d ==
+template <int M>
+__global__ void __launch_bounds__(DCfg<M>::THREADS, 1)
+k_hconv_dot_rows(double2* __restrict__ f, const double2* __restrict__ g, int npairs, long istride, long nrows,
+                 const double2* __restrict__ twM, const double2* __restrict__ tw3M) {
+  using C = DCfg<M>;
+  constexpr int E = C::E, T = C::T, G = C::G;
+  extern __shared__ __align__(16) double2 smem[];
+  const int grp = threadIdx.x / T, t = threadIdx.x - grp * T;
+  double2* xb = smem + grp * C::XB;
+  const auto sync = dsync<M>(grp);
+  const double inv = 1.0 / (3.0 * M);
+  const double s3 = 0.86602540378443864676372317075294;  // sqrt(3)/2
+  for (long row0 = (long)blockIdx.x * G; row0 < nrows; row0 += (long)gridDim.x * G) {
+    const long row = row0 + grp;
+    if constexpr (C::NAMED) {
+      if (row >= nrows) break;
+    }
+    const bool ok = row < nrows;
+    const long roff = (ok ? row : 0) * (long)M;
+    double2 v[E], Q[E];
+    double p[E];
+#pragma unroll 1
+    for (int rr = 0; rr < 3; ++rr) {
+      const int r = rr == 0 ? 0 : (rr == 1 ? 1 : -1);
+      const double2 c = make_double2(r == 0 ? 1.0 : -0.5, r == 0 ? 0.0 : (r < 0 ? s3 : -s3));  // zeta_3^{-r}
+#pragma unroll
+      for (int i = 0; i < E; ++i) p[i] = 0.0;
+#pragma unroll 1
+      for (int q = 0; q < npairs; ++q) {                       // p_r = sum_i Re * Im (the dot product)
+        const double2* fr = f + q * istride + roff;
+        const double2* gr = g + q * istride + roff;
+        const double2 zt = ldtw(&tw3M[t]);
+        auto split = [&](int i, double2 zr) {
+          const int k = t + T * i;
+          if (i == 0 && t == 0) {
+            v[i] = make_double2(ldv(&fr[0]).x, ldv(&gr[0]).x);   // w_{0,r} = Re U_0 (AMB-7)
+          } else {
+            const double2 fk = ldv(&fr[k]), gk = ldv(&gr[k]), fm = ldv(&fr[M - k]), gm = ldv(&gr[M - k]);
+            const double2 P = make_double2(fk.x - gk.y, fk.y + gk.x);
+            const double2 R = make_double2(fm.x + gm.y, gm.x - fm.y);
+            v[i] = cmul(zr, cadd(P, cmul(c, R)));
+          }
+        };
+        if (r == 0) {
+#pragma unroll
+          for (int i = 0; i < E; ++i) split(i, make_double2(1.0, 0.0));
+        } else if (r > 0) {
+          for_roots<3 * E, 1, +1, E>(zt, split);
+        } else {
+          for_roots<3 * E, 1, -1, E>(cconj(zt), split);
+        }
+        fft<M, E, +1>(v, t, xb, twM, sync);                    // two c2r in one complex FFT
+#pragma unroll
+        for (int i = 0; i < E; ++i) p[i] = fma(v[i].x, v[i].y, p[i]);
+      }
+      if (r == 0) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) Q[i].x = p[i];
+      } else if (r == 1) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) Q[i].y = p[i];
+        fft<M, E, -1>(Q, t, xb, twM, sync);                    // Q = fft(p_0 + i p_1)
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i) v[i] = make_double2(p[i], 0.0);
+        fft<M, E, -1>(v, t, xb, twM, sync);                    // P_{-1}
+      }
+    }
+    // P_0, P_1 from Q through Q_{m-k}; recombination (Eq. fft0forwardB)
+#pragma unroll
+    for (int i = 0; i < E; ++i) xb[t + T * i] = Q[i];
+    sync();
+    if (ok) {
+      double2* fw = f + roff;
+      for_roots<3 * E, 1, +1, E>(ldtw(&tw3M[t]), [&](int i, double2 tz) {
+        const int k = t + T * i;
+        const double2 a = Q[i], b = cconj(xb[(M - k) & (M - 1)]);
+        const double2 pp0 = cscale(cadd(a, b), 0.5);
+        const double2 d = csub(a, b);
+        const double2 pp1 = make_double2(0.5 * d.y, -0.5 * d.x);
+        fw[k] = cscale(cadd(cadd(pp0, cmul(v[i], tz)), cmulc(pp1, tz)), inv);
+      });
+    }
+    sync();
+  }
+}
+
+// ------------------------------------------------------- 2D helpers ------
+// Hermitian projection of the stored ky = 0 line of a (2mx-1) x my centered
+// array (AMB-7; "automatically enforce Hermitian symmetry"):
+// U_{kx,0} <- (U_{kx,0} + conj U_{-kx,0}) / 2, U_{0,0} real.
+__global__ void k_enforce_symmetry_2d(double2* __restrict__ a, int mx, int my, long batch) {
+  const long n = (long)mx * batch;                   // kx = 0..mx-1 for every item
+  for (long id = (long)blockIdx.x * blockDim.x + threadIdx.x; id < n; id += (long)gridDim.x * blockDim.x) {
+    const long b = id / mx;
+    const int kx = (int)(id - b * mx);
+    double2* A = a + b * (long)(2 * mx - 1) * my;
+    double2* P = A + (long)(mx - 1 + kx) * my;       // (kx, 0)
+    double2* N = A + (long)(mx - 1 - kx) * my;       // (-kx, 0)
+    const double2 u = *P, w = *N;
+    const double2 s = make_double2(0.5 * (u.x + w.x), 0.5 * (u.y - w.y));
+    *P = s;
+    *N = cconj(s);
+  }
+}
+
+// Inputs of the 2D Euler advective term: from the vorticity
+// spectrum w (centered kx, Hermitian ky >= 0), the M = 2 dot-product pairs
+//   f_1 = i kx w,  f_2 = i ky w,  g_1 = i ky w / k^2,  g_2 = -i kx w / k^2
+// (1/k^2 := 0 at k = 0: no mean flow).  f, g: 2 x (2mx-1) x my each.
+__global__ void k_advection2d_inputs(const double2* __restrict__ w, double2* __restrict__ f, double2* __restrict__ g,
+                                     int mx, int my) {
+  const long n = (long)(2 * mx - 1) * my;
+  for (long id = (long)blockIdx.x * blockDim.x + threadIdx.x; id < n; id += (long)gridDim.x * blockDim.x) {
+    const long i = id / my;
+    const double kx = (double)(i - (mx - 1)), ky = (double)(id - i * my);
+    const double2 a = w[id];
+    const double k2 = kx * kx + ky * ky;
+    const double ik2 = k2 > 0.0 ? 1.0 / k2 : 0.0;
+    f[id] = make_double2(-kx * a.y, kx * a.x);                    // i kx w
+    f[n + id] = make_double2(-ky * a.y, ky * a.x);                // i ky w
+    g[id] = make_double2(-ky * a.y * ik2, ky * a.x * ik2);        // i ky w / k^2
+    g[n + id] = make_double2(kx * a.y * ik2, -kx * a.x * ik2);    // -i kx w / k^2
+  }
+}
+
+// ================================================================ launchers ==
+template <int M>
+cudaError_t hconv_dot_rows(double2* f, const double2* g, int npairs, long istride, long nrows, cudaStream_t s) {
+  using C = DCfg<M>;
+  const double2* twM = pass_table(M, C::E);
+  const double2* tw3M = zeta_table(3 * M);
+  if (!twM || !tw3M) return cudaErrorMemoryAllocation;
+  const size_t smem = (size_t)C::G * C::XB * 16;
+  cudaError_t e = cudaFuncSetAttribute(k_hconv_dot_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  long need = (nrows + C::G - 1) / C::G;
+  long grid = num_sms();
+  if (need < grid) grid = need;
+  if (grid < 1) grid = 1;
+  void* args[] = {&f, &g, &npairs, &istride, &nrows, &twM, &tw3M};
+  count_launch();
+  return cudaLaunchKernel((const void*)k_hconv_dot_rows<M>, dim3((unsigned)grid), dim3(C::THREADS), args, smem, s);
+}
+
+cudaError_t launch_hconv_dot_rows(double2* f, const double2* g, int npairs, long istride, int m, long nrows,
+                                  cudaStream_t s) {
+  switch (m) {
+    case 2: return hconv_dot_rows<2>(f, g, npairs, istride, nrows, s);
+    case 4: return hconv_dot_rows<4>(f, g, npairs, istride, nrows, s);
+    case 8: return hconv_dot_rows<8>(f, g, npairs, istride, nrows, s);
+    case 16: return hconv_dot_rows<16>(f, g, npairs, istride, nrows, s);
+    case 32: return hconv_dot_rows<32>(f, g, npairs, istride, nrows, s);
+    case 64: return hconv_dot_rows<64>(f, g, npairs, istride, nrows, s);
+    case 128: return hconv_dot_rows<128>(f, g, npairs, istride, nrows, s);
+    case 256: return hconv_dot_rows<256>(f, g, npairs, istride, nrows, s);
+    case 512: return hconv_dot_rows<512>(f, g, npairs, istride, nrows, s);
+    case 1024: return hconv_dot_rows<1024>(f, g, npairs, istride, nrows, s);
+    case 2048: return hconv_dot_rows<2048>(f, g, npairs, istride, nrows, s);
+    case 4096: return hconv_dot_rows<4096>(f, g, npairs, istride, nrows, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_enforce_symmetry_2d(double2* a, int mx, int my, long batch, cudaStream_t s) {
+  const long n = (long)mx * batch;
+  const int threads = 256;
+  long blocks = (n + threads - 1) / threads;
+  if (blocks > 4L * num_sms() * 8) blocks = 4L * num_sms() * 8;
+  if (blocks < 1) blocks = 1;
+  count_launch();
+  k_enforce_symmetry_2d<<<(unsigned)blocks, threads, 0, s>>>(a, mx, my, batch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_advection2d_inputs(const double2* w, double2* f, double2* g, int mx, int my, cudaStream_t s) {
+  const long n = (long)(2 * mx - 1) * my;
+  const int threads = 256;
+  long blocks = (n + threads - 1) / threads;
+  if (blocks > 16L * num_sms()) blocks = 16L * num_sms();
+  if (blocks < 1) blocks = 1;
+  count_launch();
+  k_advection2d_inputs<<<(unsigned)blocks, threads, 0, s>>>(w, f, g, mx, my);
+  return cudaGetLastError();
+}
+
+}  // namespace idc

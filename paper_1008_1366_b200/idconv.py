@@ -50,6 +50,12 @@ SIGNATURES = {
     "idc_cconv3d_dist_emulated": ([_I, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), _S, _S, _S,
                                    _P, _S, _P], _I),
     "idc_hconv3d_dist": ([_P, _P, _P, _S, _S, _S, _P, _S, _P], _I),
+    "idc_hconv1d_dot": ([_P, _P, _S, _S, _S, _P], _I),
+    "idc_dot_workspace_bytes": ([_I, _S, _S, _S], _S),
+    "idc_hconv2d_dot": ([_P, _P, _S, _S, _S, _P, _S, _P], _I),
+    "idc_enforce_symmetry_2d": ([_P, _S, _S, _S, _P], _I),
+    "idc_advection2d_workspace_bytes": ([_S, _S], _S),
+    "idc_advection2d": ([_P, _P, _S, _S, _P, _S, _P], _I),
     "idc_dist_plan_kind": ([_I, _S, _S, _S, _I, _I, ctypes.POINTER(ctypes.c_longlong)], _I),
     "idc_dist_emulated_workspace_bytes_kind": ([_I, _S, _S, _S, _I], _S),
     "idc_hconv3d_dist_emulated": ([_I, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), _S, _S, _S,
@@ -134,6 +140,11 @@ def _prep(arrs):
     if any(a.device != dev for a in arrs):
         raise ValueError("all arrays must be on the same device")
     return dev.type == "cuda"
+
+
+def _need_cuda(arrs):
+    if not _prep(arrs):
+        raise ValueError("this call takes CUDA tensors (no host or CPU path)")
 
 
 def _run(arrs, kind, sizes, batch, call, work, stream):
@@ -237,6 +248,62 @@ def fill_uniform(out, array_id: int, seed: int, start: int = 0, stream=None):
 def launch_count() -> int:
     """Hot-path kernels launched by the library so far (idc_launch_count)."""
     return int(lib().idc_launch_count())
+
+
+# ------------------------------------ multivector dot products (NEXT-1) --
+
+def hconv1d_dot(f, g, stream=None):
+    """sum_i hconv1d(f[i], g[i]).  f, g: (M, batch, m) or (M, m)
+    complex128 CUDA tensors; the result is written to f[0] and returned."""
+    _prep([f, g])
+    if f.dim() == 2:
+        M, B, m = f.shape[0], 1, f.shape[1]
+    else:
+        M, B, m = f.shape
+    _check(lib().idc_hconv1d_dot(ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(g.data_ptr()), M, m, B,
+                                 _stream_ptr(stream, f.device)), "idc_hconv1d_dot")
+    return f[0]
+
+
+def hconv2d_dot(f, g, work=None, stream=None):
+    """sum_i hconv2d(f[i], g[i]): f, g (M, 2mx-1, my); result in f[0]."""
+    _need_cuda([f, g])
+    M, nx, my = f.shape
+    mx = (nx + 1) // 2
+    nb = int(lib().idc_dot_workspace_bytes(HCONV2D, M, mx, my))
+    if nb == 0:
+        raise IdcError(ERR_UNSUPPORTED, "idc_hconv2d_dot")
+    w, wb = _workspace(nb, f.device, work)
+    _check(lib().idc_hconv2d_dot(ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(g.data_ptr()), M, mx, my,
+                                 ctypes.c_void_p(w.data_ptr()), wb, _stream_ptr(stream, f.device)), "idc_hconv2d_dot")
+    return f[0]
+
+
+def enforce_symmetry_2d(a, stream=None):
+    """Hermitian projection of the ky = 0 line of a (..., 2mx-1, my) array, in place."""
+    _need_cuda([a])
+    nx, my = a.shape[-2:]
+    B = a.numel() // (nx * my)
+    _check(lib().idc_enforce_symmetry_2d(ctypes.c_void_p(a.data_ptr()), (nx + 1) // 2, my, B,
+                                         _stream_ptr(stream, a.device)), "idc_enforce_symmetry_2d")
+    return a
+
+
+def advection2d(w, out=None, work=None, stream=None):
+    """The paper's 2D Euler call conv2(i kx w, i ky w, i ky w/k^2, -i kx w/k^2)
+     on a (2mx-1, my) centered Hermitian vorticity spectrum."""
+    _need_cuda([w])
+    nx, my = w.shape
+    mx = (nx + 1) // 2
+    if out is None:
+        out = torch.empty_like(w)
+    nb = int(lib().idc_advection2d_workspace_bytes(mx, my))
+    if nb == 0:
+        raise IdcError(ERR_UNSUPPORTED, "idc_advection2d")
+    wk, wb = _workspace(nb, w.device, work)
+    _check(lib().idc_advection2d(ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(out.data_ptr()), mx, my,
+                                 ctypes.c_void_p(wk.data_ptr()), wb, _stream_ptr(stream, w.device)), "idc_advection2d")
+    return out
 
 
 # ------------------------------------------------------ distributed 3D --
