@@ -200,6 +200,23 @@ IDC_API size_t idc_dist_emulated_workspace_bytes_kind(idc_kind k, size_t mx, siz
 IDC_API idc_status idc_hconv3d_dist_emulated(int nranks, idc_c128** f_slabs, idc_c128** g_slabs, size_t mx,
                                              size_t my, size_t mz, void* work, size_t work_bytes, idc_stream stream);
 
+/* ---- host buffers ------------------------------------------------------- */
+
+/* Batched 1D convolution (k = IDC_CCONV1D, IDC_HCONV1D or IDC_TCONV1D) on
+ * HOST arrays: in_host[0..1] (f, g) or [0..2] (f, g, h), each batch x m,
+ * out_host <- the result (may alias in_host[0]; inputs otherwise unchanged).
+ * Rows are streamed through the device in chunks of chunk_rows on an internal
+ * pool of streams: the copy of chunk c+1 in, the fused row kernel of chunk c
+ * and the copy of chunk c-1 out overlap.  Host memory should be page-locked
+ * (cudaHostAlloc / torch pin_memory) for the copies to be asynchronous.
+ * work: DEVICE workspace of idc_host_workspace_bytes(k, m, chunk_rows),
+ * 256-byte aligned.  Ordered after prior work on `stream`; `stream` waits for
+ * completion of all chunks (synchronize it before reading out_host). */
+IDC_API size_t idc_host_workspace_bytes(idc_kind k, size_t m, size_t chunk_rows);
+IDC_API idc_status idc_conv1d_host(idc_kind k, const idc_c128* const* in_host, idc_c128* out_host, size_t m,
+                                   size_t batch, size_t chunk_rows, void* work, size_t work_bytes,
+                                   idc_stream stream);
+
 /* ---- multivector dot-product convolutions ---------- */
 
 /* "we allow the convolution inputs to be arrays of vectors, f_i

@@ -54,10 +54,20 @@ long slab_group(size_t slab_bytes_all, long nslabs) {
   return std::max<long>(1, std::min<long>(G, nslabs));
 }
 // Internal stream pool for concurrent slab groups (created once per device).
-constexpr int kSlabStreams = 4;
+constexpr int kMaxSlabStreams = 4;
+// slab streams in flight (IDC_SLAB_STREAMS, 1..4, default 4; experiments only)
+int slab_streams() {
+  static int n = 0;
+  if (n == 0) {
+    const char* e = getenv("IDC_SLAB_STREAMS");
+    n = e ? atoi(e) : kMaxSlabStreams;
+    if (n < 1 || n > kMaxSlabStreams) n = kMaxSlabStreams;
+  }
+  return n;
+}
 struct Pool {
-  cudaStream_t s[kSlabStreams];
-  cudaEvent_t fork, done[kSlabStreams];
+  cudaStream_t s[kMaxSlabStreams];
+  cudaEvent_t fork, done[kMaxSlabStreams];
   bool ok = false;
 };
 Pool& pool() {
@@ -66,7 +76,7 @@ Pool& pool() {
   cudaGetDevice(&dev);
   Pool& q = p[dev & 15];
   if (!q.ok) {
-    for (int i = 0; i < kSlabStreams; ++i) {
+    for (int i = 0; i < kMaxSlabStreams; ++i) {
       cudaStreamCreateWithFlags(&q.s[i], cudaStreamNonBlocking);
       cudaEventCreateWithFlags(&q.done[i], cudaEventDisableTiming);
     }
@@ -86,24 +96,24 @@ size_t hconv2d_work_bytes(size_t mx, size_t my) {
   if (!pow2ok(mx) || !pow2ok(my)) return 0;
   return 2 * (mx + 1) * my * W16 + hconv_rows_work_bytes((int)my);
 }
-// slabs per group; kSlabStreams groups are in flight at once, so the L2
+// slabs per group; slab_streams() groups are in flight at once, so the L2
 // budget is shared between them
 static long c3_group(size_t mx, size_t my, size_t mz) {
-  return slab_group(kSlabStreams * 4 * my * mz * W16, 2 * (long)mx);
+  return slab_group(slab_streams() * 4 * my * mz * W16, 2 * (long)mx);
 }
 static long h3_group(size_t mx, size_t my, size_t mz) {
-  return slab_group(kSlabStreams * 2 * ((2 * my - 1) + (my + 1)) * mz * W16, 3 * (long)mx);
+  return slab_group(slab_streams() * 2 * ((2 * my - 1) + (my + 1)) * mz * W16, 3 * (long)mx);
 }
 size_t cconv3d_work_bytes(size_t mx, size_t my, size_t mz) {
   if (!pow2ok(mx) || !pow2ok(my) || !pow2ok(mz)) return 0;
   const long G = c3_group(mx, my, mz);
-  return 2 * mx * my * mz * W16 + kSlabStreams * (2 * (size_t)G * my * mz * W16 + cconv_rows_work_bytes((int)mz));
+  return 2 * mx * my * mz * W16 + slab_streams() * (2 * (size_t)G * my * mz * W16 + cconv_rows_work_bytes((int)mz));
 }
 size_t hconv3d_work_bytes(size_t mx, size_t my, size_t mz) {
   if (!pow2ok(mx) || !pow2ok(my) || !pow2ok(mz)) return 0;
   const long G = h3_group(mx, my, mz);
   return 2 * (mx + 1) * (2 * my - 1) * mz * W16 +
-         kSlabStreams * (2 * (size_t)G * (my + 1) * mz * W16 + hconv_rows_work_bytes((int)mz));
+         slab_streams() * (2 * (size_t)G * (my + 1) * mz * W16 + hconv_rows_work_bytes((int)mz));
 }
 
 // ------------------------------------------------------------------- 2D --
@@ -159,20 +169,20 @@ cudaError_t run_cconv3d(double2* f, double2* g, int mx, int my, int mz, double2*
   const long G = c3_group(mx, my, mz);
   double2* U = work;
   double2* V = U + n;
-  double2* per = V + n;                                    // kSlabStreams x (U2, V2, row work)
+  double2* per = V + n;                                    // slab_streams() x (U2, V2, row work)
   const long per_elems = 2 * G * slab + (long)(cconv_rows_work_bytes(mz) / W16);
   IDC_TRY(launch_pad_bwd(f, g, U, V, mx, slab, 1, 0, 0, s));              // x: fftpadBackward over all (y,z)
   Pool& P = pool();
   IDC_TRY(cudaEventRecord(P.fork, s));
-  for (int i = 0; i < kSlabStreams; ++i) IDC_TRY(cudaStreamWaitEvent(P.s[i], P.fork, 0));
+  for (int i = 0; i < slab_streams(); ++i) IDC_TRY(cudaStreamWaitEvent(P.s[i], P.fork, 0));
   long gi = 0;
   for (int half = 0; half < 2; ++half) {                                   // x-residue slabs: f (even), U (odd)
     double2* A = half == 0 ? f : U;
     double2* B = half == 0 ? g : V;
     for (long s0 = 0; s0 < mx; s0 += G, ++gi) {
       const long gs = std::min<long>(G, mx - s0);
-      cudaStream_t st = P.s[gi % kSlabStreams];
-      double2* U2 = per + (gi % kSlabStreams) * per_elems;
+      cudaStream_t st = P.s[gi % slab_streams()];
+      double2* U2 = per + (gi % slab_streams()) * per_elems;
       double2* V2 = U2 + G * slab;
       double2* rw = V2 + G * slab;
       double2* a = A + s0 * slab;
@@ -184,7 +194,7 @@ cudaError_t run_cconv3d(double2* f, double2* g, int mx, int my, int mz, double2*
       IDC_TRY(launch_pad_fwd(a, U2, my, mz, gs, slab, slab, st));
     }
   }
-  for (int i = 0; i < kSlabStreams; ++i) {
+  for (int i = 0; i < slab_streams(); ++i) {
     IDC_TRY(cudaEventRecord(P.done[i], P.s[i]));
     IDC_TRY(cudaStreamWaitEvent(s, P.done[i], 0));
   }
@@ -202,7 +212,7 @@ cudaError_t run_hconv3d(double2* f, double2* g, int mx, int my, int mz, double2*
   IDC_TRY(launch_pad0_bwd(f, g, U, V, mx, slab, 1, 0, 0, s));             // x: fft0padBackward
   Pool& P = pool();
   IDC_TRY(cudaEventRecord(P.fork, s));
-  for (int i = 0; i < kSlabStreams; ++i) IDC_TRY(cudaStreamWaitEvent(P.s[i], P.fork, 0));
+  for (int i = 0; i < slab_streams(); ++i) IDC_TRY(cudaStreamWaitEvent(P.s[i], P.fork, 0));
   long gi = 0;
   for (int half = 0; half < 2; ++half) {                                   // slabs: 2mx-1 in f, mx+1 in U
     double2* A = half == 0 ? f : U;
@@ -210,8 +220,8 @@ cudaError_t run_hconv3d(double2* f, double2* g, int mx, int my, int mz, double2*
     const long ns = half == 0 ? 2L * mx - 1 : (long)mx + 1;
     for (long s0 = 0; s0 < ns; s0 += G, ++gi) {
       const long gs = std::min<long>(G, ns - s0);
-      cudaStream_t st = P.s[gi % kSlabStreams];
-      double2* U2 = per + (gi % kSlabStreams) * per_elems;
+      cudaStream_t st = P.s[gi % slab_streams()];
+      double2* U2 = per + (gi % slab_streams()) * per_elems;
       double2* V2 = U2 + G * uslab;
       double2* rw = V2 + G * uslab;
       double2* a = A + s0 * slab;
@@ -223,7 +233,7 @@ cudaError_t run_hconv3d(double2* f, double2* g, int mx, int my, int mz, double2*
       IDC_TRY(launch_pad0_fwd(a, U2, my, mz, gs, slab, uslab, st));
     }
   }
-  for (int i = 0; i < kSlabStreams; ++i) {
+  for (int i = 0; i < slab_streams(); ++i) {
     IDC_TRY(cudaEventRecord(P.done[i], P.s[i]));
     IDC_TRY(cudaStreamWaitEvent(s, P.done[i], 0));
   }

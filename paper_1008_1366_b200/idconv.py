@@ -51,6 +51,8 @@ SIGNATURES = {
                                    _P, _S, _P], _I),
     "idc_hconv3d_dist": ([_P, _P, _P, _S, _S, _S, _P, _S, _P], _I),
     "idc_hconv1d_dot": ([_P, _P, _S, _S, _S, _P], _I),
+    "idc_host_workspace_bytes": ([_I, _S, _S], _S),
+    "idc_conv1d_host": ([_I, ctypes.POINTER(ctypes.c_void_p), _P, _S, _S, _S, _P, _S, _P], _I),
     "idc_dot_workspace_bytes": ([_I, _S, _S, _S], _S),
     "idc_hconv2d_dot": ([_P, _P, _S, _S, _S, _P, _S, _P], _I),
     "idc_enforce_symmetry_2d": ([_P, _S, _S, _S, _P], _I),
@@ -147,9 +149,33 @@ def _need_cuda(arrs):
         raise ValueError("this call takes CUDA tensors (no host or CPU path)")
 
 
+HOST_CHUNK_BYTES = 16 << 20      # rows per chunk of the host-buffer 1D path: ~16 MB per array
+
+
+def _run_host_1d(arrs, kind, m, batch, stream):
+    """Host tensors of a 1D kind: idc_conv1d_host streams chunks of rows through
+    the device (copies of chunk c+1 overlap the kernel of chunk c and the copy
+    back of chunk c-1; pinned host memory makes the copies asynchronous)."""
+    device = torch.device("cuda", torch.cuda.current_device())
+    chunk = max(1, min(batch, HOST_CHUNK_BYTES // (16 * m)))
+    nb = int(lib().idc_host_workspace_bytes(kind, m, chunk))
+    if nb == 0:
+        raise IdcError(ERR_UNSUPPORTED, "idc_conv1d_host")
+    w, wb = _workspace(nb + 256, device, None)
+    base = (w.data_ptr() + 255) // 256 * 256
+    ins = (ctypes.c_void_p * len(arrs))(*[a.data_ptr() for a in arrs])
+    _check(lib().idc_conv1d_host(kind, ins, ctypes.c_void_p(arrs[0].data_ptr()), m, batch, chunk,
+                                 ctypes.c_void_p(base), nb, _stream_ptr(stream, device)), "idc_conv1d_host")
+    if stream is None:                      # host results are complete on return
+        torch.cuda.current_stream(device).synchronize()
+    return arrs[0]
+
+
 def _run(arrs, kind, sizes, batch, call, work, stream):
     """Marshal (possibly host) tensors through one C-ABI call."""
     on_dev = _prep(arrs)
+    if not on_dev and kind in (CCONV1D, HCONV1D, TCONV1D):
+        return _run_host_1d(arrs, kind, sizes[0], batch, stream)
     if on_dev:
         dev_arrs = arrs
         device = arrs[0].device
