@@ -72,15 +72,9 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
   constexpr int T = C::T;
   extern __shared__ __align__(16) double2 smem[];
   const int grp = threadIdx.x / T, t = threadIdx.x - grp * T;
-#ifndef IDC_CCONV_SMEM_STASH
   constexpr bool FFT2 = E <= 8;
   double2* xb = smem + grp * (FFT2 ? 2 : 1) * C::XB;   // one exchange buffer per vector in flight
   double2* xb2 = xb + C::XB;
-#else
-  double2* xb = smem + grp * (C::XB + 2 * M);
-  double2* S = xb + C::XB;
-  double2* P = S + M;
-#endif
   const auto sync = row_sync<M, E, G>(grp);
   const double inv = 1.0 / (2.0 * M);
   for (long row0 = (long)blockIdx.x * G; row0 < nrows; row0 += (long)gridDim.x * G) {
@@ -91,7 +85,6 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
     const bool ok = row < nrows;
     const double2* fr = f + (ok ? row : 0) * (long)M;
     const double2* gr = g + (ok ? row : 0) * (long)M;
-#ifndef IDC_CCONV_SMEM_STASH
     // the next rows of this group: bulk prefetch into L2 (hides the HBM
     // latency of the first loads of the next iteration)
     if (IDC_ROWS_PREFETCH && t == 0 && row + (long)gridDim.x * G < nrows) {
@@ -147,44 +140,6 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
         fw[t + T * i] = cscale(cadd(x[i], cmul(y[i], w)), inv);
       });
     }
-#else
-    double2 v[E];
-    // r = 0: u = fft^{-1} f ; v = fft^{-1} g ; u*v
-#pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = ldv(&fr[t + T * i]);
-    fft<M, E, +1>(v, t, xb, twM, sync);
-#pragma unroll
-    for (int i = 0; i < E; ++i) S[t + T * i] = v[i];
-#pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = ldv(&gr[t + T * i]);
-    fft<M, E, +1>(v, t, xb, twM, sync);
-#pragma unroll
-    for (int i = 0; i < E; ++i) P[t + T * i] = cmul(S[t + T * i], v[i]);
-    // r = 1: zeta_{2m}^k-shifted streams
-#pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = cmul(ldv(&fr[t + T * i]), ldtw(&tw2M[t + T * i]));
-    fft<M, E, +1>(v, t, xb, twM, sync);
-#pragma unroll
-    for (int i = 0; i < E; ++i) S[t + T * i] = v[i];
-#pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = cmul(ldv(&gr[t + T * i]), ldtw(&tw2M[t + T * i]));
-    fft<M, E, +1>(v, t, xb, twM, sync);
-#pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = cmul(S[t + T * i], v[i]);
-    // forward transforms, recombination and 1/(2m)
-    fft<M, E, -1>(v, t, xb, twM, sync);
-#pragma unroll
-    for (int i = 0; i < E; ++i) S[t + T * i] = cmulc(v[i], ldtw(&tw2M[t + T * i]));
-#pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = P[t + T * i];
-    fft<M, E, -1>(v, t, xb, twM, sync);
-    if (ok) {
-      double2* fw = f + row * (long)M;
-#pragma unroll
-      for (int i = 0; i < E; ++i) fw[t + T * i] = cscale(cadd(v[i], S[t + T * i]), inv);
-    }
-
-#endif
   }
 }
 
@@ -401,11 +356,7 @@ cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s) {
   const double2* tw2M = zeta_table(2 * M);
   if (!twM || !tw2M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw2M};
-#ifndef IDC_CCONV_SMEM_STASH
   const size_t per = (E <= 8 ? 2 : 1) * C::XB;   // exchange buffer(s) only (intermediates in registers)
-#else
-  const size_t per = C::XB + 2 * M;
-#endif
   return launch2(k_cconv_rows2<M, E, G>, C::THREADS, (size_t)G * per * 16, nrows, G, s, args);
 }
 
