@@ -238,6 +238,19 @@ IDC_API idc_status idc_hconv1d_dot(idc_c128* f, idc_c128* g, size_t npairs, size
 IDC_API size_t idc_dot_workspace_bytes(idc_kind k, size_t npairs, size_t m0, size_t m1);
 IDC_API idc_status idc_hconv2d_dot(idc_c128* f, idc_c128* g, size_t npairs, size_t mx, size_t my, void* work,
                                    size_t work_bytes, idc_stream stream);
+/* idc_cconv1d_dot: complex rows (Function cconv, D1 summed over i),
+ * 1 <= m <= 4096; idc_tconv1d_dot: centered Hermitian ternary rows
+ * (Function tconv, D3 summed over the npairs triples f_i, g_i, h_i),
+ * 2 <= m <= 4096.  Same stacking as idc_hconv1d_dot; no workspace. */
+IDC_API idc_status idc_cconv1d_dot(idc_c128* f, idc_c128* g, size_t npairs, size_t m, size_t batch,
+                                   idc_stream stream);
+IDC_API idc_status idc_tconv1d_dot(idc_c128* f, idc_c128* g, idc_c128* h, size_t npairs, size_t m, size_t batch,
+                                   idc_stream stream);
+/* idc_cconv2d_dot: npairs stacked mx x my complex arrays (my <= 4096);
+ * pair 0 <- sum_i cconv2d(f_i, g_i).  Workspace idc_dot_workspace_bytes(
+ * IDC_CCONV2D, npairs, mx, my) = 2 npairs mx my words (P:803-808 per pair). */
+IDC_API idc_status idc_cconv2d_dot(idc_c128* f, idc_c128* g, size_t npairs, size_t mx, size_t my, void* work,
+                                   size_t work_bytes, idc_stream stream);
 /* Hermitian projection of the stored ky = 0 line of batch (2mx-1) x my
  * arrays, in place (AMB-7): U_{kx,0} <- (U_{kx,0} +
  * conj U_{-kx,0})/2, so U_{0,0} becomes real.  Idempotent. */

@@ -171,9 +171,45 @@ idc_status idc_hconv3d(idc_c128* f, idc_c128* g, size_t mx, size_t my, size_t mz
 
 size_t idc_dot_workspace_bytes(idc_kind k, size_t npairs, size_t m0, size_t m1) {
   if (npairs == 0) return 0;
-  if (k == IDC_HCONV1D) return 0;
   if (k == IDC_HCONV2D) return idc::hconv2d_dot_work_bytes(npairs, m0, m1);
-  return 0;
+  if (k == IDC_CCONV2D) return idc::cconv2d_dot_work_bytes(npairs, m0, m1);
+  return 0;   // 1D kinds need none
+}
+
+idc_status idc_cconv1d_dot(idc_c128* f, idc_c128* g, size_t npairs, size_t m, size_t batch, idc_stream stream) {
+  if (m == 0 || batch == 0 || npairs == 0) return IDC_ERR_INVALID;
+  if (!size_ok(m, 1, 4096)) return IDC_ERR_UNSUPPORTED;
+  const void* arrs[] = {f, g};
+  idc_status st = check_arrays(arrs, 2, npairs * m * batch * sizeof(idc_c128), nullptr, 0, 0);
+  if (st != IDC_OK) return st;
+  return from_cuda(idc::launch_cconv_dot_rows(reinterpret_cast<double2*>(f), reinterpret_cast<double2*>(g),
+                                              (int)npairs, (long)(m * batch), (int)m, (long)batch,
+                                              (cudaStream_t)stream));
+}
+
+idc_status idc_tconv1d_dot(idc_c128* f, idc_c128* g, idc_c128* h, size_t npairs, size_t m, size_t batch,
+                           idc_stream stream) {
+  if (m == 0 || batch == 0 || npairs == 0) return IDC_ERR_INVALID;
+  if (!size_ok(m, 2, 4096)) return IDC_ERR_UNSUPPORTED;
+  const void* arrs[] = {f, g, h};
+  idc_status st = check_arrays(arrs, 3, npairs * m * batch * sizeof(idc_c128), nullptr, 0, 0);
+  if (st != IDC_OK) return st;
+  return from_cuda(idc::launch_tconv_dot_rows(reinterpret_cast<double2*>(f), reinterpret_cast<double2*>(g),
+                                              reinterpret_cast<double2*>(h), (int)npairs, (long)(m * batch), (int)m,
+                                              (long)batch, (cudaStream_t)stream));
+}
+
+idc_status idc_cconv2d_dot(idc_c128* f, idc_c128* g, size_t npairs, size_t mx, size_t my, void* work,
+                           size_t work_bytes, idc_stream stream) {
+  if (mx == 0 || my == 0 || npairs == 0) return IDC_ERR_INVALID;
+  if (!size_ok(mx, 1, 8192) || !size_ok(my, 1, 4096)) return IDC_ERR_UNSUPPORTED;
+  size_t need = idc::cconv2d_dot_work_bytes(npairs, mx, my);
+  if (need == 0) return IDC_ERR_UNSUPPORTED;
+  const void* arrs[] = {f, g};
+  idc_status st = check_arrays(arrs, 2, npairs * mx * my * sizeof(idc_c128), work, work_bytes, need);
+  if (st != IDC_OK) return st;
+  return from_cuda(idc::run_cconv2d_dot(reinterpret_cast<double2*>(f), reinterpret_cast<double2*>(g), (int)npairs,
+                                        (int)mx, (int)my, reinterpret_cast<double2*>(work), (cudaStream_t)stream));
 }
 
 idc_status idc_hconv1d_dot(idc_c128* f, idc_c128* g, size_t npairs, size_t m, size_t batch, idc_stream stream) {

@@ -35,6 +35,11 @@ template <int M> cudaError_t tconv_rows3(double2* f, double2* g, double2* h, lon
 // row pairs (pair i at f + i*istride, g + i*istride), result in pair 0.
 cudaError_t launch_hconv_dot_rows(double2* f, const double2* g, int npairs, long istride, int m, long nrows,
                                   cudaStream_t s);
+// K2d / K4d (rows_dot.cu): complex and ternary dot products, same layout.
+cudaError_t launch_cconv_dot_rows(double2* f, const double2* g, int npairs, long istride, int m, long nrows,
+                                  cudaStream_t s);
+cudaError_t launch_tconv_dot_rows(double2* f, const double2* g, const double2* h, int npairs, long istride, int m,
+                                  long nrows, cudaStream_t s);
 // Hermitian projection of the ky = 0 lines of batch (2mx-1) x my arrays.
 cudaError_t launch_enforce_symmetry_2d(double2* a, int mx, int my, long batch, cudaStream_t s);
 // The four M = 2 inputs of the 2D Euler advective term from w.

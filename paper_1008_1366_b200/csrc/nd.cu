@@ -163,6 +163,23 @@ cudaError_t run_hconv2d_dot(double2* f, double2* g, int npairs, int mx, int my, 
   return launch_pad0_fwd(f, U, mx, my, 1, 0, 0, s);                      // fft0padForward, pair 0
 }
 
+// Complex 2D dot product (Function cconv2 with sum_i f_i * g_i): K5 along x on
+// all 2*npairs arrays, K2d on the rows of both x-streams, K6 on pair 0.
+size_t cconv2d_dot_work_bytes(size_t npairs, size_t mx, size_t my) {
+  if (!pow2ok(mx) || !pow2ok(my) || my > 4096 || npairs == 0) return 0;
+  return 2 * npairs * mx * my * W16;
+}
+
+cudaError_t run_cconv2d_dot(double2* f, double2* g, int npairs, int mx, int my, double2* work, cudaStream_t s) {
+  const long n = (long)mx * my;
+  double2* U = work;
+  double2* V = work + (long)npairs * n;
+  IDC_TRY(launch_pad_bwd(f, g, U, V, mx, my, npairs, n, n, s));           // fftpadBackward on every column
+  IDC_TRY(launch_cconv_dot_rows(f, g, npairs, n, my, mx, s));             // dot-product rows, even x-stream
+  IDC_TRY(launch_cconv_dot_rows(U, V, npairs, n, my, mx, s));             // dot-product rows, odd x-stream
+  return launch_pad_fwd(f, U, mx, my, 1, 0, 0, s);                        // fftpadForward, pair 0
+}
+
 // ------------------------------------------------------------------- 3D --
 cudaError_t run_cconv3d(double2* f, double2* g, int mx, int my, int mz, double2* work, cudaStream_t s) {
   const long slab = (long)my * mz, n = (long)mx * slab;

@@ -143,6 +143,196 @@ k_hconv_dot_rows(double2* __restrict__ f, const double2* __restrict__ g, int npa
   }
 }
 
+// ===================================================================== K2d ==
+// Function cconv with the dot product: for each residue r the
+// products of all pairs are accumulated, acc_r = sum_i fft^{-1}(f_i^r) *
+// fft^{-1}(g_i^r), and each accumulator is forward transformed once:
+// f_0 <- (fft(acc_0) + zeta_{2m}^{-k} fft(acc_1)) / (2m).  E = 8 so that the
+// two accumulators and the pair being transformed fit in registers; the two
+// transforms of a pair (and the two forward transforms) run in lockstep.
+template <int M>
+struct D2Cfg {
+  static constexpr int E = M < 8 ? M : 8;
+  static constexpr int T = M / E;
+  static constexpr int G = T >= 256 ? 1 : 256 / T;
+  static constexpr int THREADS = G * T;
+  static constexpr int XB = xbuf_elems<M, E>() > M ? xbuf_elems<M, E>() : M;
+  static constexpr bool NAMED = (T % 32 == 0) && G > 1;
+};
+
+template <int M>
+__device__ __forceinline__ DSync<D2Cfg<M>::NAMED> d2sync(int grp) {
+  if constexpr (D2Cfg<M>::NAMED) return DSync<true>{1 + grp, D2Cfg<M>::T};
+  else return DSync<false>{};
+}
+
+template <int M>
+__global__ void __launch_bounds__(D2Cfg<M>::THREADS, 1)
+k_cconv_dot_rows(double2* __restrict__ f, const double2* __restrict__ g, int npairs, long istride, long nrows,
+                 const double2* __restrict__ twM, const double2* __restrict__ tw2M) {
+  using C = D2Cfg<M>;
+  constexpr int E = C::E, T = C::T, G = C::G;
+  extern __shared__ __align__(16) double2 smem[];
+  const int grp = threadIdx.x / T, t = threadIdx.x - grp * T;
+  double2* xb = smem + grp * 2 * C::XB;
+  double2* xb2 = xb + C::XB;
+  const auto sync = d2sync<M>(grp);
+  const double inv = 1.0 / (2.0 * M);
+  for (long row0 = (long)blockIdx.x * G; row0 < nrows; row0 += (long)gridDim.x * G) {
+    const long row = row0 + grp;
+    if constexpr (C::NAMED) {
+      if (row >= nrows) break;
+    }
+    const bool ok = row < nrows;
+    const long roff = (ok ? row : 0) * (long)M;
+    double2 a0[E], a1[E], x[E], y[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) a0[i] = a1[i] = make_double2(0.0, 0.0);
+#pragma unroll 1
+    for (int q = 0; q < npairs; ++q) {
+      const double2* fr = f + q * istride + roff;
+      const double2* gr = g + q * istride + roff;
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        x[i] = ldv(&fr[t + T * i]);
+        y[i] = ldv(&gr[t + T * i]);
+      }
+      fft2<M, E, +1>(x, y, t, xb, xb2, twM, sync);                         // r = 0
+#pragma unroll
+      for (int i = 0; i < E; ++i) a0[i] = cadd(a0[i], cmul(x[i], y[i]));
+      const double2 zt = ldtw(&tw2M[t]);                                   // zeta_{2m}^k = zeta_{2m}^t zeta_{2E}^i
+      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) {
+        x[i] = cmul(ldv(&fr[t + T * i]), w);
+        y[i] = cmul(ldv(&gr[t + T * i]), w);
+      });
+      fft2<M, E, +1>(x, y, t, xb, xb2, twM, sync);                         // r = 1
+#pragma unroll
+      for (int i = 0; i < E; ++i) a1[i] = cadd(a1[i], cmul(x[i], y[i]));
+    }
+    fft2<M, E, -1>(a0, a1, t, xb, xb2, twM, sync);                         // forward
+    if (ok) {
+      double2* fw = f + roff;
+      for_roots<2 * E, 1, -1, E>(cconj(ldtw(&tw2M[t])), [&](int i, double2 w) {
+        fw[t + T * i] = cscale(cadd(a0[i], cmul(a1[i], w)), inv);
+      });
+    }
+  }
+}
+
+// ===================================================================== K4d ==
+// Centered Hermitian ternary dot product sum_i f_i * g_i * h_i (P:859-867
+// applied to Function tconv): per residue pair (r0, r0 + 1) of the four-
+// residue form every triple's
+// products u^f u^g u^h are accumulated before the one forward transform of
+// the pair; the first pair's recombined contribution is kept in shared
+// memory (ACC) until the second pair adds to it.
+template <int M>
+__global__ void __launch_bounds__(D2Cfg<M>::THREADS, 1)
+k_tconv_dot_rows(double2* __restrict__ f, const double2* __restrict__ g, const double2* __restrict__ h, int npairs,
+                 long istride, long nrows, const double2* __restrict__ twM, const double2* __restrict__ tw4M) {
+  using C = D2Cfg<M>;
+  constexpr int E = C::E, T = C::T, G = C::G;
+  extern __shared__ __align__(16) double2 smem[];
+  const int grp = threadIdx.x / T, t = threadIdx.x - grp * T;
+  double2* xb = smem + grp * (C::XB + M);
+  double2* ACC = xb + C::XB;
+  const auto sync = d2sync<M>(grp);
+  const double inv = 1.0 / (4.0 * M);
+  for (long row0 = (long)blockIdx.x * G; row0 < nrows; row0 += (long)gridDim.x * G) {
+    const long row = row0 + grp;
+    if constexpr (C::NAMED) {
+      if (row >= nrows) break;
+    }
+    const bool ok = row < nrows;
+    const long roff = (ok ? row : 0) * (long)M;
+    auto pair = [&](auto R0) {
+      constexpr int r0 = decltype(R0)::value;
+      const double2 ca = r0 == 0 ? make_double2(1, 0) : make_double2(-1, 0);   // (-i)^{r0}
+      const double2 cb = r0 == 0 ? make_double2(0, -1) : make_double2(0, 1);   // (-i)^{r0+1}
+      double2 acc[E], v[E];
+      double a0[E], a1[E];
+#pragma unroll
+      for (int i = 0; i < E; ++i) acc[i] = make_double2(0.0, 0.0);
+#pragma unroll 1
+      for (int q = 0; q < npairs; ++q) {
+        const double2* fr = f + q * istride + roff;
+        const double2* gr = g + q * istride + roff;
+        const double2* hr = h + q * istride + roff;
+        // f/g streams r0, r0 + 1 (two c2r each), then h packed across the pair
+        const double2 za = ldtw(&tw4M[r0 * t]), zb = ldtw(&tw4M[(r0 + 1) * t]);
+        static_for<E>([&](auto I) {
+          constexpr int i = decltype(I)::value;
+          const int k = t + T * i;
+          if (i == 0 && t == 0) {
+            v[i] = make_double2(ldv(&fr[0]).x, ldv(&gr[0]).x);
+          } else {
+            const double2 fk = ldv(&fr[k]), gk = ldv(&gr[k]), fm = ldv(&fr[M - k]), gm = ldv(&gr[M - k]);
+            const double2 P = make_double2(fk.x - gk.y, fk.y + gk.x);
+            const double2 R = make_double2(fm.x + gm.y, gm.x - fm.y);
+            v[i] = cmul(twc<r0 * i, 4 * E, +1>(za), cadd(P, cmul(ca, R)));
+          }
+        });
+        fft<M, E, +1>(v, t, xb, twM, sync);
+#pragma unroll
+        for (int i = 0; i < E; ++i) a0[i] = v[i].x * v[i].y;
+        const double2 zb2 = ldtw(&tw4M[(r0 + 1) * t]);
+        static_for<E>([&](auto I) {
+          constexpr int i = decltype(I)::value;
+          const int k = t + T * i;
+          if (i == 0 && t == 0) {
+            v[i] = make_double2(ldv(&fr[0]).x, ldv(&gr[0]).x);
+          } else {
+            const double2 fk = ldv(&fr[k]), gk = ldv(&gr[k]), fm = ldv(&fr[M - k]), gm = ldv(&gr[M - k]);
+            const double2 P = make_double2(fk.x - gk.y, fk.y + gk.x);
+            const double2 R = make_double2(fm.x + gm.y, gm.x - fm.y);
+            v[i] = cmul(twc<(r0 + 1) * i, 4 * E, +1>(zb2), cadd(P, cmul(cb, R)));
+          }
+        });
+        fft<M, E, +1>(v, t, xb, twM, sync);
+#pragma unroll
+        for (int i = 0; i < E; ++i) a1[i] = v[i].x * v[i].y;
+        const double2 za3 = ldtw(&tw4M[r0 * t]), zb3 = ldtw(&tw4M[(r0 + 1) * t]);
+        static_for<E>([&](auto I) {
+          constexpr int i = decltype(I)::value;
+          const int k = t + T * i;
+          if (i == 0 && t == 0) {
+            const double h0 = ldv(&hr[0]).x;
+            v[i] = make_double2(h0, h0);
+          } else {
+            const double2 hk = ldv(&hr[k]), hm = cconj(ldv(&hr[M - k]));
+            const double2 w0 = cmul(twc<r0 * i, 4 * E, +1>(za3), cadd(hk, cmul(ca, hm)));
+            const double2 w1 = cmul(twc<(r0 + 1) * i, 4 * E, +1>(zb3), cadd(hk, cmul(cb, hm)));
+            v[i] = make_double2(w0.x - w1.y, w0.y + w1.x);
+          }
+        });
+        fft<M, E, +1>(v, t, xb, twM, sync);
+#pragma unroll
+        for (int i = 0; i < E; ++i) acc[i] = make_double2(fma(a0[i], v[i].x, acc[i].x), fma(a1[i], v[i].y, acc[i].y));
+      }
+      fft<M, E, -1>(acc, t, xb, twM, sync);
+      // separate the pair's two real-data spectra through acc_{m-k}, recombine
+#pragma unroll
+      for (int i = 0; i < E; ++i) xb[t + T * i] = acc[i];
+      sync();
+      const double2 za4 = ldtw(&tw4M[r0 * t]), zb4 = ldtw(&tw4M[(r0 + 1) * t]);
+      static_for<E>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        const int k = t + T * i;
+        const double2 a = acc[i], b = cconj(xb[(M - k) & (M - 1)]);
+        const double2 pp0 = cscale(cadd(a, b), 0.5);
+        const double2 d = csub(a, b);
+        const double2 pp1 = make_double2(0.5 * d.y, -0.5 * d.x);
+        const double2 ct = cadd(cmulc(pp0, twc<r0 * i, 4 * E, +1>(za4)), cmulc(pp1, twc<(r0 + 1) * i, 4 * E, +1>(zb4)));
+        if constexpr (r0 == 0) ACC[k] = ct;
+        else if (ok) f[roff + k] = cscale(cadd(ACC[k], ct), inv);
+      });
+      sync();
+    };
+    pair(std::integral_constant<int, 0>{});
+    pair(std::integral_constant<int, 2>{});
+  }
+}
+
 // ------------------------------------------------------- 2D helpers ------
 // Hermitian projection of the stored ky = 0 line of a (2mx-1) x my centered
 // array (AMB-7; "automatically enforce Hermitian symmetry"):
@@ -217,6 +407,84 @@ cudaError_t launch_hconv_dot_rows(double2* f, const double2* g, int npairs, long
     case 2048: return hconv_dot_rows<2048>(f, g, npairs, istride, nrows, s);
     case 4096: return hconv_dot_rows<4096>(f, g, npairs, istride, nrows, s);
   }
+  return cudaErrorInvalidValue;
+}
+
+template <int M>
+cudaError_t cconv_dot_rows(double2* f, const double2* g, int npairs, long istride, long nrows, cudaStream_t s) {
+  using C = D2Cfg<M>;
+  const double2* twM = pass_table(M, C::E);
+  const double2* tw2M = zeta_table(2 * M);
+  if (!twM || !tw2M) return cudaErrorMemoryAllocation;
+  const size_t smem = (size_t)C::G * 2 * C::XB * 16;
+  cudaError_t e = cudaFuncSetAttribute(k_cconv_dot_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  long need = (nrows + C::G - 1) / C::G, grid = num_sms();
+  if (need < grid) grid = need;
+  if (grid < 1) grid = 1;
+  void* args[] = {&f, &g, &npairs, &istride, &nrows, &twM, &tw2M};
+  count_launch();
+  return cudaLaunchKernel((const void*)k_cconv_dot_rows<M>, dim3((unsigned)grid), dim3(C::THREADS), args, smem, s);
+}
+
+template <int M>
+cudaError_t tconv_dot_rows(double2* f, const double2* g, const double2* h, int npairs, long istride, long nrows,
+                           cudaStream_t s) {
+  using C = D2Cfg<M>;
+  const double2* twM = pass_table(M, C::E);
+  const double2* tw4M = zeta_table(4 * M);
+  if (!twM || !tw4M) return cudaErrorMemoryAllocation;
+  const size_t smem = (size_t)C::G * (C::XB + M) * 16;
+  cudaError_t e = cudaFuncSetAttribute(k_tconv_dot_rows<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  long need = (nrows + C::G - 1) / C::G, grid = num_sms();
+  if (need < grid) grid = need;
+  if (grid < 1) grid = 1;
+  void* args[] = {&f, &g, &h, &npairs, &istride, &nrows, &twM, &tw4M};
+  count_launch();
+  return cudaLaunchKernel((const void*)k_tconv_dot_rows<M>, dim3((unsigned)grid), dim3(C::THREADS), args, smem, s);
+}
+
+cudaError_t launch_cconv_dot_rows(double2* f, const double2* g, int npairs, long istride, int m, long nrows,
+                                  cudaStream_t s) {
+#define IDC_CALL(MM) cconv_dot_rows<MM>(f, g, npairs, istride, nrows, s)
+  switch (m) {
+    case 1: return IDC_CALL(1);
+    case 2: return IDC_CALL(2);
+    case 4: return IDC_CALL(4);
+    case 8: return IDC_CALL(8);
+    case 16: return IDC_CALL(16);
+    case 32: return IDC_CALL(32);
+    case 64: return IDC_CALL(64);
+    case 128: return IDC_CALL(128);
+    case 256: return IDC_CALL(256);
+    case 512: return IDC_CALL(512);
+    case 1024: return IDC_CALL(1024);
+    case 2048: return IDC_CALL(2048);
+    case 4096: return IDC_CALL(4096);
+  }
+#undef IDC_CALL
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_tconv_dot_rows(double2* f, const double2* g, const double2* h, int npairs, long istride, int m,
+                                  long nrows, cudaStream_t s) {
+#define IDC_CALL(MM) tconv_dot_rows<MM>(f, g, h, npairs, istride, nrows, s)
+  switch (m) {
+    case 2: return IDC_CALL(2);
+    case 4: return IDC_CALL(4);
+    case 8: return IDC_CALL(8);
+    case 16: return IDC_CALL(16);
+    case 32: return IDC_CALL(32);
+    case 64: return IDC_CALL(64);
+    case 128: return IDC_CALL(128);
+    case 256: return IDC_CALL(256);
+    case 512: return IDC_CALL(512);
+    case 1024: return IDC_CALL(1024);
+    case 2048: return IDC_CALL(2048);
+    case 4096: return IDC_CALL(4096);
+  }
+#undef IDC_CALL
   return cudaErrorInvalidValue;
 }
 

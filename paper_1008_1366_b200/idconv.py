@@ -55,6 +55,9 @@ SIGNATURES = {
     "idc_conv1d_host": ([_I, ctypes.POINTER(ctypes.c_void_p), _P, _S, _S, _S, _P, _S, _P], _I),
     "idc_dot_workspace_bytes": ([_I, _S, _S, _S], _S),
     "idc_hconv2d_dot": ([_P, _P, _S, _S, _S, _P, _S, _P], _I),
+    "idc_cconv1d_dot": ([_P, _P, _S, _S, _S, _P], _I),
+    "idc_tconv1d_dot": ([_P, _P, _P, _S, _S, _S, _P], _I),
+    "idc_cconv2d_dot": ([_P, _P, _S, _S, _S, _P, _S, _P], _I),
     "idc_enforce_symmetry_2d": ([_P, _S, _S, _S, _P], _I),
     "idc_advection2d_workspace_bytes": ([_S, _S], _S),
     "idc_advection2d": ([_P, _P, _S, _S, _P, _S, _P], _I),
@@ -288,6 +291,41 @@ def hconv1d_dot(f, g, stream=None):
         M, B, m = f.shape
     _check(lib().idc_hconv1d_dot(ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(g.data_ptr()), M, m, B,
                                  _stream_ptr(stream, f.device)), "idc_hconv1d_dot")
+    return f[0]
+
+
+def _dot1d(name, arrs, stream):
+    _need_cuda(arrs)
+    f = arrs[0]
+    if f.dim() == 2:
+        M, B, m = f.shape[0], 1, f.shape[1]
+    else:
+        M, B, m = f.shape
+    ptrs = [ctypes.c_void_p(a.data_ptr()) for a in arrs]
+    _check(getattr(lib(), name)(*ptrs, M, m, B, _stream_ptr(stream, f.device)), name)
+    return f[0]
+
+
+def cconv1d_dot(f, g, stream=None):
+    """sum_i cconv1d(f[i], g[i]); f, g (M, batch, m) or (M, m); result in f[0]."""
+    return _dot1d("idc_cconv1d_dot", [f, g], stream)
+
+
+def tconv1d_dot(f, g, h, stream=None):
+    """sum_i tconv1d(f[i], g[i], h[i]); (M, batch, m) or (M, m); result in f[0]."""
+    return _dot1d("idc_tconv1d_dot", [f, g, h], stream)
+
+
+def cconv2d_dot(f, g, work=None, stream=None):
+    """sum_i cconv2d(f[i], g[i]): f, g (M, mx, my); result in f[0]."""
+    _need_cuda([f, g])
+    M, mx, my = f.shape
+    nb = int(lib().idc_dot_workspace_bytes(CCONV2D, M, mx, my))
+    if nb == 0:
+        raise IdcError(ERR_UNSUPPORTED, "idc_cconv2d_dot")
+    w, wb = _workspace(nb, f.device, work)
+    _check(lib().idc_cconv2d_dot(ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(g.data_ptr()), M, mx, my,
+                                 ctypes.c_void_p(w.data_ptr()), wb, _stream_ptr(stream, f.device)), "idc_cconv2d_dot")
     return f[0]
 
 

@@ -109,3 +109,38 @@ def test_enforce_symmetry_2d_gpu():
     assert np.array_equal(b[:, :, 1:], a[:, :, 1:])              # other lines untouched
     idconv.enforce_symmetry_2d(A)
     assert np.array_equal(A.cpu().numpy(), b)                    # idempotent
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,B,M", [(1, 2, 2), (8, 3, 1), (64, 5, 3), (1024, 3, 2), (4096, 2, 2)])
+def test_cconv1d_dot_gpu(m, B, M):
+    import torch
+    from paper_1008_1366_b200 import idconv
+    fs = [synthgen.cconv1d_inputs(m, B, roles=(2 * i, 2 * i + 1)) for i in range(M)]
+    F = torch.from_numpy(np.stack([a for a, b in fs])).cuda()
+    G = torch.from_numpy(np.stack([b for a, b in fs])).cuda()
+    idconv.cconv1d_dot(F, G)
+    assert rel_l2(F[0].cpu().numpy(), sum(direct.cconv1d(a, b) for a, b in fs)) < 1e-14
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,B,M", [(2, 2, 2), (16, 3, 1), (256, 3, 3), (2048, 2, 2), (4096, 1, 2)])
+def test_tconv1d_dot_gpu(m, B, M):
+    import torch
+    from paper_1008_1366_b200 import idconv
+    fs = [synthgen.hconv1d_inputs(m, B, roles=(3 * i, 3 * i + 1, 3 * i + 2)) for i in range(M)]
+    F, G, H = (torch.from_numpy(np.stack([t[j] for t in fs])).cuda() for j in range(3))
+    idconv.tconv1d_dot(F, G, H)
+    assert rel_l2(F[0].cpu().numpy(), sum(direct.tconv1d(*t) for t in fs)) < 1e-14
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mx,my,M", [(4, 8, 2), (16, 16, 3), (64, 32, 2)])
+def test_cconv2d_dot_gpu(mx, my, M):
+    import torch
+    from paper_1008_1366_b200 import idconv
+    fs = [synthgen.cconv2d_inputs(mx, my, 1, roles=(2 * i, 2 * i + 1)) for i in range(M)]
+    F = torch.from_numpy(np.stack([a[0] for a, b in fs])).cuda()
+    G = torch.from_numpy(np.stack([b[0] for a, b in fs])).cuda()
+    idconv.cconv2d_dot(F, G)
+    assert rel_l2(F[0].cpu().numpy(), sum(direct.cconv2d(a[0], b[0]) for a, b in fs)) < 1e-14
