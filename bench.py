@@ -82,6 +82,8 @@ WORKLOADS = {
         dict(kind="hconv2d", m=(2048, 2048), batch=1, narr=2)]),
     "c4adv": dict(desc="NEXT-1: 2D Euler advective term (M=2 dot-product conv2, P:867-876), mx=my=2048", parts=[
         dict(kind="advection2d", m=(2048, 2048), batch=1, narr=2)]),
+    "c4t": dict(desc="NEXT-2: 2D centered Hermitian ternary (Function tconv2, P:1087-1109), mx=my=2048", parts=[
+        dict(kind="tconv2d", m=(2048, 2048), batch=1, narr=3)]),
     "c5a": dict(desc="configs[4]: cconv3d 512^3", parts=[
         dict(kind="cconv3d", m=(512, 512, 512), batch=1, narr=2)]),
     "c5b": dict(desc="configs[4]: hconv3d 512^3 modes ((2m-1)^2 x m)", parts=[
@@ -97,6 +99,8 @@ def shape_of(p):
         return (p["batch"],) + tuple(m)
     if k in ("hconv2d", "advection2d"):
         return (2 * m[0] - 1, m[1])
+    if k == "tconv2d":
+        return (2 * m[0], m[1])
     if k == "cconv3d":
         return tuple(m)
     if k == "hconv3d":
@@ -130,6 +134,11 @@ def part_model(p):
         mx, my = m
         fl = 15 * my * flops_cfft(mx) + 3 * mx * 15 * flops_rfft(my)
         return W * (12 * (2 * mx - 1) * my + 30 * mx * my), fl
+    if kind == "tconv2d":
+        # x: 3 inputs -> 2 streams of 2mx (K5), rows: 2 x 2mx ternary rows, x forward (K6)
+        mx, my = m
+        fl = 8 * my * flops_cfft(2 * mx) + 4 * mx * 8 * flops_rfft(2 * my)
+        return 20 * W * 2 * mx * my, fl
     if kind == "cconv3d":
         mx, my, mz = m
         fl = 6 * my * mz * flops_cfft(mx) + 2 * mx * (6 * mz * flops_cfft(my) + 2 * my * 6 * flops_cfft(mz))
@@ -203,6 +212,10 @@ def make_inputs(idc, torch, p, rank, dev):
     """Seeded device inputs for one part (the config's recipe, DESIGN.md "Input
     recipe"); item ids offset by rank (weak scaling)."""
     kind, B, narr = p["kind"], p["batch"], p["narr"]
+    if kind == "tconv2d":       # paper layout: a zero kx = -mx row, then the hconv2d recipe
+        q = dict(p, kind="hconv2d")
+        return [torch.cat([torch.zeros((1, a.shape[1]), dtype=a.dtype, device=dev), a], dim=0).contiguous()
+                for a in make_inputs(idc, torch, q, rank, dev)]
     shp = shape_of(p)
     arrs = []
     for role in range(narr):

@@ -73,7 +73,8 @@ typedef enum {
   IDC_CCONV2D = 3,
   IDC_HCONV2D = 4,
   IDC_CCONV3D = 5,
-  IDC_HCONV3D = 6
+  IDC_HCONV3D = 6,
+  IDC_TCONV2D = 7
 } idc_kind;
 
 /* Human-readable name of a status code (static storage). */
@@ -134,6 +135,21 @@ IDC_API idc_status idc_cconv2d(idc_c128* f, idc_c128* g, size_t mx, size_t my, s
  * f <- the centered Hermitian convolution on the same index set. */
 IDC_API idc_status idc_hconv2d(idc_c128* f, idc_c128* g, size_t mx, size_t my,
                        void* work, size_t work_bytes, idc_stream stream);
+
+/* tconv2d: Function tconv2, the 2D centered
+ * Hermitian ternary convolution.  f, g, h: 2mx x my (the paper's layout:
+ * row i holds kx = i - mx, row 0 is the kx = -mx row, read as zero and
+ * zeroed on entry; column j holds ky = j >= 0, Hermitian extension and
+ * ky = 0 projection as hconv2d).  x uses the implicit double-dealiased
+ * centered transform fft0tpad (N = 4mx, two residues of size
+ * 2mx), rows the 1D ternary (Function tconv).  f rows 1..2mx-1 <- the sum
+ * over p + q + r = k of f_p g_q h_r, kx in [-mx+1, mx-1], ky in [0, my-1];
+ * row 0 of f is set to zero; g, h unspecified on return.  mx, my powers of
+ * two, 1 <= mx <= 2048, 1 <= my <= 4096.  Workspace
+ * idc_workspace_bytes(IDC_TCONV2D, mx, my, 0, 1) = 3 * 2mx * my words
+ * (U, V, W of Function tconv2). */
+IDC_API idc_status idc_tconv2d(idc_c128* f, idc_c128* g, idc_c128* h, size_t mx, size_t my, void* work,
+                               size_t work_bytes, idc_stream stream);
 
 /* ---- 3D -------------------------------------------------------------- */
 

@@ -27,6 +27,8 @@ Layers:
   (P:891-897, AMB-9).
 * O4 ``closed.*`` -- the paper's exact test families
   and their derived 2D/3D/ternary analogues.
+* O1b ``ternary2d.*`` -- the 2D centered Hermitian ternary sum (Function
+  tconv2, NEXT-2): two-stage direct 2D convolution and a brute-force loop.
 * O5 ``application.*`` -- the 2D pseudospectral Euler sum of P:867-876
   written out (pinned by a two-mode closed form and by its decomposition into
   D5 direct sums).
@@ -645,6 +647,58 @@ class application:
                 Wq = np.where(ok, W[np.clip(qx + mx - 1, 0, nx - 1), np.clip(qy + my - 1, 0, ny - 1)], 0.0)
                 term = (px * ky - py * kx) * inv * W * Wq
                 out[kx + mx - 1, ky] = term.sum()
+        return out
+
+
+# ===================================================== O1b 2D ternary (NEXT-2) ==
+
+class ternary2d:
+    """The 2D centered Hermitian ternary convolution of Function tconv2
+    (P:962-964 in two dimensions), written as sums."""
+
+    @staticmethod
+    def full(A):
+        """(2mx, my) paper layout (row 0 = kx -mx, ignored) -> full centered
+        (2mx-1, 2my-1) array with U_{kx,-ky} = conj U_{-kx,ky} and the ky = 0
+        line projected (AMB-7)."""
+        return application.hermitian_full2d(_c(A)[1:])
+
+    @staticmethod
+    def direct(f, g, h):
+        """t_k = sum_{p+q+r=k} f_p g_q h_r over the Hermitian-extended arrays
+        (|px|,|qx|,|rx| <= mx-1, |py|,|qy|,|ry| <= my-1), two stages of direct 2D
+        linear convolution (scipy.signal.convolve2d, method 'direct'); output in
+        the paper layout (2mx, my): row i = kx i - mx, row 0 = 0, ky in [0, my)."""
+        from scipy.signal import convolve2d
+        F, G, H = ternary2d.full(f), ternary2d.full(g), ternary2d.full(h)
+        nx, ny = F.shape
+        mx, my = (nx + 1) // 2, (ny + 1) // 2
+        e = convolve2d(F, G, mode="full")                 # indices p+q, origin (2mx-2, 2my-2)
+        t = convolve2d(e, H, mode="full")                 # origin (3mx-3, 3my-3)
+        ox, oy = 3 * (mx - 1), 3 * (my - 1)
+        out = np.zeros((2 * mx, my), dtype=np.complex128)
+        out[1:] = t[ox - (mx - 1):ox + mx, oy:oy + my]
+        return out
+
+    @staticmethod
+    def brute(f, g, h):
+        """Same sum by plain loops over all (p, q) with r = k - p - q (tiny sizes)."""
+        F, G, H = ternary2d.full(f), ternary2d.full(g), ternary2d.full(h)
+        nx, ny = F.shape
+        mx, my = (nx + 1) // 2, (ny + 1) // 2
+        out = np.zeros((2 * mx, my), dtype=np.complex128)
+        for kx in range(-(mx - 1), mx):
+            for ky in range(my):
+                acc = 0j
+                for px in range(-(mx - 1), mx):
+                    for py in range(-(my - 1), my):
+                        for qx in range(-(mx - 1), mx):
+                            for qy in range(-(my - 1), my):
+                                rx, ry = kx - px - qx, ky - py - qy
+                                if abs(rx) <= mx - 1 and abs(ry) <= my - 1:
+                                    acc += F[px + mx - 1, py + my - 1] * G[qx + mx - 1, qy + my - 1] * \
+                                        H[rx + mx - 1, ry + my - 1]
+                out[kx + mx, ky] = acc
         return out
 
 

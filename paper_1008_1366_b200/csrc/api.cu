@@ -73,6 +73,7 @@ size_t idc_workspace_bytes(idc_kind k, size_t m0, size_t m1, size_t m2, size_t b
     case IDC_HCONV2D: return idc::hconv2d_work_bytes(m0, m1);
     case IDC_CCONV3D: return idc::cconv3d_work_bytes(m0, m1, m2);
     case IDC_HCONV3D: return idc::hconv3d_work_bytes(m0, m1, m2);
+    case IDC_TCONV2D: return idc::tconv2d_work_bytes(m0, m1);
   }
   return 0;
 }
@@ -138,6 +139,20 @@ idc_status idc_hconv2d(idc_c128* f, idc_c128* g, size_t mx, size_t my, void* wor
   if (st != IDC_OK) return st;
   return from_cuda(idc::run_hconv2d(reinterpret_cast<double2*>(f), reinterpret_cast<double2*>(g), (int)mx, (int)my,
                                     reinterpret_cast<double2*>(work), (cudaStream_t)stream));
+}
+
+idc_status idc_tconv2d(idc_c128* f, idc_c128* g, idc_c128* h, size_t mx, size_t my, void* work,
+                       size_t work_bytes, idc_stream stream) {
+  if (mx == 0 || my == 0) return IDC_ERR_INVALID;
+  if (!size_ok(mx, 1, 2048) || !size_ok(my, 1, 4096)) return IDC_ERR_UNSUPPORTED;
+  size_t need = idc::tconv2d_work_bytes(mx, my);
+  if (need == 0) return IDC_ERR_UNSUPPORTED;
+  const void* arrs[] = {f, g, h};
+  idc_status st = check_arrays(arrs, 3, 2 * mx * my * sizeof(idc_c128), work, work_bytes, need);
+  if (st != IDC_OK) return st;
+  return from_cuda(idc::run_tconv2d(reinterpret_cast<double2*>(f), reinterpret_cast<double2*>(g),
+                                    reinterpret_cast<double2*>(h), (int)mx, (int)my, reinterpret_cast<double2*>(work),
+                                    (cudaStream_t)stream));
 }
 
 idc_status idc_cconv3d(idc_c128* f, idc_c128* g, size_t mx, size_t my, size_t mz, void* work, size_t work_bytes,

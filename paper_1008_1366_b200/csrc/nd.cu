@@ -163,6 +163,36 @@ cudaError_t run_hconv2d_dot(double2* f, double2* g, int npairs, int mx, int my, 
   return launch_pad0_fwd(f, U, mx, my, 1, 0, 0, s);                      // fft0padForward, pair 0
 }
 
+// Function tconv2: fft0tpadBackward along x on every column of
+// f, g, h (2mx rows, origin at row mx, row 0 = kx -mx = 0): with k' = k + mx,
+// u_{2l+r} = (-1)^l i^{-r} sum_{k'} zeta_{2mx}^{lk'} zeta_{4mx}^{rk'} U_{k'-mx}
+// (Eq. fft0tbackward): fftpadBackward of the 2mx-row column (K5, N = 2mx)
+// gives (-1)^l i^{r} u_{2l+r}; the odd stream is multiplied by i^{-1} so that
+// every row is (-1)^l u (real factor: the rows stay Hermitian in ky for the
+// 1D ternary row kernel K4).  The ternary product carries (-1)^{3l} =
+// (-1)^l, which is exactly the (-1)^l of Eq. fft0tforward, leaving
+// 4m U_k = sum_r zeta_{4m}^{-rk'} i^r fft(p_r)(k'): K6 with odd phase i.
+size_t tconv2d_work_bytes(size_t mx, size_t my) {
+  if (!pow2ok(mx) || !pow2ok(my) || mx > 2048 || my > 4096) return 0;
+  return 3 * 2 * mx * my * W16 + tconv_rows_work_bytes((int)my);
+}
+
+cudaError_t run_tconv2d(double2* f, double2* g, double2* h, int mx, int my, double2* work, cudaStream_t s) {
+  const long n = 2L * mx * my, N = 2L * mx;
+  double2* U = work;
+  double2* V = U + n;
+  double2* Wk = V + n;
+  double2* rw = Wk + n;
+  for (double2* a : {f, g, h}) IDC_TRY(cudaMemsetAsync(a, 0, (size_t)my * W16, s));   // row kx = -mx
+  const double2 mi = {0.0, -1.0}, pi = {0.0, 1.0};
+  IDC_TRY(launch_pad_bwd(f, g, U, V, (int)N, my, 1, 0, 0, s, mi));       // fft0tpadBackward: f, g
+  IDC_TRY(launch_pad_bwd(h, nullptr, Wk, nullptr, (int)N, my, 1, 0, 0, s, mi));   // and h
+  IDC_TRY(launch_tconv_rows(f, g, h, my, N, rw, s));                    // tconv on the r = 0 rows
+  IDC_TRY(launch_tconv_rows(U, V, Wk, my, N, rw, s));                   // tconv on the r = 1 rows
+  IDC_TRY(launch_pad_fwd(f, U, (int)N, my, 1, 0, 0, s, pi));            // fft0tpadForward
+  return cudaMemsetAsync(f, 0, (size_t)my * W16, s);                    // kx = -mx: outside the range
+}
+
 // Complex 2D dot product (Function cconv2 with sum_i f_i * g_i): K5 along x on
 // all 2*npairs arrays, K2d on the rows of both x-streams, K6 on pair 0.
 size_t cconv2d_dot_work_bytes(size_t npairs, size_t mx, size_t my) {

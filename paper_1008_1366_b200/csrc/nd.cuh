@@ -15,6 +15,8 @@ cudaError_t run_cconv2d(double2* f, double2* g, int mx, int my, long batch, doub
 cudaError_t run_hconv2d(double2* f, double2* g, int mx, int my, double2* work, cudaStream_t s);
 cudaError_t run_cconv3d(double2* f, double2* g, int mx, int my, int mz, double2* work, cudaStream_t s);
 size_t hconv2d_dot_work_bytes(size_t npairs, size_t mx, size_t my);
+size_t tconv2d_work_bytes(size_t mx, size_t my);
+cudaError_t run_tconv2d(double2* f, double2* g, double2* h, int mx, int my, double2* work, cudaStream_t s);
 size_t cconv2d_dot_work_bytes(size_t npairs, size_t mx, size_t my);
 cudaError_t run_cconv2d_dot(double2* f, double2* g, int npairs, int mx, int my, double2* work, cudaStream_t s);
 cudaError_t run_hconv2d_dot(double2* f, double2* g, int npairs, int mx, int my, double2* work, cudaStream_t s);

@@ -53,7 +53,7 @@ struct Pencil {
 template <int N, int E, int W>
 __global__ void __launch_bounds__(PCfg<N, E, W>::THREADS)
 k_pad_bwd(double2* __restrict__ f, double2* __restrict__ g, double2* __restrict__ U, double2* __restrict__ V,
-          Pencil pc, const double2* __restrict__ twN, const double2* __restrict__ tw2N) {
+          Pencil pc, const double2* __restrict__ twN, const double2* __restrict__ tw2N, double2 ophase) {
   using C = PCfg<N, E, W>;
   constexpr int T = C::T;
   extern __shared__ __align__(16) double2 smem[];
@@ -68,7 +68,7 @@ k_pad_bwd(double2* __restrict__ f, double2* __restrict__ g, double2* __restrict_
   for (int i = 0; i < E; ++i) x0[i] = ok ? a[(long)(t + T * i) * pc.ncols] : make_double2(0, 0);
   // odd stream u_{2l+1} = sum_k zeta_m^{lk} zeta_{2m}^k U_k  (Eq. cconv1backward)
 #pragma unroll
-  for (int i = 0; i < E; ++i) v[i] = cmul(x0[i], ldtw(&tw2N[t + T * i]));
+  for (int i = 0; i < E; ++i) v[i] = cmul(x0[i], cmul(ldtw(&tw2N[t + T * i]), ophase));
   fft<N, E, +1>(v, t, smem, twN, CtaSync{}, xs);
   if (ok) {
 #pragma unroll
@@ -86,7 +86,7 @@ k_pad_bwd(double2* __restrict__ f, double2* __restrict__ g, double2* __restrict_
 template <int N, int E, int W>
 __global__ void __launch_bounds__(PCfg<N, E, W>::THREADS)
 k_pad_fwd(double2* __restrict__ f, const double2* __restrict__ U, Pencil pc, const double2* __restrict__ twN,
-          const double2* __restrict__ tw2N) {
+          const double2* __restrict__ tw2N, double2 ophase) {
   using C = PCfg<N, E, W>;
   constexpr int T = C::T;
   extern __shared__ __align__(16) double2 smem[];
@@ -101,7 +101,7 @@ k_pad_fwd(double2* __restrict__ f, const double2* __restrict__ U, Pencil pc, con
   for (int i = 0; i < E; ++i) v[i] = ok ? u[(long)(t + T * i) * pc.ncols] : make_double2(0, 0);
   fft<N, E, -1>(v, t, smem, twN, CtaSync{}, xs);
 #pragma unroll
-  for (int i = 0; i < E; ++i) s[i] = cmulc(v[i], ldtw(&tw2N[t + T * i]));  // zeta_{2m}^{-k} U_k
+  for (int i = 0; i < E; ++i) s[i] = cmul(cmulc(v[i], ldtw(&tw2N[t + T * i])), ophase);  // c zeta_{2m}^{-k} U_k
 #pragma unroll
   for (int i = 0; i < E; ++i) v[i] = ok ? a[(long)(t + T * i) * pc.ncols] : make_double2(0, 0);
   fft<N, E, -1>(v, t, smem, twN, CtaSync{}, xs);
@@ -247,28 +247,28 @@ cudaError_t launchp(K kernel, int threads, size_t smem, dim3 grid, cudaStream_t 
 
 template <int N>
 cudaError_t pad_bwd_n(double2* f, double2* g, double2* U, double2* V, long ncols, long batch, long bstride,
-                      long ustride, cudaStream_t s) {
+                      long ustride, cudaStream_t s, double2 ophase) {
   constexpr int E = PTune<N>::E, W = PTune<N>::W;
   using C = PCfg<N, E, W>;
   const double2* twN = pass_table(N, PTune<N>::E);
   const double2* tw2N = zeta_table(2 * N);
   if (!twN || !tw2N) return cudaErrorMemoryAllocation;
   Pencil pc{ncols, bstride, ustride};
-  void* args[] = {&f, &g, &U, &V, &pc, &twN, &tw2N};
+  void* args[] = {&f, &g, &U, &V, &pc, &twN, &tw2N, &ophase};
   dim3 grid((unsigned)((ncols + W - 1) / W), (unsigned)batch, g ? 2 : 1);
   return launchp(k_pad_bwd<N, E, W>, C::THREADS, (size_t)C::XB * 16, grid, s, args);
 }
 
 template <int N>
 cudaError_t pad_fwd_n(double2* f, const double2* U, long ncols, long batch, long bstride, long ustride,
-                      cudaStream_t s) {
+                      cudaStream_t s, double2 ophase) {
   constexpr int E = PTune<N>::E, W = PTune<N>::W;
   using C = PCfg<N, E, W>;
   const double2* twN = pass_table(N, PTune<N>::E);
   const double2* tw2N = zeta_table(2 * N);
   if (!twN || !tw2N) return cudaErrorMemoryAllocation;
   Pencil pc{ncols, bstride, ustride};
-  void* args[] = {&f, &U, &pc, &twN, &tw2N};
+  void* args[] = {&f, &U, &pc, &twN, &tw2N, &ophase};
   dim3 grid((unsigned)((ncols + W - 1) / W), (unsigned)batch, 1);
   return launchp(k_pad_fwd<N, E, W>, C::THREADS, (size_t)C::XB * 16, grid, s, args);
 }
@@ -338,15 +338,15 @@ cudaError_t pad0_fwd_n(double2* f, const double2* U, long ncols, long batch, lon
     }
 
 cudaError_t launch_pad_bwd(double2* f, double2* g, double2* U, double2* V, int m, long ncols, long batch,
-                           long bstride, long ustride, cudaStream_t s) {
-  IDC_TDISPATCH(m, return pad_bwd_tma<NN>(f, g, U, V, ncols, batch, bstride, ustride, s));
-  IDC_PDISPATCH(m, return pad_bwd_n<NN>(f, g, U, V, ncols, batch, bstride, ustride, s));
+                           long bstride, long ustride, cudaStream_t s, double2 odd_phase) {
+  IDC_TDISPATCH(m, return pad_bwd_tma<NN>(f, g, U, V, ncols, batch, bstride, ustride, s, odd_phase));
+  IDC_PDISPATCH(m, return pad_bwd_n<NN>(f, g, U, V, ncols, batch, bstride, ustride, s, odd_phase));
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_pad_fwd(double2* f, const double2* U, int m, long ncols, long batch, long bstride, long ustride,
-                           cudaStream_t s) {
-  IDC_TDISPATCH(m, return pad_fwd_tma<NN>(f, U, ncols, batch, bstride, ustride, s));
-  IDC_PDISPATCH(m, return pad_fwd_n<NN>(f, U, ncols, batch, bstride, ustride, s));
+                           cudaStream_t s, double2 odd_phase) {
+  IDC_TDISPATCH(m, return pad_fwd_tma<NN>(f, U, ncols, batch, bstride, ustride, s, odd_phase));
+  IDC_PDISPATCH(m, return pad_fwd_n<NN>(f, U, ncols, batch, bstride, ustride, s, odd_phase));
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_pad0_bwd(double2* f, double2* g, double2* U, double2* V, int m, long ncols, long batch,

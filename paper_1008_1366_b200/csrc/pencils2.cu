@@ -82,7 +82,7 @@ template <int N>
 __global__ void __launch_bounds__(TCfg<N>::THREADS, IDC_PENCIL_MINB)
 k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mg, double2* __restrict__ f,
               double2* __restrict__ g, double2* __restrict__ U, double2* __restrict__ V, Tiles tl,
-              const double2* __restrict__ twN, const double2* __restrict__ tw2N) {
+              const double2* __restrict__ twN, const double2* __restrict__ tw2N, double2 ophase) {
   using C = TCfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   extern __shared__ __align__(128) double2 smem[];
@@ -127,7 +127,7 @@ k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
     }
     // odd stream u_{2l+1} = sum_k zeta_m^{lk} zeta_{2m}^k U_k  (Eq. cconv1backward)
     // zeta_{2m}^k, k = t + T i: zeta_{2m}^t x zeta_{2E}^i (immediate)
-    for_roots<2 * E, 1, +1, E>(ldtw(&tw2N[t]), [&](int i, double2 w) { v[i] = cmul(x0[i], w); });
+    for_roots<2 * E, 1, +1, E>(cmul(ldtw(&tw2N[t]), ophase), [&](int i, double2 w) { v[i] = cmul(x0[i], w); });
     fft<N, E, +1>(v, t, xb, twN, CtaSync{}, xs);
     const long rs = (long)T * tl.ncols;   // pointer step between a thread's rows
     if (ok) {
@@ -148,7 +148,7 @@ k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
 template <int N>
 __global__ void __launch_bounds__(TCfg<N>::THREADS, IDC_PENCIL_MINB)
 k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mu, double2* __restrict__ f,
-              Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw2N) {
+              Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw2N, double2 ophase) {
   using C = TCfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   extern __shared__ __align__(128) double2 smem[];
@@ -195,7 +195,7 @@ k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
       load_rows<W, BR>(&mu, su, c2, 0, N, item2, &bars[1]);
     }
     fft<N, E, -1>(v, t, xb, twN, CtaSync{}, xs);
-    for_roots<2 * E, 1, -1, E>(cconj(ldtw(&tw2N[t])), [&](int i, double2 w) { s[i] = cmul(v[i], w); });  // zeta_{2m}^{-k} U_k
+    for_roots<2 * E, 1, -1, E>(cconj(ldtw(&tw2N[t])), [&](int i, double2 w) { s[i] = cmul(cmul(v[i], w), ophase); });  // c zeta_{2m}^{-k} U_k
     mbar_wait(&bars[0], phase);
     phase ^= 1;
 #pragma unroll
@@ -455,7 +455,7 @@ Tiles make_tiles(long ncols, long batch, int inputs, long bstride, long ustride)
 
 template <int N>
 cudaError_t pad_bwd_tma(double2* f, double2* g, double2* U, double2* V, long ncols, long batch, long bstride,
-                        long ustride, cudaStream_t s) {
+                        long ustride, cudaStream_t s, double2 ophase) {
   using C = TCfg<N>;
   const double2* twN = pass_table(N, TCfg<N>::E);
   const double2* tw2N = zeta_table(2 * N);
@@ -464,14 +464,14 @@ cudaError_t pad_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nco
   if (!encode_pencil_map(&mf, f, ncols, N, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
   if (!encode_pencil_map(&mg, g ? g : f, ncols, N, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
   Tiles tl = make_tiles<N>(ncols, batch, g ? 2 : 1, bstride, ustride);
-  void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw2N};
+  void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw2N, &ophase};
   const size_t smem = ((size_t)N * C::W + C::XB) * 16 + 16;
   return launch_t(k_pad_bwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
 }
 
 template <int N>
 cudaError_t pad_fwd_tma(double2* f, const double2* U, long ncols, long batch, long bstride, long ustride,
-                        cudaStream_t s) {
+                        cudaStream_t s, double2 ophase) {
   using C = TCfg<N>;
   const double2* twN = pass_table(N, TCfg<N>::E);
   const double2* tw2N = zeta_table(2 * N);
@@ -480,7 +480,7 @@ cudaError_t pad_fwd_tma(double2* f, const double2* U, long ncols, long batch, lo
   if (!encode_pencil_map(&mf, f, ncols, N, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
   if (!encode_pencil_map(&mu, U, ncols, N, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
   Tiles tl = make_tiles<N>(ncols, batch, 1, bstride, ustride);
-  void* args[] = {&mf, &mu, &f, &tl, &twN, &tw2N};
+  void* args[] = {&mf, &mu, &f, &tl, &twN, &tw2N, &ophase};
   const size_t smem = (2 * (size_t)N * C::W + C::XB) * 16 + 32;
   return launch_t(k_pad_fwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
 }
@@ -520,8 +520,9 @@ cudaError_t pad0_fwd_tma(double2* f, const double2* U, long ncols, long batch, l
 }
 
 #define IDC_INST_T(N)                                                                                           \
-  template cudaError_t pad_bwd_tma<N>(double2*, double2*, double2*, double2*, long, long, long, long, cudaStream_t); \
-  template cudaError_t pad_fwd_tma<N>(double2*, const double2*, long, long, long, long, cudaStream_t);              \
+  template cudaError_t pad_bwd_tma<N>(double2*, double2*, double2*, double2*, long, long, long, long, cudaStream_t, \
+                                      double2);                                                                    \
+  template cudaError_t pad_fwd_tma<N>(double2*, const double2*, long, long, long, long, cudaStream_t, double2);     \
   template cudaError_t pad0_bwd_tma<N>(double2*, double2*, double2*, double2*, long, long, long, long,             \
                                        cudaStream_t);                                                            \
   template cudaError_t pad0_fwd_tma<N>(double2*, const double2*, long, long, long, long, cudaStream_t);

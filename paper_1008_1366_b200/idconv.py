@@ -23,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("IDCONV_LIB") or os.path.join(_HERE, "libidconv.so")
 
 OK, ERR_INVALID, ERR_UNSUPPORTED, ERR_WORKSPACE, ERR_CUDA, ERR_NCCL = range(6)
-CCONV1D, HCONV1D, TCONV1D, CCONV2D, HCONV2D, CCONV3D, HCONV3D = range(7)
+CCONV1D, HCONV1D, TCONV1D, CCONV2D, HCONV2D, CCONV3D, HCONV3D, TCONV2D = range(8)
 
 # name -> (argtypes, restype)
 _P, _S, _I, _U64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint64
@@ -39,6 +39,7 @@ SIGNATURES = {
     "idc_hconv2d": ([_P, _P, _S, _S, _P, _S, _P], _I),
     "idc_cconv3d": ([_P, _P, _S, _S, _S, _P, _S, _P], _I),
     "idc_hconv3d": ([_P, _P, _S, _S, _S, _P, _S, _P], _I),
+    "idc_tconv2d": ([_P, _P, _P, _S, _S, _P, _S, _P], _I),
     "idc_comm_init": ([ctypes.POINTER(ctypes.c_void_p), _I, _I, _P], _I),
     "idc_comm_destroy": ([_P], _I),
     "idc_comm_unique_id": ([_P], _I),
@@ -232,6 +233,16 @@ def cconv2d(f, g, work=None, stream=None):
     L = lib()
     return _run([f, g], CCONV2D, (mx, my, 1), B,
                 lambda p, w, wb, s: L.idc_cconv2d(p[0], p[1], mx, my, B, w, wb, s), work, stream)
+
+
+def tconv2d(f, g, h, work=None, stream=None):
+    """Function tconv2 on (2mx, my) arrays (row 0 = kx -mx, read as
+    zero); f rows 1..2mx-1 <- the centered Hermitian ternary convolution."""
+    nx, my = f.shape[-2], f.shape[-1]
+    mx = nx // 2
+    L = lib()
+    return _run([f, g, h], TCONV2D, (mx, my, 1), 1,
+                lambda p, w, wb, s: L.idc_tconv2d(p[0], p[1], p[2], mx, my, w, wb, s), work, stream)
 
 
 def hconv2d(f, g, work=None, stream=None):

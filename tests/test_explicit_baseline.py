@@ -41,3 +41,13 @@ def test_explicit_3d():
     assert rel_l2(ex.cconv3d(T(f), T(g)).numpy(), direct.cconv3d(f, g)) < 1e-14
     f, g = synthgen.hconv3d_inputs(4, 4, 4)
     assert rel_l2(ex.hconv3d(T(f), T(g)).numpy(), direct.hconv3d(f, g)) < 1e-14
+
+
+def test_explicit_tconv2d():
+    from oracle import ternary2d
+    mx, my = 4, 8
+    arrs = []
+    for r in range(3):
+        a = synthgen.hconv2d_inputs(mx, my, roles=(r,))[0]
+        arrs.append(np.concatenate([np.zeros((1, my), dtype=np.complex128), a], axis=0))
+    assert rel_l2(ex.tconv2d(*(T(a) for a in arrs)).numpy(), ternary2d.direct(*arrs)) < 1e-14

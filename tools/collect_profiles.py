@@ -15,7 +15,7 @@ src = os.path.join(ROOT, "gpurun_out")
 dst = os.path.join(ROOT, "profiles")
 os.makedirs(dst, exist_ok=True)
 
-for w in ["c2", "c1", "c3a", "c3b", "c4", "c4adv", "c5a", "c5b", "ref"]:
+for w in ["c2", "c1", "c3a", "c3b", "c4", "c4adv", "c4t", "c5a", "c5b", "ref"]:
     p = os.path.join(src, f"{tag}_bench_{w}.json")
     if os.path.exists(p):
         shutil.copy(p, os.path.join(dst, f"{tag}_bench_{w}.json"))

@@ -94,6 +94,25 @@ def hconv2d(f, g):
     return H[idx[0], :my]
 
 
+def tconv2d(f, g, h):
+    """2D centered Hermitian ternary (Function tconv2's problem): paper layout
+    (2mx, my), row 0 = kx -mx ignored; pad x to 4mx (centered), y to 4my
+    (Hermitian half), three c2r, product, r2c."""
+    nx, my = f.shape
+    mx = nx // 2
+    Nx, Ny = 4 * mx, 4 * my
+    u = None
+    for a in (f, g, h):
+        P, idx = _centered_pad(a[1:], (mx,), (Nx,), Ny)
+        x = F.irfft2(P, s=(Nx, Ny)) * (Nx * Ny)
+        del P
+        u = x if u is None else u * x
+    H = F.rfft2(u) / (Nx * Ny)
+    out = torch.zeros_like(f)
+    out[1:] = H[idx[0], :my]
+    return out
+
+
 def cconv3d(f, g):
     mx, my, mz = f.shape
     s = (2 * mx, 2 * my, 2 * mz)
@@ -124,6 +143,7 @@ CONFIGS = [  # (name, kind, shape, arrays) -- BASELINE.json configs
     ("c3a", "cconv2d", (1024, 1024), 2),
     ("c3b", "cconv2d", (64, 256, 256), 2),
     ("c4", "hconv2d", (4095, 2048), 2),
+    ("c4t", "tconv2d", (4096, 2048), 3),
     ("c5a", "cconv3d", (512, 512, 512), 2),
     ("c5b", "hconv3d", (1023, 1023, 512), 2),
 ]
@@ -155,8 +175,10 @@ def main():
         arrs = [torch.empty(shape, dtype=torch.complex128, device="cuda") for _ in range(narr)]
         for i, x in enumerate(arrs):
             idconv.fill_uniform(x, synthgen.array_id(i), synthgen.SEED)
+            if kind == "tconv2d":
+                x[0] = 0                                   # kx = -mx row
         explicit = {"cconv1d": cconv1d, "hconv1d": hconv1d, "tconv1d": tconv1d, "cconv2d": cconv2d,
-                    "hconv2d": hconv2d, "cconv3d": cconv3d, "hconv3d": hconv3d}[kind]
+                    "hconv2d": hconv2d, "tconv2d": tconv2d, "cconv3d": cconv3d, "hconv3d": hconv3d}[kind]
         if kind == "cconv2d" and len(shape) == 3:
             ex = lambda: explicit(arrs[0], arrs[1])    # batched over the leading axis
         else:
