@@ -283,6 +283,18 @@ IDC_API size_t idc_advection2d_workspace_bytes(size_t mx, size_t my);
 IDC_API idc_status idc_advection2d(const idc_c128* w, idc_c128* out, size_t mx, size_t my, void* work,
                                    size_t work_bytes, idc_stream stream);
 
+/* ---- general p/q implicit padding ------------------ */
+
+/* pm data modes implicitly zero padded to N = qm, decomposed as
+ * j = q l + r (q residues) and k = t m + s; each residue is one size-m
+ * transform.  idc_cconv1d_pq applies it to the complex convolution: rows of
+ * L = p*m modes (f, g: batch x L, row-major), f <- h_k = sum_{i<=k} f_i
+ * g_{k-i}, k < L (D1 at length L) -- e.g. p = 3, q = 7 convolves rows of
+ * 3*2^k modes.  Requires 1 <= p <= 3, 2p <= q <= 8 (alias free), m a power of
+ * two in [8, 2048].  g unspecified on return; no workspace. */
+IDC_API idc_status idc_cconv1d_pq(idc_c128* f, idc_c128* g, size_t p, size_t q, size_t m, size_t batch,
+                                  idc_stream stream);
+
 /* ---- synthetic inputs (not part of the method) -------------------------- */
 
 /* Fill n complex values with the counter-based splitmix64 generator of

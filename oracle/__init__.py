@@ -433,6 +433,39 @@ class implicit:
         ge, go = implicit.fftpad_backward(g)
         return implicit.fftpad_forward(fe * ge, fo * go)
 
+    # ---- general p/q padding
+    @staticmethod
+    def fftpad_pq_backward(U, p, q):
+        """pm modes U (..., pm) implicitly padded to qm: returns dict r -> stream
+        u_{q l + r}, l < m, u_{ql+r} = sum_s zeta_m^{ls} sum_{t<p} zeta_{qm}^{r(tm+s)} U_{tm+s}."""
+        U = _c(U)
+        m = U.shape[-1] // p
+        Wm = _dftm(m, +1)
+        s = np.arange(m)
+        out = {}
+        for r in range(q):
+            w = sum(zeta(q * m, r * (t * m + s)) * U[..., t * m:(t + 1) * m] for t in range(p))
+            out[r] = w @ Wm.T
+        return out
+
+    @staticmethod
+    def fftpad_pq_forward(streams, p, q, m):
+        """qm U_k = sum_{r<q} zeta_{qm}^{-rk} sum_l zeta_m^{-kl} u_{ql+r}, k < pm; returns U."""
+        k = np.arange(p * m)
+        Wk = dft_matrix(m, k, range(m), -1)
+        out = 0
+        for r in range(q):
+            out = out + zeta(q * m, -r * k) * (streams[r] @ Wk.T)
+        return out / (q * m)
+
+    @staticmethod
+    def cconv1d_pq(f, g, p, q):
+        """Complex convolution with p/q implicit padding: products of the q residue streams."""
+        m = f.shape[-1] // p
+        sf = implicit.fftpad_pq_backward(f, p, q)
+        sg = implicit.fftpad_pq_backward(g, p, q)
+        return implicit.fftpad_pq_forward({r: sf[r] * sg[r] for r in range(q)}, p, q, m)
+
     # ---- centered 2/3 rule, Eqs. fft0backwardA/B, fft0forward (P:425-443)
     @staticmethod
     def fft0pad_backward(A):

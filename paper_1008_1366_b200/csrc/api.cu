@@ -283,4 +283,16 @@ idc_status idc_advection2d(const idc_c128* w, idc_c128* out, size_t mx, size_t m
   return from_cuda(cudaMemcpyAsync(out, F, n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
 }
 
+// ---- general p/q implicit padding (NEXT-3) --------------------
+
+idc_status idc_cconv1d_pq(idc_c128* f, idc_c128* g, size_t p, size_t q, size_t m, size_t batch, idc_stream stream) {
+  if (m == 0 || batch == 0 || p == 0 || q == 0) return IDC_ERR_INVALID;
+  if (p > 3 || q > 8 || q < 2 * p || !size_ok(m, 8, 2048)) return IDC_ERR_UNSUPPORTED;
+  const void* arrs[] = {f, g};
+  idc_status st = check_arrays(arrs, 2, p * m * batch * sizeof(idc_c128), nullptr, 0, 0);
+  if (st != IDC_OK) return st;
+  return from_cuda(idc::launch_cconv_pq_rows(reinterpret_cast<double2*>(f), reinterpret_cast<double2*>(g), (int)p,
+                                             (int)q, (int)m, (long)batch, (cudaStream_t)stream));
+}
+
 }  // extern "C"

@@ -40,6 +40,8 @@ cudaError_t launch_cconv_dot_rows(double2* f, const double2* g, int npairs, long
                                   cudaStream_t s);
 cudaError_t launch_tconv_dot_rows(double2* f, const double2* g, const double2* h, int npairs, long istride, int m,
                                   long nrows, cudaStream_t s);
+// K2pq (rows_dot.cu): complex rows of p*m modes implicitly padded to q*m.
+cudaError_t launch_cconv_pq_rows(double2* f, const double2* g, int p, int q, int m, long nrows, cudaStream_t s);
 // Hermitian projection of the ky = 0 lines of batch (2mx-1) x my arrays.
 cudaError_t launch_enforce_symmetry_2d(double2* a, int mx, int my, long batch, cudaStream_t s);
 // The four M = 2 inputs of the 2D Euler advective term from w.

@@ -333,6 +333,86 @@ k_tconv_dot_rows(double2* __restrict__ f, const double2* __restrict__ g, const d
   }
 }
 
+// ===================================================================== K2pq ==
+// General p/q implicit padding: rows of
+// L = pm complex modes, implicitly zero padded to N = qm (q >= 2p: the linear
+// convolution of the first pm terms is alias free).  j = q l + r, k = t m + s:
+//   u_{ql+r} = sum_s zeta_m^{ls} sum_{t<p} zeta_{qm}^{r(tm+s)} U_{tm+s}
+// -- q transforms of size m per input -- and the forward
+//   qm U_k = sum_{r<q} zeta_{qm}^{-rk} sum_l zeta_m^{-kl} u_{ql+r},  k < pm.
+// Per residue r the two inputs' streams are transformed in lockstep, their
+// product forward transformed, and its contribution zeta_{qm}^{-rk} F_r(k mod
+// m) added to the p output accumulators (registers) of the row.
+template <int M, int P>
+__global__ void __launch_bounds__(D2Cfg<M>::THREADS, 1)
+k_cconv_pq_rows(double2* __restrict__ f, const double2* __restrict__ g, int q, long nrows,
+                const double2* __restrict__ twM, const double2* __restrict__ twqM) {
+  using C = D2Cfg<M>;
+  constexpr int E = C::E, T = C::T, G = C::G;
+  extern __shared__ __align__(16) double2 smem[];
+  const int grp = threadIdx.x / T, t = threadIdx.x - grp * T;
+  double2* xb = smem + grp * 2 * C::XB;
+  double2* xb2 = xb + C::XB;
+  const auto sync = d2sync<M>(grp);
+  const long L = (long)P * M;
+  const double inv = 1.0 / ((double)q * M);
+  for (long row0 = (long)blockIdx.x * G; row0 < nrows; row0 += (long)gridDim.x * G) {
+    const long row = row0 + grp;
+    if constexpr (C::NAMED) {
+      if (row >= nrows) break;
+    }
+    const bool ok = row < nrows;
+    const double2* fr = f + (ok ? row : 0) * L;
+    const double2* gr = g + (ok ? row : 0) * L;
+    double2 acc[P][E], x[E], y[E];
+#pragma unroll
+    for (int tt = 0; tt < P; ++tt)
+#pragma unroll
+      for (int i = 0; i < E; ++i) acc[tt][i] = make_double2(0.0, 0.0);
+    const int qm = q * M;
+    // index of zeta_{qm}^{r(tm+s)} in the qm-entry table: (rt mod q) m + rs < 2qm
+    auto zidx = [&](int r, int tt, int s) {
+      const int j = ((r * tt) % q) * M + r * s;
+      return j >= qm ? j - qm : j;
+    };
+#pragma unroll 1
+    for (int r = 0; r < q; ++r) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int s = t + T * i;
+        double2 xs = make_double2(0.0, 0.0), ys = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int tt = 0; tt < P; ++tt) {
+          const int k = tt * M + s;
+          const double2 z = ldtw(&twqM[zidx(r, tt, s)]);              // zeta_{qm}^{r(tm+s)}
+          xs = cadd(xs, cmul(z, ldv(&fr[k])));
+          ys = cadd(ys, cmul(z, ldv(&gr[k])));
+        }
+        x[i] = xs;
+        y[i] = ys;
+      }
+      fft2<M, E, +1>(x, y, t, xb, xb2, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) x[i] = cmul(x[i], y[i]);
+      fft<M, E, -1>(x, t, xb, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int s = t + T * i;
+#pragma unroll
+        for (int tt = 0; tt < P; ++tt)
+          acc[tt][i] = cadd(acc[tt][i], cmulc(x[i], ldtw(&twqM[zidx(r, tt, s)])));   // zeta_{qm}^{-rk}
+      }
+    }
+    if (ok) {
+      double2* fw = f + row * L;
+#pragma unroll
+      for (int tt = 0; tt < P; ++tt)
+#pragma unroll
+        for (int i = 0; i < E; ++i) fw[(long)tt * M + t + T * i] = cscale(acc[tt][i], inv);
+    }
+  }
+}
+
 // ------------------------------------------------------- 2D helpers ------
 // Hermitian projection of the stored ky = 0 line of a (2mx-1) x my centered
 // array (AMB-7; "automatically enforce Hermitian symmetry"):
@@ -485,6 +565,48 @@ cudaError_t launch_tconv_dot_rows(double2* f, const double2* g, const double2* h
     case 4096: return IDC_CALL(4096);
   }
 #undef IDC_CALL
+  return cudaErrorInvalidValue;
+}
+
+template <int M, int P>
+cudaError_t cconv_pq_rows(double2* f, const double2* g, int q, long nrows, cudaStream_t s) {
+  using C = D2Cfg<M>;
+  const double2* twM = pass_table(M, C::E);
+  const double2* twqM = zeta_table(q * M);
+  if (!twM || !twqM) return cudaErrorMemoryAllocation;
+  const size_t smem = (size_t)C::G * 2 * C::XB * 16;
+  cudaError_t e = cudaFuncSetAttribute(k_cconv_pq_rows<M, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  long need = (nrows + C::G - 1) / C::G, grid = num_sms();
+  if (need < grid) grid = need;
+  if (grid < 1) grid = 1;
+  void* args[] = {&f, &g, &q, &nrows, &twM, &twqM};
+  count_launch();
+  return cudaLaunchKernel((const void*)k_cconv_pq_rows<M, P>, dim3((unsigned)grid), dim3(C::THREADS), args, smem, s);
+}
+
+template <int P>
+cudaError_t cconv_pq_dispatch(double2* f, const double2* g, int q, int m, long nrows, cudaStream_t s) {
+  switch (m) {
+    case 8: return cconv_pq_rows<8, P>(f, g, q, nrows, s);
+    case 16: return cconv_pq_rows<16, P>(f, g, q, nrows, s);
+    case 32: return cconv_pq_rows<32, P>(f, g, q, nrows, s);
+    case 64: return cconv_pq_rows<64, P>(f, g, q, nrows, s);
+    case 128: return cconv_pq_rows<128, P>(f, g, q, nrows, s);
+    case 256: return cconv_pq_rows<256, P>(f, g, q, nrows, s);
+    case 512: return cconv_pq_rows<512, P>(f, g, q, nrows, s);
+    case 1024: return cconv_pq_rows<1024, P>(f, g, q, nrows, s);
+    case 2048: return cconv_pq_rows<2048, P>(f, g, q, nrows, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_cconv_pq_rows(double2* f, const double2* g, int p, int q, int m, long nrows, cudaStream_t s) {
+  switch (p) {
+    case 1: return cconv_pq_dispatch<1>(f, g, q, m, nrows, s);
+    case 2: return cconv_pq_dispatch<2>(f, g, q, m, nrows, s);
+    case 3: return cconv_pq_dispatch<3>(f, g, q, m, nrows, s);
+  }
   return cudaErrorInvalidValue;
 }
 

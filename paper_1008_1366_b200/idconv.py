@@ -59,6 +59,7 @@ SIGNATURES = {
     "idc_cconv1d_dot": ([_P, _P, _S, _S, _S, _P], _I),
     "idc_tconv1d_dot": ([_P, _P, _P, _S, _S, _S, _P], _I),
     "idc_cconv2d_dot": ([_P, _P, _S, _S, _S, _P, _S, _P], _I),
+    "idc_cconv1d_pq": ([_P, _P, _S, _S, _S, _S, _P], _I),
     "idc_enforce_symmetry_2d": ([_P, _S, _S, _S, _P], _I),
     "idc_advection2d_workspace_bytes": ([_S, _S], _S),
     "idc_advection2d": ([_P, _P, _S, _S, _P, _S, _P], _I),
@@ -338,6 +339,19 @@ def cconv2d_dot(f, g, work=None, stream=None):
     _check(lib().idc_cconv2d_dot(ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(g.data_ptr()), M, mx, my,
                                  ctypes.c_void_p(w.data_ptr()), wb, _stream_ptr(stream, f.device)), "idc_cconv2d_dot")
     return f[0]
+
+
+def cconv1d_pq(f, g, p: int, q: int, stream=None):
+    """Complex convolution of rows of L = p*m modes with implicit p/q padding
+    (P:693-716): f, g (batch, L) or (L,) CUDA tensors; f <- result."""
+    _need_cuda([f, g])
+    L = f.shape[-1]
+    if L % p:
+        raise ValueError("row length must be a multiple of p")
+    B = f.numel() // L
+    _check(lib().idc_cconv1d_pq(ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(g.data_ptr()), p, q, L // p, B,
+                                _stream_ptr(stream, f.device)), "idc_cconv1d_pq")
+    return f
 
 
 def hconv2d_dot(f, g, work=None, stream=None):
