@@ -464,4 +464,28 @@ cudaError_t launch_tconv_rows(double2* f, double2* g, double2* h, int m, long nr
   return cudaErrorInvalidValue;
 }
 
+// Both residue-stream row sets of an outer transform in one launch where the
+// kernel supports it (K2 rows2, K3 rows3), two launches otherwise.
+cudaError_t launch_cconv_rows_sets(double2* f, double2* g, long n0, double2* f1, double2* g1, long n1, int m,
+                                   double2* work, cudaStream_t s) {
+  RowSets rs{f1, g1, n0};
+  if (m <= IDC_V2_MAX_M) { IDC_DISPATCH_M(m, return cconv_rows2<MM>(f, g, n0 + n1, s, rs)); }
+  cudaError_t e = launch_cconv_rows(f, g, m, n0, work, s);
+  return e != cudaSuccess ? e : launch_cconv_rows(f1, g1, m, n1, work, s);
+}
+cudaError_t launch_hconv_rows_sets(double2* f, double2* g, long n0, double2* f1, double2* g1, long n1, int m,
+                                   double2* work, cudaStream_t s) {
+  RowSets rs{f1, g1, n0};
+  if (m >= IDC_V3_MIN_M && m <= 4096) {
+    switch (m) {
+      case 512: return hconv_rows3<512>(f, g, n0 + n1, s, rs);
+      case 1024: return hconv_rows3<1024>(f, g, n0 + n1, s, rs);
+      case 2048: return hconv_rows3<2048>(f, g, n0 + n1, s, rs);
+      case 4096: return hconv_rows3<4096>(f, g, n0 + n1, s, rs);
+    }
+  }
+  cudaError_t e = launch_hconv_rows(f, g, m, n0, work, s);
+  return e != cudaSuccess ? e : launch_hconv_rows(f1, g1, m, n1, work, s);
+}
+
 }  // namespace idc

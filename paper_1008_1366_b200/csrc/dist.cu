@@ -152,13 +152,13 @@ cudaError_t phase_b(const Plan& p, const RankBufs& b, double2* roww, cudaStream_
   const long cols = p.nres * p.mz;
   if (p.herm) {
     TRYC(launch_pad0_bwd(b.recvF, b.recvG, b.sendF, b.sendG, (int)p.mx, cols, 1, 0, 0, s));
-    TRYC(launch_hconv_rows(b.recvF, b.recvG, (int)p.mz, p.nxg * p.nres, roww, s));
-    TRYC(launch_hconv_rows(b.sendF, b.sendG, (int)p.mz, (p.mx + 1) * p.nres, roww, s));
+    TRYC(idc::launch_hconv_rows_sets(b.recvF, b.recvG, p.nxg * p.nres, b.sendF, b.sendG, (p.mx + 1) * p.nres,
+                                     (int)p.mz, roww, s));
     return launch_pad0_fwd(b.recvF, b.sendF, (int)p.mx, cols, 1, 0, 0, s);
   }
   TRYC(launch_pad_bwd(b.recvF, b.recvG, b.sendF, b.sendG, (int)p.mx, cols, 1, 0, 0, s));
-  TRYC(launch_cconv_rows(b.recvF, b.recvG, (int)p.mz, p.mx * p.nres, roww, s));
-  TRYC(launch_cconv_rows(b.sendF, b.sendG, (int)p.mz, p.mx * p.nres, roww, s));
+  TRYC(idc::launch_cconv_rows_sets(b.recvF, b.recvG, p.mx * p.nres, b.sendF, b.sendG, p.mx * p.nres, (int)p.mz,
+                                   roww, s));
   return launch_pad_fwd(b.recvF, b.sendF, (int)p.mx, cols, 1, 0, 0, s);
 }
 

@@ -22,13 +22,30 @@ cudaError_t launch_hconv_rows(double2* f, double2* g, int m, long nrows, double2
 cudaError_t launch_tconv_rows(double2* f, double2* g, double2* h, int m, long nrows, double2* work,
                               cudaStream_t s);
 
+// Two row sets in one launch: rows [0, n0) are rows of (f, g), rows
+// [n0, nrows) are rows of (f1, g1) -- the two residue streams of an outer
+// implicit transform (Functions cconv2 / conv2 run cconv / conv on both),
+// one launch instead of two (better wave balance, one fewer launch).
+struct RowSets {
+  double2* f1 = nullptr;
+  double2* g1 = nullptr;
+  long n0 = -1;       // < 0: one set
+};
+__host__ __device__ inline double2* row_ptr(double2* a0, double2* a1, long n0, long row, int m) {
+  return (n0 < 0 || row < n0) ? a0 + row * (long)m : a1 + (row - n0) * (long)m;
+}
+cudaError_t launch_cconv_rows_sets(double2* f, double2* g, long n0, double2* f1, double2* g1, long n1, int m,
+                                   double2* work, cudaStream_t s);
+cudaError_t launch_hconv_rows_sets(double2* f, double2* g, long n0, double2* f1, double2* g1, long n1, int m,
+                                   double2* work, cudaStream_t s);
+
 // Register-resident variants (rows2.cu), m <= 4096.
-template <int M> cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s);
+template <int M> cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s, RowSets rs = {});
 template <int M> cudaError_t hconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s);
 template <int M> cudaError_t tconv_rows2(double2* f, double2* g, double2* h, long nrows, cudaStream_t s);
 
 // TMA-staged Hermitian / ternary variants (rows3.cu), 512 <= m <= 4096.
-template <int M> cudaError_t hconv_rows3(double2* f, double2* g, long nrows, cudaStream_t s);
+template <int M> cudaError_t hconv_rows3(double2* f, double2* g, long nrows, cudaStream_t s, RowSets rs = {});
 template <int M> cudaError_t tconv_rows3(double2* f, double2* g, double2* h, long nrows, cudaStream_t s);
 
 // K3d (rows_dot.cu): centered Hermitian dot-product convolution of npairs

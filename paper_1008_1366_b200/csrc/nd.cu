@@ -129,8 +129,7 @@ cudaError_t run_cconv2d(double2* f, double2* g, int mx, int my, long batch, doub
   double2* V = work + batch * n;
   double2* rw = V + batch * n;
   IDC_TRY(launch_pad_bwd(f, g, U, V, mx, my, batch, n, n, s));            // fftpadBackward on columns
-  IDC_TRY(launch_cconv_rows(f, g, my, batch * mx, rw, s));                // cconv on rows of stream 0
-  IDC_TRY(launch_cconv_rows(U, V, my, batch * mx, rw, s));                // cconv on rows of stream 1
+  IDC_TRY(launch_cconv_rows_sets(f, g, batch * mx, U, V, batch * mx, my, rw, s));   // cconv on rows of both streams
   return launch_pad_fwd(f, U, mx, my, batch, n, n, s);                    // fftpadForward on columns
 }
 
@@ -139,8 +138,7 @@ cudaError_t run_hconv2d(double2* f, double2* g, int mx, int my, double2* work, c
   double2* V = work + (long)(mx + 1) * my;
   double2* rw = V + (long)(mx + 1) * my;
   IDC_TRY(launch_pad0_bwd(f, g, U, V, mx, my, 1, 0, 0, s));               // fft0padBackward on columns
-  IDC_TRY(launch_hconv_rows(f, g, my, 2L * mx - 1, rw, s));               // conv on rows i = 0..2mx-2
-  IDC_TRY(launch_hconv_rows(U, V, my, (long)mx + 1, rw, s));              // conv on rows i = 0..mx
+  IDC_TRY(launch_hconv_rows_sets(f, g, 2L * mx - 1, U, V, (long)mx + 1, my, rw, s));   // conv on the 3mx stream rows
   return launch_pad0_fwd(f, U, mx, my, 1, 0, 0, s);                       // fft0padForward on columns
 }
 
@@ -236,8 +234,7 @@ cudaError_t run_cconv3d(double2* f, double2* g, int mx, int my, int mz, double2*
       double2* b = B + s0 * slab;
       // cconv2 on the group's slabs, reusing this stream's U2/V2
       IDC_TRY(launch_pad_bwd(a, b, U2, V2, my, mz, gs, slab, slab, st));
-      IDC_TRY(launch_cconv_rows(a, b, mz, gs * my, rw, st));
-      IDC_TRY(launch_cconv_rows(U2, V2, mz, gs * my, rw, st));
+      IDC_TRY(launch_cconv_rows_sets(a, b, gs * my, U2, V2, gs * my, mz, rw, st));
       IDC_TRY(launch_pad_fwd(a, U2, my, mz, gs, slab, slab, st));
     }
   }
@@ -275,8 +272,7 @@ cudaError_t run_hconv3d(double2* f, double2* g, int mx, int my, int mz, double2*
       double2* b = B + s0 * slab;
       // conv2 on the group's slabs, reusing this stream's U2/V2
       IDC_TRY(launch_pad0_bwd(a, b, U2, V2, my, mz, gs, slab, uslab, st));
-      IDC_TRY(launch_hconv_rows(a, b, mz, gs * (2L * my - 1), rw, st));
-      IDC_TRY(launch_hconv_rows(U2, V2, mz, gs * ((long)my + 1), rw, st));
+      IDC_TRY(launch_hconv_rows_sets(a, b, gs * (2L * my - 1), U2, V2, gs * ((long)my + 1), mz, rw, st));
       IDC_TRY(launch_pad0_fwd(a, U2, my, mz, gs, slab, uslab, st));
     }
   }

@@ -67,7 +67,7 @@ __device__ __forceinline__ double2 herm_pair2(double2 fk, double2 gk, double2 fm
 template <int M, int E, int G>
 __global__ void __launch_bounds__(Cfg2<M, E, G>::THREADS, Cfg2<M, E, G>::MINB)
 k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, const double2* __restrict__ twM,
-              const double2* __restrict__ tw2M) {
+              const double2* __restrict__ tw2M, RowSets rs) {
   using C = Cfg2<M, E, G>;
   constexpr int T = C::T;
   extern __shared__ __align__(16) double2 smem[];
@@ -83,13 +83,13 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
       if (row >= nrows) break;
     }
     const bool ok = row < nrows;
-    const double2* fr = f + (ok ? row : 0) * (long)M;
-    const double2* gr = g + (ok ? row : 0) * (long)M;
+    double2* fr = row_ptr(f, rs.f1, rs.n0, ok ? row : 0, M);
+    const double2* gr = row_ptr(g, rs.g1, rs.n0, ok ? row : 0, M);
     // the next rows of this group: bulk prefetch into L2 (hides the HBM
     // latency of the first loads of the next iteration)
     if (IDC_ROWS_PREFETCH && t == 0 && row + (long)gridDim.x * G < nrows) {
-      prefetch_l2(f + (row + (long)gridDim.x * G) * (long)M, M * 16u);
-      prefetch_l2(g + (row + (long)gridDim.x * G) * (long)M, M * 16u);
+      prefetch_l2(row_ptr(f, rs.f1, rs.n0, row + (long)gridDim.x * G, M), M * 16u);
+      prefetch_l2(row_ptr(g, rs.g1, rs.n0, row + (long)gridDim.x * G, M), M * 16u);
     }
     // Every intermediate in registers (at most three E-vectors live): no
     // shared-memory stash traffic, only the FFT exchanges.  With E = 8 the
@@ -135,7 +135,7 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
     }
     // recombination and 1/(2m)
     if (ok) {
-      double2* fw = f + row * (long)M;
+      double2* fw = fr;
       for_roots<2 * E, 1, -1, E>(cconj(zt), [&](int i, double2 w) {       // zeta_{2m}^{-k}
         fw[t + T * i] = cscale(cadd(x[i], cmul(y[i], w)), inv);
       });
@@ -349,13 +349,13 @@ struct Tune {
 }  // namespace
 
 template <int M>
-cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s) {
+cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s, RowSets rs) {
   constexpr int E = Tune<M>::E, G = Tune<M>::G;
   using C = Cfg2<M, E, G>;
   const double2* twM = pass_table(M, Tune<M>::E);
   const double2* tw2M = zeta_table(2 * M);
   if (!twM || !tw2M) return cudaErrorMemoryAllocation;
-  void* args[] = {&f, &g, &nrows, &twM, &tw2M};
+  void* args[] = {&f, &g, &nrows, &twM, &tw2M, &rs};
   const size_t per = (E <= 8 ? 2 : 1) * C::XB;   // exchange buffer(s) only (intermediates in registers)
   return launch2(k_cconv_rows2<M, E, G>, C::THREADS, (size_t)G * per * 16, nrows, G, s, args);
 }
@@ -384,7 +384,7 @@ cudaError_t tconv_rows2(double2* f, double2* g, double2* h, long nrows, cudaStre
 }
 
 #define IDC_INST2(M)                                                                        \
-  template cudaError_t cconv_rows2<M>(double2*, double2*, long, cudaStream_t);              \
+  template cudaError_t cconv_rows2<M>(double2*, double2*, long, cudaStream_t, RowSets);     \
   template cudaError_t hconv_rows2<M>(double2*, double2*, long, cudaStream_t);              \
   template cudaError_t tconv_rows2<M>(double2*, double2*, double2*, long, cudaStream_t);
 IDC_INST2(1)

@@ -68,8 +68,8 @@ __device__ __forceinline__ double2 zpair(const double2* F, const double2* Gs, in
 // ====================================================================== K3 ==
 template <int M>
 __global__ void __launch_bounds__(Cfg3<M>::THREADS, 1)
-k_hconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, long nrows, const double2* __restrict__ twM,
-              const double2* __restrict__ tw3M) {
+k_hconv_rows3(double2* __restrict__ f, double2* __restrict__ g, long nrows, const double2* __restrict__ twM,
+              const double2* __restrict__ tw3M, RowSets rs) {
   using C = Cfg3<M>;
   constexpr int E = C::E, T = C::T, G = C::G;
   extern __shared__ __align__(128) double2 smem[];
@@ -88,8 +88,8 @@ k_hconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, long nrows
   __syncthreads();
   if (t == 0 && row < nrows) {
     mbar_arrive_expect_tx(bar, 2u * M * 16u);
-    tma_load_1d(F, f + row * (long)M, M * 16u, bar);
-    tma_load_1d(Gs, g + row * (long)M, M * 16u, bar);
+    tma_load_1d(F, row_ptr(f, rs.f1, rs.n0, row, M), M * 16u, bar);
+    tma_load_1d(Gs, row_ptr(g, rs.g1, rs.n0, row, M), M * 16u, bar);
   }
   const double inv = 1.0 / (3.0 * M);
   const double s3 = 0.86602540378443864676372317075294;  // sqrt(3)/2
@@ -131,8 +131,8 @@ k_hconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, long nrows
     sync();
     if (t == 0 && row + stride < nrows) {
       mbar_arrive_expect_tx(bar, 2u * M * 16u);
-      tma_load_1d(F, f + (row + stride) * (long)M, M * 16u, bar);
-      tma_load_1d(Gs, g + (row + stride) * (long)M, M * 16u, bar);
+      tma_load_1d(F, row_ptr(f, rs.f1, rs.n0, row + stride, M), M * 16u, bar);
+      tma_load_1d(Gs, row_ptr(g, rs.g1, rs.n0, row + stride, M), M * 16u, bar);
     }
     fft<M, E, +1>(v, t, xb, twM, sync);
 #pragma unroll
@@ -142,7 +142,7 @@ k_hconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, long nrows
 #pragma unroll
     for (int i = 0; i < E; ++i) xb[t + T * i] = Q[i];
     sync();
-    double2* fw = f + row * (long)M;
+    double2* fw = row_ptr(f, rs.f1, rs.n0, row, M);
     auto recombine = [&](int i, double2 tz) {
       const int k = t + T * i;
       const double2 a = Q[i], b = cconj(xb[(M - k) & (M - 1)]);
@@ -302,12 +302,12 @@ cudaError_t launch3(K kernel, int threads, size_t smem, long nrows, int groups, 
 }  // namespace
 
 template <int M>
-cudaError_t hconv_rows3(double2* f, double2* g, long nrows, cudaStream_t s) {
+cudaError_t hconv_rows3(double2* f, double2* g, long nrows, cudaStream_t s, RowSets rs) {
   using C = Cfg3<M>;
   const double2* twM = pass_table(M, Cfg3<M>::E);
   const double2* tw3M = zeta_table(3 * M);
   if (!twM || !tw3M) return cudaErrorMemoryAllocation;
-  void* args[] = {&f, &g, &nrows, &twM, &tw3M};
+  void* args[] = {&f, &g, &nrows, &twM, &tw3M, &rs};
   return launch3(k_hconv_rows3<M>, C::THREADS, C::SMEM, nrows, C::G, s, args);
 }
 
@@ -322,7 +322,7 @@ cudaError_t tconv_rows3(double2* f, double2* g, double2* h, long nrows, cudaStre
 }
 
 #define IDC_INST3(M)                                                                        \
-  template cudaError_t hconv_rows3<M>(double2*, double2*, long, cudaStream_t);              \
+  template cudaError_t hconv_rows3<M>(double2*, double2*, long, cudaStream_t, RowSets);     \
   template cudaError_t tconv_rows3<M>(double2*, double2*, double2*, long, cudaStream_t);
 IDC_INST3(512)
 IDC_INST3(1024)
