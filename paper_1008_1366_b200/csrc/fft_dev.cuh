@@ -265,50 +265,63 @@ __host__ __device__ constexpr int pass_tab_offset(int ns_target) {
 }
 
 // One Stockham radix-R pass; twiddles then DFT_R, data stays in registers.
+// Twiddles of one Stockham pass for this thread: for each of its B = E/R
+// butterflies, w^c (c < Q) and w^{Qa} (a < R/Q), w = exp(2 pi i jm/(NS R)),
+// from the pass table.  Loaded ahead of the exchange that precedes the pass,
+// so the load latency is hidden behind the barriers.
+template <int N, int E, int R, int NS>
+struct PassTw {
+  static constexpr int B = E / R, Q = pass_q(R);
+  double2 lo[B][Q], hi[B][R / Q];
+};
+template <int N, int E, int R, int NS>
+__device__ __forceinline__ PassTw<N, E, R, NS> load_pass_tw(int t, const double2* __restrict__ tw) {
+  PassTw<N, E, R, NS> p;
+  if constexpr (NS > 1) {
+    constexpr int T = N / E, B = E / R, Q = pass_q(R);
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int jm = (t + T * b) & (NS - 1);
+      const double2* tp = tw + pass_tab_offset<N, E>(NS) + jm;
+#pragma unroll
+      for (int c = 1; c < Q; ++c) p.lo[b][c] = ldtw_pass(&tp[(c - 1) * NS]);
+#pragma unroll
+      for (int a = 1; a < R / Q; ++a) p.hi[b][a] = ldtw_pass(&tp[(Q - 2 + a) * NS]);
+    }
+  }
+  return p;
+}
+
+// One Stockham radix-R pass with preloaded twiddles; data stays in registers.
 template <int N, int E, int R, int NS, int SIGN>
-__device__ __forceinline__ void pass_compute(double2 (&v)[E], int t, const double2* __restrict__ tw) {
-  constexpr int T = N / E, B = E / R;
+__device__ __forceinline__ void pass_compute(double2 (&v)[E], const PassTw<N, E, R, NS>& pt) {
+  constexpr int B = E / R;
 #pragma unroll
   for (int b = 0; b < B; ++b) {
     double2 x[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r] = v[b + r * B];
     if constexpr (NS > 1) {
-      // w^r, w = exp(2 pi i jm/(NS R)), r = Q a + c: load w^c (c < Q) and
-      // w^{Qa} (a < R/Q) from the pass table
-      const int jm = (t + T * b) & (NS - 1);
-      {
-      constexpr int Q = pass_q(R);
-      const double2* tp = tw + pass_tab_offset<N, E>(NS) + jm;
-      double2 lo[Q], hi[R / Q];
-#pragma unroll
-      for (int c = 1; c < Q; ++c) lo[c] = ldtw_pass(&tp[(c - 1) * NS]);
-#pragma unroll
-      for (int a = 1; a < R / Q; ++a) hi[a] = ldtw_pass(&tp[(Q - 2 + a) * NS]);
-#ifndef IDC_PASS_TW_PRODUCT
       // x[Qa + c] * w^c * w^{Qa}: two multiplies per element instead of
       // forming every w^r = w^{Qa} w^c first (same multiply count, but no
       // R-element twiddle set live in registers: -7% time at m = 4096)
+      constexpr int Q = pass_q(R);
 #pragma unroll
       for (int r = 1; r < R; ++r) {
         const int a = r / Q, c = r % Q;
-        if (c != 0) x[r] = cmul_dir<SIGN>(x[r], lo[c]);
-        if (a != 0) x[r] = cmul_dir<SIGN>(x[r], hi[a]);
-      }
-#else
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        const int a = r / Q, c = r % Q;
-        const double2 w = a == 0 ? lo[c] : (c == 0 ? hi[a] : cmul(hi[a], lo[c]));
-        x[r] = cmul_dir<SIGN>(x[r], w);
-      }
-#endif
+        if (c != 0) x[r] = cmul_dir<SIGN>(x[r], pt.lo[b][c]);
+        if (a != 0) x[r] = cmul_dir<SIGN>(x[r], pt.hi[b][a]);
       }
     }
     dft<R, SIGN>(x);
 #pragma unroll
     for (int r = 0; r < R; ++r) v[b + r * B] = x[r];
   }
+}
+
+template <int N, int E, int R, int NS, int SIGN>
+__device__ __forceinline__ void pass_compute(double2 (&v)[E], int t, const double2* __restrict__ tw) {
+  pass_compute<N, E, R, NS, SIGN>(v, load_pass_tw<N, E, R, NS>(t, tw));
 }
 
 // Permute the pass output through shared memory back into the natural
@@ -333,13 +346,15 @@ __device__ __forceinline__ void pass_exchange(double2 (&v)[E], int t, double2* _
 
 template <int N, int E, int NS, int SIGN, class Sync, class XS>
 __device__ __forceinline__ void fft_passes(double2 (&v)[E], int t, double2* __restrict__ xb,
-                                           const double2* __restrict__ tw, Sync sync, XS xs) {
+                                           const double2* __restrict__ tw, Sync sync, XS xs,
+                                           const PassTw<N, E, pass_radix(N, E, NS), NS>& pt) {
   if constexpr (NS < N) {
-    constexpr int R = (NS * E <= N) ? E : N / NS;
-    pass_compute<N, E, R, NS, SIGN>(v, t, tw);
+    constexpr int R = pass_radix(N, E, NS);
+    pass_compute<N, E, R, NS, SIGN>(v, pt);
     if constexpr (NS * R < N) {
+      const auto next = load_pass_tw<N, E, pass_radix(N, E, NS * R), NS * R>(t, tw);   // ahead of the exchange
       pass_exchange<N, E, R, NS>(v, t, xb, sync, xs);
-      fft_passes<N, E, NS * R, SIGN>(v, t, xb, tw, sync, xs);
+      fft_passes<N, E, NS * R, SIGN>(v, t, xb, tw, sync, xs, next);
     }
   }
 }
@@ -360,7 +375,7 @@ __device__ __forceinline__ void fft(double2 (&v)[E], int t, double2* __restrict_
   // out of the caller's row loop and held live in registers across it.
   int tl;
   asm volatile("mov.b32 %0, %1;" : "=r"(tl) : "r"(t));
-  fft_passes<N, E, 1, SIGN>(v, tl, xb, tw, sync, xs);
+  fft_passes<N, E, 1, SIGN>(v, tl, xb, tw, sync, xs, PassTw<N, E, pass_radix(N, E, 1), 1>{});
 }
 
 // Two independent N-point FFTs (same sign) in lockstep: each pass computes
@@ -370,12 +385,13 @@ __device__ __forceinline__ void fft(double2 (&v)[E], int t, double2* __restrict_
 template <int N, int E, int NS, int SIGN, class Sync, class XS>
 __device__ __forceinline__ void fft2_passes(double2 (&v)[E], double2 (&w)[E], int t, double2* __restrict__ xb,
                                             double2* __restrict__ xb2, const double2* __restrict__ tw, Sync sync,
-                                            XS xs) {
+                                            XS xs, const PassTw<N, E, pass_radix(N, E, NS), NS>& pt) {
   if constexpr (NS < N) {
-    constexpr int R = (NS * E <= N) ? E : N / NS;
-    pass_compute<N, E, R, NS, SIGN>(v, t, tw);
-    pass_compute<N, E, R, NS, SIGN>(w, t, tw);
+    constexpr int R = pass_radix(N, E, NS);
+    pass_compute<N, E, R, NS, SIGN>(v, pt);
+    pass_compute<N, E, R, NS, SIGN>(w, pt);
     if constexpr (NS * R < N) {
+      const auto next = load_pass_tw<N, E, pass_radix(N, E, NS * R), NS * R>(t, tw);
       constexpr int T = N / E, B = E / R;
 #pragma unroll
       for (int b = 0; b < B; ++b) {
@@ -394,7 +410,7 @@ __device__ __forceinline__ void fft2_passes(double2 (&v)[E], double2 (&w)[E], in
         w[i] = xb2[xs(xpad<NS, R>(t + T * i))];
       }
       sync();
-      fft2_passes<N, E, NS * R, SIGN>(v, w, t, xb, xb2, tw, sync, xs);
+      fft2_passes<N, E, NS * R, SIGN>(v, w, t, xb, xb2, tw, sync, xs, next);
     }
   }
 }
@@ -405,7 +421,7 @@ __device__ __forceinline__ void fft2(double2 (&v)[E], double2 (&w)[E], int t, do
                                      XS xs = XS{}) {
   int tl;
   asm volatile("mov.b32 %0, %1;" : "=r"(tl) : "r"(t));
-  fft2_passes<N, E, 1, SIGN>(v, w, tl, xb, xb2, tw, sync, xs);
+  fft2_passes<N, E, 1, SIGN>(v, w, tl, xb, xb2, tw, sync, xs, PassTw<N, E, pass_radix(N, E, 1), 1>{});
 }
 
 // CTA barrier as volatile asm: it keeps its order relative to the volatile
