@@ -164,6 +164,17 @@ __device__ __forceinline__ double2 twc(double2 a) {
   }
 }
 
+// x * i^Q (Q mod 4): sign flips and swaps only (a generic cmul by the
+// constant (0, 1) would still cost four fp64 instructions under IEEE rules)
+template <int Q>
+__device__ __forceinline__ double2 mul_i(double2 x) {
+  constexpr int q = ((Q % 4) + 4) % 4;
+  if constexpr (q == 0) return x;
+  else if constexpr (q == 1) return make_double2(-x.y, x.x);
+  else if constexpr (q == 2) return make_double2(-x.x, -x.y);
+  else return make_double2(x.y, -x.x);
+}
+
 // Per-element roots of the residue split / recombination: element i of a
 // lane (k = t + T i, T = M / E) needs zeta_{QM}^{R k} = zeta_{QM}^{R t} *
 // zeta_{QE}^{R i}.  The lane loads zt = zeta_{QM}^{R t} once; the second

@@ -199,11 +199,12 @@ k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const doub
     // (za, zb are re-loaded per stage -- volatile loads -- so that the derived
     // per-element roots are recomputed, not kept live across transforms.)
     double2 v[E], w[E];
+    // c_r = (-i)^r = i^{-r} is applied by sign flips / swaps (mul_i); residue
+    // r = 0 has no root at all.
     auto split = [&](auto R0) {   // both f/g residue streams of the pair, one read of the staged row
       constexpr int r0 = decltype(R0)::value;
-      const double2 ca = r0 == 0 ? make_double2(1, 0) : make_double2(-1, 0);   // (-i)^{r0}
-      const double2 cb = r0 == 0 ? make_double2(0, -1) : make_double2(0, 1);   // (-i)^{r0+1}
-      const double2 za = ldtw(&tw4M[r0 * t]), zb = ldtw(&tw4M[(r0 + 1) * t]);
+      const double2 za = r0 == 0 ? make_double2(1, 0) : ldtw(&tw4M[r0 * t]);
+      const double2 zb = ldtw(&tw4M[(r0 + 1) * t]);
       static_for<E>([&](auto I) {
         constexpr int i = decltype(I)::value;
         const int k = t + T * i;
@@ -213,16 +214,17 @@ k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const doub
           const double2 fk = F[k], gk = Gs[k], fm = F[M - k], gm = Gs[M - k];
           const double2 P = make_double2(fk.x - gk.y, fk.y + gk.x);
           const double2 R = make_double2(fm.x + gm.y, gm.x - fm.y);
-          v[i] = cmul(twc<r0 * i, 4 * E, +1>(za), cadd(P, cmul(ca, R)));
-          w[i] = cmul(twc<(r0 + 1) * i, 4 * E, +1>(zb), cadd(P, cmul(cb, R)));
+          const double2 sa = cadd(P, mul_i<-r0>(R));
+          if constexpr (r0 == 0) v[i] = sa;
+          else v[i] = cmul(twc<r0 * i, 4 * E, +1>(za), sa);
+          w[i] = cmul(twc<(r0 + 1) * i, 4 * E, +1>(zb), cadd(P, mul_i<-(r0 + 1)>(R)));
         }
       });
     };
     auto hpack = [&](auto R0) {   // h packed across the pair: w^h_{r0} + i w^h_{r0+1}
       constexpr int r0 = decltype(R0)::value;
-      const double2 ca = r0 == 0 ? make_double2(1, 0) : make_double2(-1, 0);
-      const double2 cb = r0 == 0 ? make_double2(0, -1) : make_double2(0, 1);
-      const double2 za = ldtw(&tw4M[r0 * t]), zb = ldtw(&tw4M[(r0 + 1) * t]);
+      const double2 za = r0 == 0 ? make_double2(1, 0) : ldtw(&tw4M[r0 * t]);
+      const double2 zb = ldtw(&tw4M[(r0 + 1) * t]);
       static_for<E>([&](auto I) {
         constexpr int i = decltype(I)::value;
         const int k = t + T * i;
@@ -231,15 +233,17 @@ k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const doub
           v[i] = make_double2(h0, h0);
         } else {
           const double2 hk = ldv(&hr[k]), hm = cconj(ldv(&hr[M - k]));
-          const double2 w0 = cmul(twc<r0 * i, 4 * E, +1>(za), cadd(hk, cmul(ca, hm)));
-          const double2 w1 = cmul(twc<(r0 + 1) * i, 4 * E, +1>(zb), cadd(hk, cmul(cb, hm)));
+          double2 w0 = cadd(hk, mul_i<-r0>(hm));
+          if constexpr (r0 != 0) w0 = cmul(twc<r0 * i, 4 * E, +1>(za), w0);
+          const double2 w1 = cmul(twc<(r0 + 1) * i, 4 * E, +1>(zb), cadd(hk, mul_i<-(r0 + 1)>(hm)));
           v[i] = make_double2(w0.x - w1.y, w0.y + w1.x);
         }
       });
     };
     auto recombine = [&](auto R0) {   // separate the pair's real-data spectra via v_{m-k}
       constexpr int r0 = decltype(R0)::value;
-      const double2 za = ldtw(&tw4M[r0 * t]), zb = ldtw(&tw4M[(r0 + 1) * t]);
+      const double2 za = r0 == 0 ? make_double2(1, 0) : ldtw(&tw4M[r0 * t]);
+      const double2 zb = ldtw(&tw4M[(r0 + 1) * t]);
       static_for<E>([&](auto I) {
         constexpr int i = decltype(I)::value;
         const int k = t + T * i;
@@ -247,7 +251,9 @@ k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const doub
         const double2 pp0 = cscale(cadd(a, b), 0.5);
         const double2 d = csub(a, b);
         const double2 pp1 = make_double2(0.5 * d.y, -0.5 * d.x);
-        const double2 ct = cadd(cmulc(pp0, twc<r0 * i, 4 * E, +1>(za)), cmulc(pp1, twc<(r0 + 1) * i, 4 * E, +1>(zb)));
+        double2 c0 = pp0;
+        if constexpr (r0 != 0) c0 = cmulc(pp0, twc<r0 * i, 4 * E, +1>(za));
+        const double2 ct = cadd(c0, cmulc(pp1, twc<(r0 + 1) * i, 4 * E, +1>(zb)));
         if constexpr (r0 == 0) fw[k] = ct;                         // partial sum of residues 0, 1
         else fw[k] = cscale(cadd(ldv(&fw[k]), ct), inv);           // + residues 2, 3, then 1/(4m)
       });
