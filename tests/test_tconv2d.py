@@ -56,3 +56,23 @@ def test_tconv2d_gpu(mx, my):
     F, G, H = (torch.from_numpy(a.copy()).cuda() for a in (f, g, h))
     idconv.tconv2d(F, G, H)
     assert rel_l2(F.cpu().numpy(), ternary2d.direct(f, g, h)) < 1e-14
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mx,my", [(512, 256), (2048, 2048)])
+def test_tconv2d_closed_form_large_gpu(mx, my):
+    # f = F e^{i(kx+ky)} (F real) family at a large size: t = FGH e^{i(kx+ky)} N3(mx,kx) N3(my,ky)
+    import torch
+    from paper_1008_1366_b200 import idconv
+    kx = torch.arange(-(mx - 1), mx, dtype=torch.float64)[:, None]
+    ky = torch.arange(my, dtype=torch.float64)[None, :]
+    e = torch.exp(1j * (kx + ky)).to(torch.complex128)
+    F, G, H = np.sqrt(2), np.sqrt(3), np.sqrt(5)
+    lay = lambda a: torch.cat([torch.zeros((1, my), dtype=torch.complex128), a], dim=0).contiguous().cuda()
+    A, B, C = lay(F * e), lay(G * e), lay(H * e)
+    idconv.tconv2d(A, B, C)
+    cx = torch.from_numpy(closed.ternary_count(mx, np.arange(-(mx - 1), mx)))[:, None]
+    cy = torch.from_numpy(closed.ternary_count(my, np.arange(my)))[None, :]
+    ref = F * G * H * e * cx * cy
+    got = A[1:].cpu()
+    assert float(torch.linalg.vector_norm(got - ref) / torch.linalg.vector_norm(ref)) < 1e-13
