@@ -32,11 +32,18 @@ namespace {
 #ifndef IDC_PENCIL_MINB
 #define IDC_PENCIL_MINB 1
 #endif
-template <int N>
+// K7 (fft0padBackward) may use its own CTA size / CTAs per SM (experiments)
+#ifndef IDC_PENCIL0_THREADS
+#define IDC_PENCIL0_THREADS IDC_PENCIL_THREADS
+#endif
+#ifndef IDC_PENCIL0_MINB
+#define IDC_PENCIL0_MINB IDC_PENCIL_MINB
+#endif
+template <int N, int TH = IDC_PENCIL_THREADS>
 struct TCfg {
   static constexpr int E = IDC_PENCIL_E;
   static constexpr int T = N / E;
-  static constexpr int W = IDC_PENCIL_THREADS / T < 1 ? 1 : (IDC_PENCIL_THREADS / T > 16 ? 16 : IDC_PENCIL_THREADS / T);
+  static constexpr int W = TH / T < 1 ? 1 : (TH / T > 16 ? 16 : TH / T);
   static constexpr int THREADS = T * W;
   static constexpr int BR = N < 256 ? N : 256;                     // TMA box rows
   static constexpr int XB = (xbuf_elems<N, E>() > 0 ? xbuf_elems<N, E>() : 1) * W;
@@ -219,11 +226,11 @@ k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
 // Centered column of 2N-1 rows staged whole (2N rows of stage, last one
 // padding), three streams written as in pencils.cu.
 template <int N>
-__global__ void __launch_bounds__(TCfg<N>::THREADS, IDC_PENCIL_MINB)
+__global__ void __launch_bounds__(TCfg<N, IDC_PENCIL0_THREADS>::THREADS, IDC_PENCIL0_MINB)
 k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mg,
                double2* __restrict__ f, double2* __restrict__ g, double2* __restrict__ U, double2* __restrict__ V,
                Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw3N) {
-  using C = TCfg<N>;
+  using C = TCfg<N, IDC_PENCIL0_THREADS>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   constexpr int R2 = ((2 * N - 1 + BR - 1) / BR) * BR;              // staged rows
   extern __shared__ __align__(128) double2 smem[];
@@ -437,9 +444,8 @@ cudaError_t launch_t(K kernel, int threads, size_t smem, long ntiles, cudaStream
   return cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s);
 }
 
-template <int N>
+template <int W>
 Tiles make_tiles(long ncols, long batch, int inputs, long bstride, long ustride) {
-  constexpr int W = TCfg<N>::W;
   Tiles tl;
   tl.ncols = ncols;
   tl.nct = (ncols + W - 1) / W;
@@ -463,7 +469,7 @@ cudaError_t pad_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nco
   CUtensorMap mf, mg;
   if (!encode_pencil_map(&mf, f, ncols, N, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
   if (!encode_pencil_map(&mg, g ? g : f, ncols, N, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
-  Tiles tl = make_tiles<N>(ncols, batch, g ? 2 : 1, bstride, ustride);
+  Tiles tl = make_tiles<C::W>(ncols, batch, g ? 2 : 1, bstride, ustride);
   void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw2N, &ophase};
   const size_t smem = ((size_t)N * C::W + C::XB) * 16 + 16;
   return launch_t(k_pad_bwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
@@ -479,7 +485,7 @@ cudaError_t pad_fwd_tma(double2* f, const double2* U, long ncols, long batch, lo
   CUtensorMap mf, mu;
   if (!encode_pencil_map(&mf, f, ncols, N, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
   if (!encode_pencil_map(&mu, U, ncols, N, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
-  Tiles tl = make_tiles<N>(ncols, batch, 1, bstride, ustride);
+  Tiles tl = make_tiles<C::W>(ncols, batch, 1, bstride, ustride);
   void* args[] = {&mf, &mu, &f, &tl, &twN, &tw2N, &ophase};
   const size_t smem = (2 * (size_t)N * C::W + C::XB) * 16 + 32;
   return launch_t(k_pad_fwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
@@ -488,15 +494,15 @@ cudaError_t pad_fwd_tma(double2* f, const double2* U, long ncols, long batch, lo
 template <int N>
 cudaError_t pad0_bwd_tma(double2* f, double2* g, double2* U, double2* V, long ncols, long batch, long bstride,
                          long ustride, cudaStream_t s) {
-  using C = TCfg<N>;
+  using C = TCfg<N, IDC_PENCIL0_THREADS>;
   constexpr int R2 = ((2 * N - 1 + C::BR - 1) / C::BR) * C::BR;
-  const double2* twN = pass_table(N, TCfg<N>::E);
+  const double2* twN = pass_table(N, C::E);
   const double2* tw3N = zeta_table(3 * N);
   if (!twN || !tw3N) return cudaErrorMemoryAllocation;
   CUtensorMap mf, mg;
   if (!encode_pencil_map(&mf, f, ncols, 2 * N - 1, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
   if (!encode_pencil_map(&mg, g ? g : f, ncols, 2 * N - 1, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
-  Tiles tl = make_tiles<N>(ncols, batch, g ? 2 : 1, bstride, ustride);
+  Tiles tl = make_tiles<C::W>(ncols, batch, g ? 2 : 1, bstride, ustride);
   void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw3N};
   const size_t smem = ((size_t)R2 * C::W + C::XB) * 16 + 16;
   return launch_t(k_pad0_bwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
@@ -513,7 +519,7 @@ cudaError_t pad0_fwd_tma(double2* f, const double2* U, long ncols, long batch, l
   if (!encode_pencil_map(&mf, f, ncols, 2 * N - 1, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
   if (!encode_pencil_map(&mu, U, ncols, N + 1, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
   if (!encode_pencil_map(&mu1, U, ncols, N + 1, batch, ustride, C::W, 1)) return cudaErrorNotSupported;
-  Tiles tl = make_tiles<N>(ncols, batch, 1, bstride, ustride);
+  Tiles tl = make_tiles<C::W>(ncols, batch, 1, bstride, ustride);
   void* args[] = {&mf, &mu, &mu1, &f, &tl, &twN, &tw3N};
   const size_t smem = (2 * (size_t)N * C::W + 32 + C::XB) * 16 + 32;
   return launch_t(k_pad0_fwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
