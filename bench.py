@@ -458,6 +458,113 @@ def cpu_baseline(args, parts):
             "sample": desc + " -- oracle direct sums (TwoProd+Neumaier, OpenMP), oracle/direct.c"}
 
 
+# ------------------------------------------------- distributed 3D (--dist) --
+
+def run_dist3d(args):
+    """Strong scaling of one 3D convolution over all ranks: rank r
+    holds x-planes [r nx, (r+1) nx) of the global config-5 arrays (hconv3d: the
+    2mx-1 planes padded to 2mx), idc_{c,h}conv3d_dist does the y-pass,
+    ncclAlltoAll, the per-residue (x, z) 2D convolutions, the all-to-all back
+    and the y-forward.  value = convolutions / max-over-ranks time."""
+    import torch
+    import torch.distributed as tdist
+    from paper_1008_1366_b200 import idconv as idc
+
+    ws, rank, local = dist_env()
+    wl = WORKLOADS[args.workload]
+    p = wl["parts"][0]
+    kind = p["kind"]
+    if kind not in ("cconv3d", "hconv3d"):
+        raise SystemExit("--dist applies to the 3D workloads (c5a, c5b)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import datetime
+    if not tdist.is_initialized():
+        tmo = datetime.timedelta(seconds=120)
+        if "MASTER_ADDR" in os.environ:                      # launched by torchrun: env:// rendezvous
+            tdist.init_process_group("nccl" if ws > 1 else "gloo", timeout=tmo)
+        else:
+            tdist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % (29650 + os.getpid() % 300),
+                                     rank=0, world_size=1, timeout=tmo)
+    comm = idc.Comm()
+    mx, my, mz = p["m"]
+    herm = kind == "hconv3d"
+    planes = 2 * mx if herm else mx
+    nx = planes // ws
+    x0 = rank * nx
+    ny = 2 * my - 1 if herm else my
+    plane = ny * mz
+    pristine = []
+    for role in range(2):
+        a = torch.empty((nx, ny, mz), dtype=torch.complex128, device=dev)
+        idc.fill_uniform(a, synthgen.array_id(role, 0), synthgen.SEED, start=x0 * plane)
+        kx = torch.arange(x0, x0 + nx, device=dev, dtype=torch.float64) - ((mx - 1) if herm else 0)
+        kyv = torch.arange(ny, device=dev, dtype=torch.float64) - ((my - 1) if herm else 0)
+        kz = torch.arange(mz, device=dev, dtype=torch.float64)
+        a /= 1.0 + kx[:, None, None] ** 2 + kyv[None, :, None] ** 2 + kz[None, None, :] ** 2
+        if herm and x0 + nx == planes:
+            a[-1].zero_()                                  # padding plane
+        pristine.append(a)
+    work = [torch.empty_like(a) for a in pristine]
+    fn = idc.hconv3d_dist if herm else idc.cconv3d_dist
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def restore():
+        for src, dst in zip(pristine, work):
+            dst.copy_(src)
+        flush.zero_()
+
+    for _ in range(args.warmup):
+        restore()
+        fn(comm, work[0], work[1], mx, my, mz)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    ms = 0.0
+    n0 = idc.launch_count()
+    for _ in range(args.steps):
+        restore()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn(comm, work[0], work[1], mx, my, mz)
+        e1.record()
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+    launches = idc.launch_count() - n0
+    tdist.barrier()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev if ws > 1 else "cpu")
+    if ws > 1:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = args.steps / (ms_max / 1e3)
+    b, fl = part_model(p)
+    pk = peaks()
+    sec = ms_max / 1e3 / args.steps
+    t_b = b / (pk["hbm_gbs"] * 1e9 * ws)
+    t_f = fl / (pk["fp64_tflops"] * 1e12 * ws)
+    out = None
+    if rank == 0:
+        bound = "hbm" if t_b >= t_f else "alu"
+        out = {
+            "metric": METRIC, "value": value, "unit": "conv/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl["desc"] + f" -- slab-sharded over {ws} rank(s), idc_{kind}_dist",
+                       "parallelism": f"x-slabs{ws}", "seed": synthgen.SEED,
+                       "l2": "L2 flushed (256 MB write) and inputs restored before every step"},
+            "roofline": {"bound": bound,
+                         "achieved": (b / sec / 1e9) if bound == "hbm" else (fl / sec / 1e12),
+                         "peak": pk["hbm_gbs"] * ws if bound == "hbm" else pk["fp64_tflops"] * ws,
+                         "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
+                         "frac": max(t_b, t_f) / sec, "kernel": kind + "_dist (all phases, aggregate peak)",
+                         "traffic": None},
+            "gpu_launches": launches, "cpu_baseline": None,
+        }
+    comm.close()
+    tdist.barrier()
+    tdist.destroy_process_group()
+    return out
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -493,10 +600,17 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle CPU work")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="3D workloads: one convolution slab-sharded over all ranks (strong scaling)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "idconv":
         print("warning: the contract asks for >= 3 warm-up steps", file=sys.stderr)
-    out = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if args.impl == "reference":
+        out = run_reference(args)
+    elif args.dist:
+        out = run_dist3d(args)
+    else:
+        out = run_ours(args)
     if out is not None:
         print(json.dumps(out), flush=True)
 
