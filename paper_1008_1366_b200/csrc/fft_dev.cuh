@@ -157,6 +157,14 @@ __device__ __forceinline__ double2 twc(double2 a) {
   } else if constexpr (j == 144) {          // * (-SIGN i)
     if constexpr (SIGN > 0) return make_double2(a.y, -a.x);
     else return make_double2(-a.y, a.x);
+  } else if constexpr (j % 48 == 24) {     // odd multiples of pi/4: |cos| = |sin|, 3 instructions
+    constexpr double c = cos192(j);
+    constexpr double s = SIGN > 0 ? sin192(j) : -sin192(j);
+    constexpr double h = 0.70710678118654752440084436210484904;   // sqrt(1/2)
+    // a (c + i s) with c = sc h, s = ss h: re = a.x c - ss (a.y h), im = a.x s + sc (a.y h)
+    constexpr double sc = c > 0 ? 1.0 : -1.0, ss = s > 0 ? 1.0 : -1.0;
+    const double ty = a.y * h;
+    return make_double2(fma(a.x, sc * h, -ss * ty), fma(a.x, ss * h, sc * ty));
   } else {
     constexpr double c = cos192(j);
     constexpr double s = SIGN > 0 ? sin192(j) : -sin192(j);
