@@ -39,15 +39,24 @@ namespace {
 #ifndef IDC_PENCIL0_MINB
 #define IDC_PENCIL0_MINB IDC_PENCIL_MINB
 #endif
-template <int N, int TH = IDC_PENCIL_THREADS>
+template <int N, int TH = IDC_PENCIL_THREADS, int EE = IDC_PENCIL_E>
 struct TCfg {
-  static constexpr int E = IDC_PENCIL_E;
+  static constexpr int E = EE;
   static constexpr int T = N / E;
   static constexpr int W = TH / T < 1 ? 1 : (TH / T > 16 ? 16 : TH / T);
   static constexpr int THREADS = T * W;
   static constexpr int BR = N < 256 ? N : 256;                     // TMA box rows
   static constexpr int XB = (xbuf_elems<N, E>() > 0 ? xbuf_elems<N, E>() : 1) * W;
 };
+
+// K5 / K6 (complex fftpad pencils): E = 16 with 256-thread CTAs at
+// m = 256 and 1024 (measured 3-5% faster on cconv2d 1024^2 and 64 x 256^2);
+// E = 8 with 512-thread CTAs at m = 512 (cconv3d 512^3 1.7% faster so) and
+// above 1024 (long columns need the threads for W >= 2).
+template <int N>
+constexpr bool k56_wide() { return N == 256 || N == 1024; }
+template <int N>
+using K56Cfg = TCfg<N, (k56_wide<N>() ? 256 : IDC_PENCIL_THREADS), (k56_wide<N>() ? 16 : IDC_PENCIL_E)>;
 
 template <int W>
 struct Slot2 {
@@ -86,11 +95,11 @@ __device__ __forceinline__ void load_rows(const CUtensorMap* map, double2* stage
 
 // ------------------------------------------------------------------- K5 --
 template <int N>
-__global__ void __launch_bounds__(TCfg<N>::THREADS, IDC_PENCIL_MINB)
+__global__ void __launch_bounds__(K56Cfg<N>::THREADS, IDC_PENCIL_MINB)
 k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mg, double2* __restrict__ f,
               double2* __restrict__ g, double2* __restrict__ U, double2* __restrict__ V, Tiles tl,
               const double2* __restrict__ twN, const double2* __restrict__ tw2N, double2 ophase) {
-  using C = TCfg<N>;
+  using C = K56Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   extern __shared__ __align__(128) double2 smem[];
   double2* stage = smem;                       // N x W
@@ -153,10 +162,10 @@ k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
 
 // ------------------------------------------------------------------- K6 --
 template <int N>
-__global__ void __launch_bounds__(TCfg<N>::THREADS, IDC_PENCIL_MINB)
+__global__ void __launch_bounds__(K56Cfg<N>::THREADS, IDC_PENCIL_MINB)
 k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mu, double2* __restrict__ f,
               Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw2N, double2 ophase) {
-  using C = TCfg<N>;
+  using C = K56Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   extern __shared__ __align__(128) double2 smem[];
   double2* sf = smem;
@@ -462,8 +471,8 @@ Tiles make_tiles(long ncols, long batch, int inputs, long bstride, long ustride)
 template <int N>
 cudaError_t pad_bwd_tma(double2* f, double2* g, double2* U, double2* V, long ncols, long batch, long bstride,
                         long ustride, cudaStream_t s, double2 ophase) {
-  using C = TCfg<N>;
-  const double2* twN = pass_table(N, TCfg<N>::E);
+  using C = K56Cfg<N>;
+  const double2* twN = pass_table(N, C::E);
   const double2* tw2N = zeta_table(2 * N);
   if (!twN || !tw2N) return cudaErrorMemoryAllocation;
   CUtensorMap mf, mg;
@@ -478,8 +487,8 @@ cudaError_t pad_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nco
 template <int N>
 cudaError_t pad_fwd_tma(double2* f, const double2* U, long ncols, long batch, long bstride, long ustride,
                         cudaStream_t s, double2 ophase) {
-  using C = TCfg<N>;
-  const double2* twN = pass_table(N, TCfg<N>::E);
+  using C = K56Cfg<N>;
+  const double2* twN = pass_table(N, C::E);
   const double2* tw2N = zeta_table(2 * N);
   if (!twN || !tw2N) return cudaErrorMemoryAllocation;
   CUtensorMap mf, mu;
