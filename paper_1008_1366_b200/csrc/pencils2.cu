@@ -58,6 +58,14 @@ constexpr bool k56_wide() { return N == 256 || N == 1024; }
 template <int N>
 using K56Cfg = TCfg<N, (k56_wide<N>() ? 256 : IDC_PENCIL_THREADS), (k56_wide<N>() ? 16 : IDC_PENCIL_E)>;
 
+// K7 / K8 (centered fft0pad pencils): E = 16 with 256-thread CTAs (255
+// registers, three radix-16 passes) for 256 <= m <= 2048 -- measured
+// hconv2d 2048^2 -5%, hconv3d 512^3 -1.5% against E = 8 / 512 threads.
+template <int N>
+constexpr bool k78_wide() { return N >= 256 && N <= 2048; }
+template <int N>
+using K78Cfg = TCfg<N, (k78_wide<N>() ? 256 : IDC_PENCIL0_THREADS), (k78_wide<N>() ? 16 : IDC_PENCIL_E)>;
+
 template <int W>
 struct Slot2 {
   int c;
@@ -235,11 +243,11 @@ k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
 // Centered column of 2N-1 rows staged whole (2N rows of stage, last one
 // padding), three streams written as in pencils.cu.
 template <int N>
-__global__ void __launch_bounds__(TCfg<N, IDC_PENCIL0_THREADS>::THREADS, IDC_PENCIL0_MINB)
+__global__ void __launch_bounds__(K78Cfg<N>::THREADS, IDC_PENCIL0_MINB)
 k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mg,
                double2* __restrict__ f, double2* __restrict__ g, double2* __restrict__ U, double2* __restrict__ V,
                Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw3N) {
-  using C = TCfg<N, IDC_PENCIL0_THREADS>;
+  using C = K78Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   constexpr int R2 = ((2 * N - 1 + BR - 1) / BR) * BR;              // staged rows
   extern __shared__ __align__(128) double2 smem[];
@@ -332,11 +340,11 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
 // 0..N-1), q = 1 (r = 0: f rows 0..N-2 and U row N, the latter through a
 // one-row box into a separate tail slot), q = 2 (r = +1: f rows N-1..2N-2).
 template <int N>
-__global__ void __launch_bounds__(TCfg<N>::THREADS, IDC_PENCIL_MINB)
+__global__ void __launch_bounds__(K78Cfg<N>::THREADS, IDC_PENCIL_MINB)
 k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mu,
                const __grid_constant__ CUtensorMap mu1, double2* __restrict__ f, Tiles tl,
                const double2* __restrict__ twN, const double2* __restrict__ tw3N) {
-  using C = TCfg<N>;
+  using C = K78Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   extern __shared__ __align__(128) double2 smem[];
   double2* st[2] = {smem, smem + N * W};
@@ -503,7 +511,7 @@ cudaError_t pad_fwd_tma(double2* f, const double2* U, long ncols, long batch, lo
 template <int N>
 cudaError_t pad0_bwd_tma(double2* f, double2* g, double2* U, double2* V, long ncols, long batch, long bstride,
                          long ustride, cudaStream_t s) {
-  using C = TCfg<N, IDC_PENCIL0_THREADS>;
+  using C = K78Cfg<N>;
   constexpr int R2 = ((2 * N - 1 + C::BR - 1) / C::BR) * C::BR;
   const double2* twN = pass_table(N, C::E);
   const double2* tw3N = zeta_table(3 * N);
@@ -520,8 +528,8 @@ cudaError_t pad0_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nc
 template <int N>
 cudaError_t pad0_fwd_tma(double2* f, const double2* U, long ncols, long batch, long bstride, long ustride,
                          cudaStream_t s) {
-  using C = TCfg<N>;
-  const double2* twN = pass_table(N, TCfg<N>::E);
+  using C = K78Cfg<N>;
+  const double2* twN = pass_table(N, C::E);
   const double2* tw3N = zeta_table(3 * N);
   if (!twN || !tw3N) return cudaErrorMemoryAllocation;
   CUtensorMap mf, mu, mu1;
