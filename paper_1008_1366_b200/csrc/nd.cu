@@ -43,25 +43,26 @@ size_t l2_bytes() {
 // L2-resident group (50%: one 512^2 slab per stream, 512-row launches) is
 // 17% slower than groups of ~10-20 slabs whose launches fill the GPU several
 // times over -- launch granularity matters more than L2 residency here, so
-// the default budget is 10x L2 (frac 1000).
+// the default budget is 20x L2 (frac 2000).
 long slab_group(size_t slab_bytes_all, long nslabs) {
   static long frac = -1;
   if (frac < 0) {
     const char* e = getenv("IDC_SLAB_L2_FRAC");
-    frac = e ? atol(e) : 1000;
+    frac = e ? atol(e) : 2000;
   }
   long G = (long)((l2_bytes() * frac / 100) / std::max<size_t>(slab_bytes_all, 1));
   return std::max<long>(1, std::min<long>(G, nslabs));
 }
 // Internal stream pool for concurrent slab groups (created once per device).
 constexpr int kMaxSlabStreams = 4;
-// slab streams in flight (IDC_SLAB_STREAMS, 1..4, default 4; experiments only)
+// slab streams in flight (IDC_SLAB_STREAMS, 1..4, default 2; measured
+// sweep tools/slab_sweep3.sh: 2 streams x ~80-slab groups best by ~1%)
 int slab_streams() {
   static int n = 0;
   if (n == 0) {
     const char* e = getenv("IDC_SLAB_STREAMS");
-    n = e ? atoi(e) : kMaxSlabStreams;
-    if (n < 1 || n > kMaxSlabStreams) n = kMaxSlabStreams;
+    n = e ? atoi(e) : 2;
+    if (n < 1 || n > kMaxSlabStreams) n = 2;
   }
   return n;
 }
