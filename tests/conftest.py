@@ -11,6 +11,12 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (run with -m gpu)")
     config.addinivalue_line("markers", "slow: long-running CPU test")
+    # The ABI tests load the in-tree library: build it (nvcc cross-compiles for
+    # sm_100a without a GPU) if a fresh checkout has not been built yet.
+    lib = os.path.join(ROOT, "paper_1008_1366_b200", "libidconv.so")
+    if not os.path.exists(lib):
+        from paper_1008_1366_b200 import _build
+        _build.build()
 
 
 @pytest.fixture(scope="session")
