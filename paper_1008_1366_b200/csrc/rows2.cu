@@ -339,11 +339,14 @@ cudaError_t launch2(K kernel, int threads, size_t smem, long nrows, int groups, 
 #endif
 // E = 8 for m <= 512 (three radix-8 passes at 512; 5-9% faster there),
 // 16 from 1024 up (three passes instead of four)
+#ifndef IDC_ROWS_CTA_THREADS
+#define IDC_ROWS_CTA_THREADS 256
+#endif
 template <int M>
 struct Tune {
   static constexpr int E = M < IDC_ROWS_E ? M : (M <= 512 ? 8 : IDC_ROWS_E);
   static constexpr int T = M / E;
-  static constexpr int G = T >= 256 ? 1 : 256 / T;
+  static constexpr int G = T >= IDC_ROWS_CTA_THREADS ? 1 : IDC_ROWS_CTA_THREADS / T;
 };
 
 }  // namespace
