@@ -15,6 +15,8 @@ from oracle import direct, rel_l2
     ("hconv1d", 256, 11, 256 * 16 * 3, False),    # pageable host memory
     ("tconv1d", 512, 7, 512 * 16 * 2, True),
     ("hconv1d", 4096, 9, 16 << 20, True),         # one chunk
+    ("cconv1d", 8192, 5, 8192 * 16 * 2, True),   # m = 8192: the row kernels' stash lives in the workspace
+    ("tconv1d", 8192, 3, 8192 * 16 * 2, False),
 ])
 def test_host_path(kind, m, B, chunk_bytes, pinned, monkeypatch):
     import torch
