@@ -317,7 +317,8 @@ def run_ours(args):
     clk.__exit__()
     if ws > 1:
         tdist.barrier()
-    part_ms = [sum(evs[k][j][0].elapsed_time(evs[k][j][1]) for k in range(args.steps)) for j in range(len(parts))]
+    samples = [[evs[k][j][0].elapsed_time(evs[k][j][1]) for k in range(args.steps)] for j in range(len(parts))]
+    part_ms = [sum(x) for x in samples]
     total_ms = sum(part_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if ws > 1:
@@ -335,6 +336,7 @@ def run_ours(args):
         t_b = b * p["batch"] / (pk["hbm_gbs"] * 1e9)
         t_f = fl * p["batch"] / (pk["fp64_tflops"] * 1e12)
         part_info.append(dict(kind=p["kind"], m=p["m"], batch=p["batch"], ms_per_call=sec * 1e3,
+                              call_stats=timing_stats(samples[len(part_info)]),
                               conv_per_s=p["batch"] / sec, hbm_gbs_alg=b * p["batch"] / sec / 1e9,
                               fp64_tflops_alg=fl * p["batch"] / sec / 1e12, t_roof_ms=max(t_b, t_f) * 1e3,
                               roofline_frac=max(t_b, t_f) / sec, bound="hbm" if t_b >= t_f else "alu"))
@@ -375,6 +377,19 @@ def run_ours(args):
         tdist.barrier()
         tdist.destroy_process_group()
     return out
+
+
+def timing_stats(t):
+    """Median and the paper's one-sided standard deviations of per-call times
+    (P:258-262, AMB-5): sigma_L/H = sqrt(sum_{t_i < T / t_i > T} (t_i - T)^2 / (n/2 - 1)),
+    T the mean of the n samples."""
+    n = len(t)
+    T = sum(t) / n
+    d = max(n / 2 - 1, 1)
+    lo = sum((x - T) ** 2 for x in t if x < T)
+    hi = sum((x - T) ** 2 for x in t if x > T)
+    return {"n": n, "mean_ms": T, "median_ms": statistics.median(t), "sigma_L_ms": (lo / d) ** 0.5,
+            "sigma_H_ms": (hi / d) ** 0.5}
 
 
 def load_traffic(kind, m):
