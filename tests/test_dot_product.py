@@ -144,3 +144,24 @@ def test_cconv2d_dot_gpu(mx, my, M):
     G = torch.from_numpy(np.stack([b[0] for a, b in fs])).cuda()
     idconv.cconv2d_dot(F, G)
     assert rel_l2(F[0].cpu().numpy(), sum(direct.cconv2d(a[0], b[0]) for a, b in fs)) < 1e-14
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mx,my", [(1, 2), (2, 2), (1, 8), (8, 2)])
+def test_dot_2d_tiny_gpu(mx, my):
+    import torch
+    from paper_1008_1366_b200 import idconv
+    fs = [synthgen.hconv2d_inputs(mx, my, roles=(2 * i, 2 * i + 1)) for i in range(2)]
+    F = torch.from_numpy(np.stack([a for a, b in fs])).cuda()
+    G = torch.from_numpy(np.stack([b for a, b in fs])).cuda()
+    idconv.hconv2d_dot(F, G)
+    assert rel_l2(F[0].cpu().numpy(), sum(direct.hconv2d(a, b) for a, b in fs)) < 1e-14
+    cs = [synthgen.cconv2d_inputs(mx, my, 1, roles=(2 * i, 2 * i + 1)) for i in range(2)]
+    F = torch.from_numpy(np.stack([a[0] for a, b in cs])).cuda()
+    G = torch.from_numpy(np.stack([b[0] for a, b in cs])).cuda()
+    idconv.cconv2d_dot(F, G)
+    assert rel_l2(F[0].cpu().numpy(), sum(direct.cconv2d(a[0], b[0]) for a, b in cs)) < 1e-14
+    w = synthgen.hconv2d_inputs(max(mx, 2), my, roles=(0,))[0]
+    out = idconv.advection2d(torch.from_numpy(w.copy()).cuda()).cpu().numpy()
+    ref = -application.euler_sum(w)
+    assert np.linalg.norm(out - ref) <= 1e-13 * max(np.linalg.norm(ref), 1.0)
