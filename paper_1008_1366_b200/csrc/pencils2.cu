@@ -12,6 +12,8 @@
 // t + T*i of column c -- consecutive lanes read consecutive 16-byte words.
 #include <cuda.h>
 
+#include <cstring>
+
 #include "fft_dev.cuh"
 #include "kernels.cuh"
 #include "nd_internal.cuh"
@@ -242,11 +244,31 @@ k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
 // ------------------------------------------------------------------- K7 --
 // Centered column of 2N-1 rows staged whole (2N rows of stage, last one
 // padding), three streams written as in pencils.cu.
+// K7 output path: each residue's transformed tile is parked in the exchange
+// buffer ([row][column], the FFT's last exchange is complete) and written by
+// TMA tensor stores -- per-thread 16-byte stores of a W = 2..4-column tile
+// kept the store data registers busy (32% long-scoreboard stalls on the
+// registers of the next store, ncu r01).  Maps: f rows 0..m-2 / m-1..2m-2,
+// the same for g, and U / V rows 0..m-1 (row m = the r = 0 stream's last
+// element, stored directly).
+#ifndef IDC_K7_TMA_STORE
+#define IDC_K7_TMA_STORE 1
+#endif
+// K8: both output halves through TMA stores (2; measured hconv3d -2.3%), U_k only
+// (1), or per-thread stores (0)
+#ifndef IDC_K8_TMA_STORE
+#define IDC_K8_TMA_STORE 2
+#endif
+struct K7StoreMaps {
+  CUtensorMap flo, fhi, glo, ghi, u, v;
+};
+
 template <int N>
 __global__ void __launch_bounds__(K78Cfg<N>::THREADS, IDC_PENCIL0_MINB)
 k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mg,
                double2* __restrict__ f, double2* __restrict__ g, double2* __restrict__ U, double2* __restrict__ V,
-               Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw3N) {
+               Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw3N,
+               const __grid_constant__ K7StoreMaps sm) {
   using C = K78Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   constexpr int R2 = ((2 * N - 1 + BR - 1) / BR) * BR;              // staged rows
@@ -320,6 +342,24 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
           load_rows<W, BR>(in2 == 0 ? &mf : &mg, stage, c2, 0, 2 * N - 1, item2, bar);
         }
       }
+#if IDC_K7_TMA_STORE
+      if (threadIdx.x == 0) bulk_wait_read();       // the previous residue's stores have read xb
+      __syncthreads();
+      fft<N, E, +1>(v, t, xb, twN, CtaSync{}, xs);  // ends with a barrier after its last exchange
+#pragma unroll
+      for (int i = 0; i < E; ++i) xb[(t + T * i) * W + c] = v[i];
+      if (r == 0 && t == T - 1 && ok) u[(long)N * S] = v[E - 1];   // l = m-1 -> U row m
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const CUtensorMap* mp = r == -1 ? (in == 0 ? &sm.u : &sm.v)
+                              : r == 0  ? (in == 0 ? &sm.flo : &sm.glo)
+                                        : (in == 0 ? &sm.fhi : &sm.ghi);
+        const int rows = r == 0 ? N - 1 : N;
+        for (int b = 0; b < rows; b += BR) tma_store_3d(mp, (int)(2 * col0), b, (int)item, xb + (long)b * W);
+        bulk_commit();
+      }
+#else
       fft<N, E, +1>(v, t, xb, twN, CtaSync{}, xs);
       if (ok) {
 #pragma unroll
@@ -331,8 +371,12 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
           *dst = v[i];
         }
       }
+#endif
     }
   }
+#if IDC_K7_TMA_STORE
+  if (threadIdx.x == 0) bulk_wait_all();
+#endif
 }
 
 // ------------------------------------------------------------------- K8 --
@@ -343,7 +387,8 @@ template <int N>
 __global__ void __launch_bounds__(K78Cfg<N>::THREADS, IDC_PENCIL_MINB)
 k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mu,
                const __grid_constant__ CUtensorMap mu1, double2* __restrict__ f, Tiles tl,
-               const double2* __restrict__ twN, const double2* __restrict__ tw3N) {
+               const double2* __restrict__ twN, const double2* __restrict__ tw3N,
+               const __grid_constant__ CUtensorMap mflo, const __grid_constant__ CUtensorMap mfhi) {
   using C = K78Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   extern __shared__ __align__(128) double2 smem[];
@@ -403,6 +448,9 @@ k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
         const int l = t + T * i;
         v[i] = (q == 1 && l == N - 1) ? tail[b][c] : st[b][l * W + c];
       }
+#if IDC_K8_TMA_STORE
+      if (q == 0 && threadIdx.x == 0) bulk_wait_read();   // last tile's output stores have read xb
+#endif
       __syncthreads();
       if (threadIdx.x == 0) {  // refill this buffer with the stream two steps ahead
         const int q2 = q + 2;
@@ -433,6 +481,41 @@ k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
         for_roots<3 * E, 1, +1, E>(zt, acc);
       }
     }
+#if IDC_K8_TMA_STORE
+    // U_k -> f rows m-1..2m-2 through the exchange buffer and TMA stores
+    // (the last FFT's exchanges are complete)
+#pragma unroll
+    for (int i = 0; i < E; ++i) xb[(t + T * i) * W + c] = cscale(ap[i], inv);
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int r0 = 0; r0 < N; r0 += BR) tma_store_3d(&mfhi, (int)(2 * col0), r0, (int)item, xb + (long)r0 * W);
+      bulk_commit();
+    }
+#if IDC_K8_TMA_STORE == 2
+    if (threadIdx.x == 0) bulk_wait_read();
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const int k = t + T * i;
+      if (k > 0) xb[(k - 1) * W + c] = cscale(an[i], inv);
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int r0 = 0; r0 < N - 1; r0 += BR) tma_store_3d(&mflo, (int)(2 * col0), r0, (int)item, xb + (long)r0 * W);
+      bulk_commit();
+    }
+#else
+    if (ok) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int k = t + T * i;
+        if (k > 0) a[(long)(k - 1) * S] = cscale(an[i], inv);
+      }
+    }
+#endif
+#else
     if (ok) {
 #pragma unroll
       for (int i = 0; i < E; ++i) {
@@ -441,7 +524,11 @@ k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
         if (k > 0) a[(long)(k - 1) * S] = cscale(an[i], inv);
       }
     }
+#endif
   }
+#if IDC_K8_TMA_STORE
+  if (threadIdx.x == 0) bulk_wait_all();
+#endif
 }
 
 // ================================================================ launchers ==
@@ -520,7 +607,24 @@ cudaError_t pad0_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nc
   if (!encode_pencil_map(&mf, f, ncols, 2 * N - 1, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
   if (!encode_pencil_map(&mg, g ? g : f, ncols, 2 * N - 1, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
   Tiles tl = make_tiles<C::W>(ncols, batch, g ? 2 : 1, bstride, ustride);
-  void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw3N};
+  K7StoreMaps sm;
+#if IDC_K7_TMA_STORE
+  {
+    double2* gg = g ? g : f;
+    double2* VV = g ? V : U;
+    const long lo = ((long)N - 1) * ncols;
+    if (!encode_pencil_map(&sm.flo, f, ncols, N - 1, batch, bstride, C::W, C::BR) ||
+        !encode_pencil_map(&sm.fhi, f + lo, ncols, N, batch, bstride, C::W, C::BR) ||
+        !encode_pencil_map(&sm.glo, gg, ncols, N - 1, batch, bstride, C::W, C::BR) ||
+        !encode_pencil_map(&sm.ghi, gg + lo, ncols, N, batch, bstride, C::W, C::BR) ||
+        !encode_pencil_map(&sm.u, U, ncols, N, batch, ustride, C::W, C::BR) ||
+        !encode_pencil_map(&sm.v, VV, ncols, N, batch, ustride, C::W, C::BR))
+      return cudaErrorNotSupported;
+  }
+#else
+  memset(&sm, 0, sizeof(sm));
+#endif
+  void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw3N, &sm};
   const size_t smem = ((size_t)R2 * C::W + C::XB) * 16 + 16;
   return launch_t(k_pad0_bwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
 }
@@ -537,7 +641,11 @@ cudaError_t pad0_fwd_tma(double2* f, const double2* U, long ncols, long batch, l
   if (!encode_pencil_map(&mu, U, ncols, N + 1, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
   if (!encode_pencil_map(&mu1, U, ncols, N + 1, batch, ustride, C::W, 1)) return cudaErrorNotSupported;
   Tiles tl = make_tiles<C::W>(ncols, batch, 1, bstride, ustride);
-  void* args[] = {&mf, &mu, &mu1, &f, &tl, &twN, &tw3N};
+  CUtensorMap mflo, mfhi;
+  if (!encode_pencil_map(&mflo, f, ncols, N - 1, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
+  if (!encode_pencil_map(&mfhi, f + ((long)N - 1) * ncols, ncols, N, batch, bstride, C::W, C::BR))
+    return cudaErrorNotSupported;
+  void* args[] = {&mf, &mu, &mu1, &f, &tl, &twN, &tw3N, &mflo, &mfhi};
   const size_t smem = (2 * (size_t)N * C::W + 32 + C::XB) * 16 + 32;
   return launch_t(k_pad0_fwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
 }
