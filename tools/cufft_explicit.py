@@ -113,6 +113,82 @@ def tconv2d(f, g, h):
     return out
 
 
+# ---- pruned explicit versions ----------
+# Johnson's pruning: transform first along the axes whose padded
+# half is zero, so that the later (outer) transforms skip the all-zero lines;
+# the inverse transforms run in the opposite order and drop the unneeded half
+# before the next axis.  Same padded sizes, same results, fewer transforms.
+
+def cconv2d_pruned(f, g):
+    """y-pruned explicit 2D complex: x transforms only on the my
+    unpadded columns, both ways."""
+    mx, my = f.shape[-2:]
+
+    def fwd(a):
+        return F.fft(F.fft(a, n=2 * mx, dim=-2), n=2 * my, dim=-1)
+    X = fwd(f)
+    X *= fwd(g)
+    return F.ifft(F.ifft(X, dim=-1)[..., :my], dim=-2)[..., :mx, :]
+
+
+def _centered_rows(A, m, N):
+    """Centered axis -2 (index i <-> k = i - (m-1)) placed at k mod N."""
+    k = torch.arange(-(m - 1), m, device=A.device) % N
+    P = torch.zeros(A.shape[:-2] + (N, A.shape[-1]), dtype=A.dtype, device=A.device)
+    P[..., k, :] = A
+    return P, k
+
+
+def hconv2d_pruned(f, g):
+    """y-pruned explicit 2D centered Hermitian: complex x transforms (3mx) on
+    the my stored half-spectrum columns only, then c2r along y (3my)."""
+    nx, my = f.shape
+    mx = (nx + 1) // 2
+    Nx, Ny = 3 * mx, 3 * my
+
+    def bwd(a):
+        P, k = _centered_rows(a, mx, Nx)
+        return F.irfft(F.ifft(P, dim=0) * Nx, n=Ny, dim=1) * Ny, k
+    u, k = bwd(f)
+    w, _ = bwd(g)
+    u *= w
+    del w
+    return F.fft(F.rfft(u, dim=1)[:, :my], dim=0)[k] / (Nx * Ny)
+
+
+def tconv2d_pruned(f, g, h):
+    """y-pruned explicit 2D centered Hermitian ternary: 4mx x
+    4my padding, x transforms on the my stored columns only."""
+    nx, my = f.shape
+    mx = nx // 2
+    Nx, Ny = 4 * mx, 4 * my
+    u = None
+    for a in (f, g, h):
+        P, k = _centered_rows(a[1:], mx, Nx)
+        x = F.irfft(F.ifft(P, dim=0) * Nx, n=Ny, dim=1) * Ny
+        del P
+        u = x if u is None else u * x
+    H = F.fft(F.rfft(u, dim=1)[:, :my], dim=0)[k] / (Nx * Ny)
+    out = torch.zeros_like(f)
+    out[1:] = H
+    return out
+
+
+def cconv3d_pruned(f, g):
+    """Pruned explicit 3D complex (the paper's xz-pruned comparison,
+    P:884-886, pruned on every axis it can be): z transforms on the mx*my
+    stored lines, y on mx*2mz, x on 2my*2mz; inverses in reverse order."""
+    mx, my, mz = f.shape
+
+    def fwd(a):
+        return F.fft(F.fft(F.fft(a, n=2 * mz, dim=2), n=2 * my, dim=1), n=2 * mx, dim=0)
+    X = fwd(f)
+    X *= fwd(g)
+    X = F.ifft(X, dim=0)[:mx]
+    X = F.ifft(X, dim=1)[:, :my]
+    return F.ifft(X, dim=2)[..., :mz]
+
+
 def cconv3d(f, g):
     mx, my, mz = f.shape
     s = (2 * mx, 2 * my, 2 * mz)
@@ -149,16 +225,36 @@ CONFIGS = [  # (name, kind, shape, arrays) -- BASELINE.json configs
 ]
 
 
+PRUNED = {"cconv2d": cconv2d_pruned, "hconv2d": hconv2d_pruned, "tconv2d": tconv2d_pruned,
+          "cconv3d": cconv3d_pruned}
+
+
 def _time(fn, reps=3):
+    """Best of `reps` timed calls (after one warm-up) and the peak device
+    memory the call allocates beyond what is live before it (bytes)."""
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
     out = fn()
     torch.cuda.synchronize()
+    peak = torch.cuda.max_memory_allocated() - base
     for a, b in ev:
         a.record()
         out = fn()
         b.record()
     torch.cuda.synchronize()
-    return min(a.elapsed_time(b) for a, b in ev), out
+    return min(a.elapsed_time(b) for a, b in ev), out, peak
+
+
+def _run(fn):
+    try:
+        t, out, peak = _time(fn)
+        return t, out.clone(), peak, None
+    except torch.OutOfMemoryError as e:
+        return None, None, None, "out of memory: " + str(e).splitlines()[0]
+    finally:
+        torch.cuda.empty_cache()
 
 
 def main():
@@ -177,25 +273,23 @@ def main():
             idconv.fill_uniform(x, synthgen.array_id(i), synthgen.SEED)
             if kind == "tconv2d":
                 x[0] = 0                                   # kx = -mx row
+        batched = kind == "cconv2d" and len(shape) == 3
+
+        def call(fn):   # the 2D complex functions are batched over leading axes
+            return lambda: fn(*arrs)
         explicit = {"cconv1d": cconv1d, "hconv1d": hconv1d, "tconv1d": tconv1d, "cconv2d": cconv2d,
                     "hconv2d": hconv2d, "tconv2d": tconv2d, "cconv3d": cconv3d, "hconv3d": hconv3d}[kind]
-        if kind == "cconv2d" and len(shape) == 3:
-            ex = lambda: explicit(arrs[0], arrs[1])    # batched over the leading axis
-        else:
-            ex = lambda: explicit(*arrs)
-        try:
-            t_ex, ref = _time(ex)
-            ref = ref.clone()
-            ex_err = None
-        except torch.OutOfMemoryError as e:
-            t_ex, ref, ex_err = None, None, "out of memory: " + str(e).splitlines()[0]
-        torch.cuda.empty_cache()
+        t_ex, ref, mem_ex, ex_err = _run(call(explicit))
+        t_pr = mem_pr = pr_err = None
+        diff_pr = None
+        if kind in PRUNED:
+            t_pr, out_pr, mem_pr, pr_err = _run(call(PRUNED[kind]))
+            if out_pr is not None and ref is not None:
+                diff_pr = float(torch.linalg.vector_norm(out_pr - ref) / torch.linalg.vector_norm(ref))
+            del out_pr
         pristine = [x.clone() for x in arrs]
-
-        def imp():
-            for x, p in zip(arrs, pristine):
-                x.copy_(p)
-            return getattr(idconv, kind)(*arrs)
+        ws = idconv.workspace_bytes(getattr(idconv, kind.upper()), *_sizes(kind, shape),
+                                    batch=shape[0] if batched else 1)
         # implicit timed without the restore copies
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         best = None
@@ -212,8 +306,13 @@ def main():
         diff = None
         if ref is not None:
             diff = float(torch.linalg.vector_norm(arrs[0] - ref) / torch.linalg.vector_norm(ref))
+        in_bytes = sum(x.numel() * 16 for x in arrs)
         row = dict(config=name, kind=kind, shape=list(shape), explicit_cufft_ms=t_ex, implicit_ms=best,
-                   speedup=(t_ex / best) if t_ex else None, rel_l2_implicit_vs_explicit=diff, error=ex_err)
+                   speedup=(t_ex / best) if t_ex else None, rel_l2_implicit_vs_explicit=diff, error=ex_err,
+                   pruned_cufft_ms=t_pr, speedup_vs_pruned=(t_pr / best) if t_pr else None,
+                   rel_l2_pruned_vs_explicit=diff_pr, pruned_error=pr_err,
+                   input_bytes=in_bytes, implicit_workspace_bytes=ws,
+                   explicit_extra_bytes=mem_ex, pruned_extra_bytes=mem_pr)
         print(json.dumps(row), flush=True)
         rows.append(row)
         del arrs, pristine, ref
@@ -221,6 +320,18 @@ def main():
     if a.out:
         with open(a.out, "w") as fh:
             json.dump(rows, fh, indent=1)
+
+
+def _sizes(kind, shape):
+    if kind in ("cconv1d", "hconv1d", "tconv1d"):
+        return (shape[-1],)
+    if kind == "cconv2d":
+        return tuple(shape[-2:])
+    if kind in ("hconv2d", "tconv2d"):
+        return ((shape[0] + 1) // 2, shape[1])
+    if kind == "cconv3d":
+        return tuple(shape)
+    return ((shape[0] + 1) // 2, (shape[1] + 1) // 2, shape[2])
 
 
 if __name__ == "__main__":
