@@ -19,7 +19,8 @@ for w in ["c2", "c1", "c3a", "c3b", "c4", "c4adv", "c4t", "c5a", "c5b", "ref"]:
     p = os.path.join(src, f"{tag}_bench_{w}.json")
     if os.path.exists(p):
         shutil.copy(p, os.path.join(dst, f"{tag}_bench_{w}.json"))
-for f in [f"{tag}_launches_c2.csv", f"{tag}_launches_c2_summary.txt", f"{tag}_smi.txt"]:
+for f in [f"{tag}_launches_c2.csv", f"{tag}_launches_c2_summary.txt", f"{tag}_smi.txt", f"{tag}_cufft_compare.json",
+          f"{tag}_pcie.json"]:
     if os.path.exists(os.path.join(src, f)):
         shutil.copy(os.path.join(src, f), os.path.join(dst, f))
 
@@ -75,4 +76,44 @@ with open(os.path.join(dst, f"{tag}_ncu_full_summary.md"), "w") as fh:
     fh.write("\n".join(lines) + "\n")
 with open(os.path.join(dst, "traffic.json"), "w") as fh:
     json.dump(traffic, fh, indent=1)
+
+# ---- 2D / 3D kernels (tools/prof_nd_full.sh <tag>nd) ----
+ND = [("c4_rows", "K3 hconv rows3<2048>, C4 (6143 rows, both x-streams)"),
+      ("c4_k7", "K7 fft0padBackward<2048>, C4 x pass"), ("c4_k8", "K8 fft0padForward<2048>, C4 x pass"),
+      ("c5a_k5x", "K5 fftpadBackward<512>, C5a x pass (all (y,z) columns)"),
+      ("c5a_rows", "K2 cconv rows2<512>, C5a first slab group"), ("c5b_k7x", "K7 fft0padBackward<512>, C5b x pass"),
+      ("c5b_rows", "K3 hconv rows3<512>, C5b first slab group")]
+nd = [f"# {tag}: ncu --set full captures of the dominant 2D / 3D kernels", "",
+      "Command: `tools/prof_nd_full.sh` (first launch of each kernel in one call of the config, `ncu --set full "
+      "--import-source on --clock-control none -k regex:<kernel> -c 1`, cold cache, replayed). Reports stay in "
+      "gpurun_out/ (too large to commit).", "",
+      "| kernel | time | DRAM read + write | DRAM GB/s | fp64 pipe | L1/shared | issue | warps | regs | local ld | "
+      "top stalls |", "|---|---|---|---|---|---|---|---|---|---|---|"]
+for short, label in ND:
+    rep = os.path.join(src, f"{tag}nd_{short}.ncu-rep")
+    if not os.path.exists(rep):
+        continue
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    h, units, v = rows[0], rows[1], rows[2]
+    sc = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "msecond": 1e-3, "usecond": 1e-6,
+          "nsecond": 1e-9, "us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1.0}
+    val = lambda k: float(v[h.index(k)].replace(",", "")) * sc.get(units[h.index(k)], 1.0)
+    raw = lambda k: float(v[h.index(k)].replace(",", ""))
+    dur, rd, wr = val("gpu__time_duration.sum"), val("dram__bytes_read.sum"), val("dram__bytes_write.sum")
+    stalls = [(h[i].replace("smsp__pcsamp_warps_issue_stalled_", ""), float(v[i].replace(",", "") or 0))
+              for i in range(len(h)) if h[i].startswith("smsp__pcsamp_warps_issue_stalled")
+              and not h[i].endswith("not_issued") and v[i].replace(",", "").replace(".", "").isdigit()]
+    tot = sum(b for a, b in stalls) or 1
+    stalls.sort(key=lambda x: -x[1])
+    nd.append(f"| {label} | {dur * 1e6:.1f} us | {rd / 1e6:.0f} + {wr / 1e6:.0f} MB | {(rd + wr) / dur / 1e9:.0f} | "
+              f"{raw('sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active'):.0f}% | "
+              f"{raw('l1tex__throughput.avg.pct_of_peak_sustained_active'):.0f}% | "
+              f"{raw('smsp__issue_active.avg.pct_of_peak_sustained_active'):.0f}% | "
+              f"{raw('sm__warps_active.avg.pct_of_peak_sustained_active'):.0f}% | "
+              f"{raw('launch__registers_per_thread'):.0f} | {raw('smsp__sass_inst_executed_op_local_ld.sum'):.0f} | "
+              + ", ".join(f"{a} {100 * b / tot:.0f}%" for a, b in stalls[:3]) + " |")
+if len(nd) > 6:
+    with open(os.path.join(dst, f"{tag}_ncu_nd_summary.md"), "w") as fh:
+        fh.write("\n".join(nd) + "\n")
 print("wrote", dst, sorted(os.listdir(dst)))
