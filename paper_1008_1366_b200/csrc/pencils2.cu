@@ -101,16 +101,46 @@ __device__ __forceinline__ void load_rows(const CUtensorMap* map, double2* stage
     tma_load_3d(stage + (long)b * W, map, (int)(2 * col0), row0 + b, (int)item, bar);
 }
 
+// Write a transformed N x W tile through the exchange buffer: park it as
+// [row][column] (the FFT's last exchange has completed), make it visible to
+// the async proxy, and let one thread issue the TMA stores (clipped at the
+// tensor's column bound for ragged tiles).  The caller waits for the stores'
+// shared-memory reads (bulk_wait_read) before xb is written again.
+template <int N, int E, int W, int BR>
+__device__ __forceinline__ void tile_store(const double2 (&v)[E], int t, int c, double2* xb, const CUtensorMap* map,
+                                           long col0, long item) {
+  constexpr int T = N / E;
+#pragma unroll
+  for (int i = 0; i < E; ++i) xb[(t + T * i) * W + c] = v[i];
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int r0 = 0; r0 < N; r0 += BR) tma_store_3d(map, (int)(2 * col0), r0, (int)item, xb + (long)r0 * W);
+    bulk_commit();
+  }
+}
+
 }  // namespace
+
+// K5 / K6: tiles of at most this many columns (16-32-byte row segments,
+// m >= 2048) leave through the exchange buffer by TMA stores (tconv2d
+// 2*2048 x 2048 1.674 -> 1.548 ms, cconv2d 4096 x 1024 0.553 -> 0.502 ms);
+// wider tiles store per thread (measured slower with TMA stores: 4 columns
+// 1.356 -> 1.384 ms on 16 x 1024^2, 8 columns cconv3d 22.05 -> 23.56 ms)
+#ifndef IDC_K56_TMA_STORE_MAXW
+#define IDC_K56_TMA_STORE_MAXW 2
+#endif
 
 // ------------------------------------------------------------------- K5 --
 template <int N>
 __global__ void __launch_bounds__(K56Cfg<N>::THREADS, IDC_PENCIL_MINB)
 k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mg, double2* __restrict__ f,
               double2* __restrict__ g, double2* __restrict__ U, double2* __restrict__ V, Tiles tl,
-              const double2* __restrict__ twN, const double2* __restrict__ tw2N, double2 ophase) {
+              const double2* __restrict__ twN, const double2* __restrict__ tw2N, double2 ophase,
+              const __grid_constant__ CUtensorMap mU, const __grid_constant__ CUtensorMap mV) {
   using C = K56Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
+  constexpr bool TS = W <= IDC_K56_TMA_STORE_MAXW;   // outputs by TMA stores
   extern __shared__ __align__(128) double2 smem[];
   double2* stage = smem;                       // N x W
   double2* xb = stage + N * W;
@@ -143,6 +173,7 @@ k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
     double2 x0[E], v[E];
 #pragma unroll
     for (int i = 0; i < E; ++i) x0[i] = stage[(t + T * i) * W + c];
+    if (TS && threadIdx.x == 0) bulk_wait_read();   // the last tile's output stores have read xb
     __syncthreads();
     const long nx = tau + gridDim.x;
     if (threadIdx.x == 0 && nx < tl.ntiles) {
@@ -155,19 +186,28 @@ k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
     // zeta_{2m}^k, k = t + T i: zeta_{2m}^t x zeta_{2E}^i (immediate)
     for_roots<2 * E, 1, +1, E>(cmul(ldtw(&tw2N[t]), ophase), [&](int i, double2 w) { v[i] = cmul(x0[i], w); });
     fft<N, E, +1>(v, t, xb, twN, CtaSync{}, xs);
-    const long rs = (long)T * tl.ncols;   // pointer step between a thread's rows
-    if (ok) {
-      double2* p = u + (long)t * tl.ncols;
+    if constexpr (TS) {
+      tile_store<N, E, W, BR>(v, t, c, xb, in == 0 ? &mU : &mV, col0, item);
+      if (threadIdx.x == 0) bulk_wait_read();
+      __syncthreads();
+      fft<N, E, +1>(x0, t, xb, twN, CtaSync{}, xs);   // even stream, in place
+      tile_store<N, E, W, BR>(x0, t, c, xb, in == 0 ? &mf : &mg, col0, item);
+    } else {
+      const long rs = (long)T * tl.ncols;   // pointer step between a thread's rows
+      if (ok) {
+        double2* p = u + (long)t * tl.ncols;
 #pragma unroll
-      for (int i = 0; i < E; ++i, p += rs) *p = v[i];
-    }
-    fft<N, E, +1>(x0, t, xb, twN, CtaSync{}, xs);   // even stream, in place
-    if (ok) {
-      double2* p = a + (long)t * tl.ncols;
+        for (int i = 0; i < E; ++i, p += rs) *p = v[i];
+      }
+      fft<N, E, +1>(x0, t, xb, twN, CtaSync{}, xs);   // even stream, in place
+      if (ok) {
+        double2* p = a + (long)t * tl.ncols;
 #pragma unroll
-      for (int i = 0; i < E; ++i, p += rs) *p = x0[i];
+        for (int i = 0; i < E; ++i, p += rs) *p = x0[i];
+      }
     }
   }
+  if (TS && threadIdx.x == 0) bulk_wait_all();
 }
 
 // ------------------------------------------------------------------- K6 --
@@ -177,6 +217,7 @@ k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
               Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw2N, double2 ophase) {
   using C = K56Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
+  constexpr bool TS = W <= IDC_K56_TMA_STORE_MAXW;   // output by TMA stores
   extern __shared__ __align__(128) double2 smem[];
   double2* sf = smem;
   double2* su = sf + N * W;
@@ -215,6 +256,7 @@ k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
     mbar_wait(&bars[1], phase);
 #pragma unroll
     for (int i = 0; i < E; ++i) v[i] = su[(t + T * i) * W + c];
+    if (TS && threadIdx.x == 0) bulk_wait_read();   // the last tile's output stores have read xb
     __syncthreads();
     if (threadIdx.x == 0 && nx < tl.ntiles) {
       mbar_arrive_expect_tx(&bars[1], BYTES);
@@ -232,13 +274,18 @@ k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
       load_rows<W, BR>(&mf, sf, c2, 0, N, item2, &bars[0]);
     }
     fft<N, E, -1>(v, t, xb, twN, CtaSync{}, xs);
-    if (ok) {
+    if constexpr (TS) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) v[i] = cscale(cadd(v[i], s[i]), inv);
+      tile_store<N, E, W, BR>(v, t, c, xb, &mf, col0, item);
+    } else if (ok) {
       double2* p = a + (long)t * tl.ncols;
       const long rs = (long)T * tl.ncols;
 #pragma unroll
       for (int i = 0; i < E; ++i, p += rs) *p = cscale(cadd(v[i], s[i]), inv);
     }
   }
+  if (TS && threadIdx.x == 0) bulk_wait_all();
 }
 
 // ------------------------------------------------------------------- K7 --
@@ -574,7 +621,10 @@ cudaError_t pad_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nco
   if (!encode_pencil_map(&mf, f, ncols, N, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
   if (!encode_pencil_map(&mg, g ? g : f, ncols, N, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
   Tiles tl = make_tiles<C::W>(ncols, batch, g ? 2 : 1, bstride, ustride);
-  void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw2N, &ophase};
+  CUtensorMap mU, mV;
+  if (!encode_pencil_map(&mU, U, ncols, N, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
+  if (!encode_pencil_map(&mV, g ? V : U, ncols, N, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
+  void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw2N, &ophase, &mU, &mV};
   const size_t smem = ((size_t)N * C::W + C::XB) * 16 + 16;
   return launch_t(k_pad_bwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
 }

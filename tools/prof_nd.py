@@ -9,10 +9,12 @@ ap.add_argument("shape")
 ap.add_argument("--reps", type=int, default=2)
 a = ap.parse_args()
 shape = tuple(int(x) for x in a.shape.split(","))
-f = torch.empty(shape, dtype=torch.complex128, device="cuda"); g = torch.empty_like(f)
-idconv.fill_uniform(f, 0, 1); idconv.fill_uniform(g, 1, 1)
+narr = 3 if a.kind == "tconv2d" else 2
+arrs = [torch.empty(shape, dtype=torch.complex128, device="cuda") for _ in range(narr)]
+for i, x in enumerate(arrs):
+    idconv.fill_uniform(x, i, 1)
 fn = getattr(idconv, a.kind)
 for r in range(a.reps):
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(); fn(f, g); e1.record(); torch.cuda.synchronize()
+    e0.record(); fn(*arrs); e1.record(); torch.cuda.synchronize()
     print(a.kind, shape, "%.3f ms" % e0.elapsed_time(e1))
