@@ -51,12 +51,13 @@ struct TCfg {
   static constexpr int XB = (xbuf_elems<N, E>() > 0 ? xbuf_elems<N, E>() : 1) * W;
 };
 
-// K5 / K6 (complex fftpad pencils): E = 16 with 256-thread CTAs at
-// m = 256 and 1024 (measured 3-5% faster on cconv2d 1024^2 and 64 x 256^2);
-// E = 8 with 512-thread CTAs at m = 512 (cconv3d 512^3 1.7% faster so) and
-// above 1024 (long columns need the threads for W >= 2).
+// K5 / K6 (complex fftpad pencils): E = 16 with 256-thread CTAs at m = 256
+// and m >= 1024 (measured 3-5% faster on cconv2d 1024^2 and 64 x 256^2;
+// 6-8% on tconv2d 2*2048 x 2048 and cconv2d 2048^2, 4096 x 1024: three
+// radix-16 passes instead of four radix-8 ones at the same tile width);
+// E = 8 with 512-thread CTAs at m = 512 (cconv3d 512^3 1.7% faster so).
 template <int N>
-constexpr bool k56_wide() { return N == 256 || N == 1024; }
+constexpr bool k56_wide() { return N == 256 || N >= 1024; }
 template <int N>
 using K56Cfg = TCfg<N, (k56_wide<N>() ? 256 : IDC_PENCIL_THREADS), (k56_wide<N>() ? 16 : IDC_PENCIL_E)>;
 
