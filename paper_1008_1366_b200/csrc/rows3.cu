@@ -34,6 +34,10 @@ struct Cfg3 {
   static constexpr int PER = 2 * M + XB;              // staged f, g + exchange buffer (double2)
   static constexpr size_t SMEM = (size_t)G * PER * 16 + (size_t)G * 16;  // + one mbarrier per group
   static constexpr bool NAMED = G > 1;
+#ifndef IDC_ROWS3_MINB_SMALL
+#define IDC_ROWS3_MINB_SMALL 1
+#endif
+  static constexpr int MINB = M <= 512 ? IDC_ROWS3_MINB_SMALL : 1;   // CTAs per SM (register cap)
 };
 
 template <bool NAMED>
@@ -67,7 +71,7 @@ __device__ __forceinline__ double2 zpair(const double2* F, const double2* Gs, in
 
 // ====================================================================== K3 ==
 template <int M>
-__global__ void __launch_bounds__(Cfg3<M>::THREADS, 1)
+__global__ void __launch_bounds__(Cfg3<M>::THREADS, Cfg3<M>::MINB)
 k_hconv_rows3(double2* __restrict__ f, double2* __restrict__ g, long nrows, const double2* __restrict__ twM,
               const double2* __restrict__ tw3M, RowSets rs) {
   using C = Cfg3<M>;
@@ -158,7 +162,7 @@ k_hconv_rows3(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
 
 // ====================================================================== K4 ==
 template <int M>
-__global__ void __launch_bounds__(Cfg3<M>::THREADS, 1)
+__global__ void __launch_bounds__(Cfg3<M>::THREADS, Cfg3<M>::MINB)
 k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const double2* __restrict__ h, long nrows,
               const double2* __restrict__ twM, const double2* __restrict__ tw4M) {
   using C = Cfg3<M>;
@@ -299,7 +303,10 @@ cudaError_t launch3(K kernel, int threads, size_t smem, long nrows, int groups, 
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   long need = (nrows + groups - 1) / groups;
-  long grid = num_sms();
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  if (per_sm < 1) per_sm = 1;
+  long grid = (long)num_sms() * per_sm;
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
   count_launch();
