@@ -178,3 +178,39 @@ def test_config5b_hconv3d_512(idc):
     del F, G
     torch.cuda.empty_cache()
     assert rel_l2(out, direct.hconv3d_at_large(f, g, idx)) < TOL
+
+
+# ------------------------------------------------ tall pencils (m >= 1024) --
+# x axes of 1024-4096 points run the pencil kernels with 1-4-column tiles
+# whose outputs leave by TMA tensor stores; a few columns (fewer than a
+# tile: clipped stores) and batches (3D tensor maps) element by element.
+
+@pytest.mark.parametrize("mx,my,B", [(2048, 1, 1), (2048, 2, 2), (4096, 2, 1), (4096, 8, 1), (1024, 2, 3)])
+def test_cconv2d_tall(idc, mx, my, B):
+    f, g = synthgen.cconv2d_inputs(mx, my, B)
+    ref = np.stack([direct.cconv2d(f[b], g[b]) for b in range(B)])
+    F, G = dev(f), dev(g)
+    idc.cconv2d(F, G)
+    assert rel_l2(F.cpu().numpy(), ref) < TOL
+
+
+@pytest.mark.parametrize("mx,my", [(1024, 1), (1024, 2), (2048, 1), (2048, 4), (4096, 2)])
+def test_hconv2d_tall(idc, mx, my):
+    f, g = synthgen.hconv2d_inputs(mx, my)
+    ref = direct.hconv2d(f, g)
+    F, G = dev(f), dev(g)
+    idc.hconv2d(F, G)
+    assert rel_l2(F.cpu().numpy(), ref) < TOL
+
+
+@pytest.mark.parametrize("mx,my", [(2048, 2), (1024, 4), (512, 1)])
+def test_tconv2d_tall(idc, mx, my):
+    from oracle import ternary2d
+    arrs = []
+    for r in range(3):
+        a = synthgen.hconv2d_inputs(mx, my, roles=(r,))[0]
+        arrs.append(np.concatenate([np.zeros((1, my), dtype=np.complex128), a], axis=0))
+    ref = ternary2d.direct(*arrs)
+    F, G, H = (dev(a) for a in arrs)
+    idc.tconv2d(F, G, H)
+    assert rel_l2(F.cpu().numpy(), ref) < TOL
