@@ -61,11 +61,15 @@ constexpr bool k56_wide() { return N == 256 || N >= 1024; }
 template <int N>
 using K56Cfg = TCfg<N, (k56_wide<N>() ? 256 : IDC_PENCIL_THREADS), (k56_wide<N>() ? 16 : IDC_PENCIL_E)>;
 
-// K7 / K8 (centered fft0pad pencils): E = 16 with 256-thread CTAs (255
-// registers, three radix-16 passes) for 256 <= m <= 2048 -- measured
-// hconv2d 2048^2 -5%, hconv3d 512^3 -1.5% against E = 8 / 512 threads.
+// K7 / K8 (centered fft0pad pencils): E = 16 with 256-thread CTAs (three
+// radix-16 passes) for 256 <= m <= 4096 -- measured hconv2d 2048^2 -5%,
+// hconv3d 512^3 -1.5%, hconv2d 8191 x 512 (m = 4096) -6% against E = 8 /
+// 512 threads.
+#ifndef IDC_K78_WIDE_MAX
+#define IDC_K78_WIDE_MAX 4096
+#endif
 template <int N>
-constexpr bool k78_wide() { return N >= 256 && N <= 2048; }
+constexpr bool k78_wide() { return N >= 256 && N <= IDC_K78_WIDE_MAX; }
 template <int N>
 using K78Cfg = TCfg<N, (k78_wide<N>() ? 256 : IDC_PENCIL0_THREADS), (k78_wide<N>() ? 16 : IDC_PENCIL_E)>;
 
