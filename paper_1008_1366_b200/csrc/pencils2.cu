@@ -65,13 +65,26 @@ using K56Cfg = TCfg<N, (k56_wide<N>() ? 256 : IDC_PENCIL_THREADS), (k56_wide<N>(
 // radix-16 passes) for 256 <= m <= 4096 -- measured hconv2d 2048^2 -5%,
 // hconv3d 512^3 -1.5%, hconv2d 8191 x 512 (m = 4096) -6% against E = 8 /
 // 512 threads.
+// 128-thread CTAs (half-width tiles, two CTAs per SM) for m in
+// [IDC_K78_NARROW_MIN, IDC_K78_NARROW_MAX]: at m = 1024 (2-column tiles)
+// hconv2d 2047 x 2048 0.332 -> 0.320 ms; at m = 512 (4-column tiles)
+// hconv3d 59.5 -> 70.8 ms, at m = 2048 (1-column tiles) hconv2d 4095 x
+// 2048 0.61 -> 0.80 ms -- the DRAM row segment width decides
+#ifndef IDC_K78_NARROW_MIN
+#define IDC_K78_NARROW_MIN 1024
+#endif
+#ifndef IDC_K78_NARROW_MAX
+#define IDC_K78_NARROW_MAX 1024
+#endif
 #ifndef IDC_K78_WIDE_MAX
 #define IDC_K78_WIDE_MAX 4096
 #endif
 template <int N>
 constexpr bool k78_wide() { return N >= 256 && N <= IDC_K78_WIDE_MAX; }
 template <int N>
-using K78Cfg = TCfg<N, (k78_wide<N>() ? 256 : IDC_PENCIL0_THREADS), (k78_wide<N>() ? 16 : IDC_PENCIL_E)>;
+using K78Cfg = TCfg<N, (k78_wide<N>() ? (N >= IDC_K78_NARROW_MIN && N <= IDC_K78_NARROW_MAX ? 128 : 256)
+                                      : IDC_PENCIL0_THREADS),
+                   (k78_wide<N>() ? 16 : IDC_PENCIL_E)>;
 
 template <int W>
 struct Slot2 {
