@@ -221,9 +221,12 @@ IDC_API idc_status idc_hconv3d_dist_emulated(int nranks, idc_c128** f_slabs, idc
 /* Batched 1D convolution (k = IDC_CCONV1D, IDC_HCONV1D or IDC_TCONV1D) on
  * HOST arrays: in_host[0..1] (f, g) or [0..2] (f, g, h), each batch x m,
  * out_host <- the result (may alias in_host[0]; inputs otherwise unchanged).
- * Rows are streamed through the device in chunks of chunk_rows on an internal
- * pool of streams: the copy of chunk c+1 in, the fused row kernel of chunk c
- * and the copy of chunk c-1 out overlap.  Host memory should be page-locked
+ * Rows are streamed through the device in chunks of at most chunk_rows on an
+ * internal pool of streams: the copy of chunk c+1 in, the fused row kernel of
+ * chunk c and the copy of chunk c-1 out overlap.  Chunks ramp up (chunk/8,
+ * chunk/4, chunk/2 rows, then chunk_rows) and the last 2*chunk_rows rows are
+ * cut into halving pieces (not below chunk/8) to shorten the pipeline's
+ * unoverlapped fill and drain; one kernel launch per chunk.  Host memory should be page-locked
  * (cudaHostAlloc / torch pin_memory) for the copies to be asynchronous.
  * work: DEVICE workspace of idc_host_workspace_bytes(k, m, chunk_rows),
  * 256-byte aligned.  Ordered after prior work on `stream`; `stream` waits for

@@ -51,6 +51,25 @@ size_t row_work(idc_kind k, int m) {
 
 size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
+// Rows of the next chunk.  The pipeline's first host->device copy and last
+// device->host copy overlap nothing, so chunks ramp up from chunk/8 rows
+// (doubling) and the last 2*chunk rows are cut into halving pieces (down to
+// chunk/8): the exposed fill and drain shrink to about 1/8 of a chunk each.
+size_t next_chunk(size_t done, size_t batch, size_t chunk, size_t index) {
+  const size_t rem = batch - done;
+  const size_t small = chunk / 8 > 0 ? chunk / 8 : 1;
+  size_t c = chunk;
+  if (index < 3) c = small << index;                      // chunk/8, chunk/4, chunk/2, then chunk
+  if (c > chunk) c = chunk;
+  if (rem < 2 * chunk) {
+    const size_t half = (rem + 1) / 2;
+    if (half < c) c = half;
+  }
+  if (c < small) c = small;
+  if (c > rem) c = rem;
+  return c;
+}
+
 }  // namespace
 
 extern "C" {
@@ -82,8 +101,8 @@ idc_status idc_conv1d_host(idc_kind k, const idc_c128* const* in_host, idc_c128*
   for (int i = 0; i < kSlots; ++i)
     if (cudaStreamWaitEvent(P.s[i], P.fork, 0) != cudaSuccess) return IDC_ERR_CUDA;
   size_t c = 0;
-  for (size_t r0 = 0; r0 < batch; r0 += chunk_rows, ++c) {
-    const size_t rows = batch - r0 < chunk_rows ? batch - r0 : chunk_rows;
+  for (size_t r0 = 0, rows = 0; r0 < batch; r0 += rows, ++c) {
+    rows = next_chunk(r0, batch, chunk_rows, c);
     const int slot = (int)(c % kSlots);
     cudaStream_t st = P.s[slot];
     char* base = static_cast<char*>(work) + slot * per_slot;

@@ -154,8 +154,9 @@ def _need_cuda(arrs):
         raise ValueError("this call takes CUDA tensors (no host or CPU path)")
 
 
-# rows per chunk of the host-buffer 1D path: ~16 MB per array (IDC_HOST_CHUNK_MB overrides)
-HOST_CHUNK_BYTES = int(float(os.environ.get("IDC_HOST_CHUNK_MB", "16")) * (1 << 20))
+# rows per chunk of the host-buffer 1D path: ~64 MB per array (IDC_HOST_CHUNK_MB overrides;
+# tools/e2e_sweep.sh: with the ramped chunk schedule 64 MB beat 16 / 32 / 128 MB)
+HOST_CHUNK_BYTES = int(float(os.environ.get("IDC_HOST_CHUNK_MB", "64")) * (1 << 20))
 
 
 def _run_host_1d(arrs, kind, m, batch, stream):
