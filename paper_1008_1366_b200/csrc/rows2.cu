@@ -32,6 +32,14 @@ struct Cfg2 {
 #ifndef IDC_ROWS_REGS
 #define IDC_ROWS_REGS 255
 #endif
+// K2 up to this m: f and g rows staged in shared memory by bulk copies
+// (mbarrier), the next row's copies issued as soon as the current row's last
+// split has read the stage; above it the rows are read from global memory
+// after an L2 prefetch.  Measured: m = 512 0.66 -> 0.63 ms (cconv3d 512^3
+// 22.0 -> 21.55 ms), m = 64 -3%, m = 1024 +2-5% (so kept off there).
+#ifndef IDC_ROWS2_TMA_MAX
+#define IDC_ROWS2_TMA_MAX 512
+#endif
   static constexpr int MINB = (65536 / (THREADS * IDC_ROWS_REGS)) < 1 ? 1 : 65536 / (THREADS * IDC_ROWS_REGS);
 };
 
@@ -60,6 +68,14 @@ __device__ __forceinline__ double2 herm_pair2(double2 fk, double2 gk, double2 fm
   return cmul(zr, cadd(P, cmul(c, R)));
 }
 
+// K2 row reads: the shared-memory stage (plain loads; the FFT barriers'
+// memory clobbers already force the re-reads) or global memory (ldv)
+template <bool ST>
+__device__ __forceinline__ double2 ldrow(const double2* p) {
+  if constexpr (ST) return *p;
+  else return ldv(p);
+}
+
 }  // namespace
 
 // ====================================================================== K2 ==
@@ -73,7 +89,29 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
   extern __shared__ __align__(16) double2 smem[];
   const int grp = threadIdx.x / T, t = threadIdx.x - grp * T;
   constexpr bool FFT2 = E <= 8;
-  double2* xb = smem + grp * (FFT2 ? 2 : 1) * C::XB;   // one exchange buffer per vector in flight
+  // ST: per group the staged f and g rows, then the exchange buffer(s); the
+  // groups' mbarriers after all groups.  Otherwise exchange buffers only.
+  constexpr bool ST = M <= IDC_ROWS2_TMA_MAX;
+  constexpr int PER = (ST ? 2 * M : 0) + (FFT2 ? 2 : 1) * C::XB;
+  double2* Fs = smem + grp * PER;
+  double2* Gs = Fs + M;
+  double2* xb = ST ? Gs + M : Fs;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G * PER) + grp;
+  const long step = (long)gridDim.x * G;
+  auto issue = [&](long r) {   // bulk copies of row r's f and g into the stage
+    mbar_arrive_expect_tx(bar, 2u * M * 16u);
+    tma_load_1d(Fs, row_ptr(f, rs.f1, rs.n0, r, M), M * 16u, bar);
+    tma_load_1d(Gs, row_ptr(g, rs.g1, rs.n0, r, M), M * 16u, bar);
+  };
+  if constexpr (ST) {
+    if (t == 0) {
+      mbar_init(bar, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (t == 0 && (long)blockIdx.x * G + grp < nrows) issue((long)blockIdx.x * G + grp);
+  }
+  uint32_t phase = 0;
   double2* xb2 = xb + C::XB;
   const auto sync = row_sync<M, E, G>(grp);
   const double inv = 1.0 / (2.0 * M);
@@ -83,14 +121,27 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
       if (row >= nrows) break;
     }
     const bool ok = row < nrows;
-    double2* fr = row_ptr(f, rs.f1, rs.n0, ok ? row : 0, M);
-    const double2* gr = row_ptr(g, rs.g1, rs.n0, ok ? row : 0, M);
-    // the next rows of this group: bulk prefetch into L2 (hides the HBM
-    // latency of the first loads of the next iteration)
-    if (IDC_ROWS_PREFETCH && t == 0 && row + (long)gridDim.x * G < nrows) {
-      prefetch_l2(row_ptr(f, rs.f1, rs.n0, row + (long)gridDim.x * G, M), M * 16u);
-      prefetch_l2(row_ptr(g, rs.g1, rs.n0, row + (long)gridDim.x * G, M), M * 16u);
+    double2* fo = row_ptr(f, rs.f1, rs.n0, ok ? row : 0, M);   // output row
+    const double2* fr = ST ? Fs : fo;                             // row reads: stage or global
+    const double2* gr = ST ? Gs : row_ptr(g, rs.g1, rs.n0, ok ? row : 0, M);
+    if constexpr (ST) {
+      if (ok) {
+        mbar_wait(bar, phase);
+        phase ^= 1;
+      }
+    } else if (IDC_ROWS_PREFETCH && t == 0 && row + step < nrows) {
+      // the next rows of this group: bulk prefetch into L2 (hides the HBM
+      // latency of the first loads of the next iteration)
+      prefetch_l2(row_ptr(f, rs.f1, rs.n0, row + step, M), M * 16u);
+      prefetch_l2(row_ptr(g, rs.g1, rs.n0, row + step, M), M * 16u);
     }
+    // after the last read of the staged rows (the r = 1 split): next row's copies
+    auto refill = [&]() {
+      if constexpr (ST) {
+        sync();
+        if (t == 0 && row + step < nrows) issue(row + step);
+      }
+    };
     // Every intermediate in registers (at most three E-vectors live): no
     // shared-memory stash traffic, only the FFT exchanges.  With E = 8 the
     // independent transforms run pairwise in lockstep (fft2: one barrier pair
@@ -100,33 +151,35 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
     double2 zt;   // zeta_{2m}^t; zeta_{2m}^k = zeta_{2m}^t zeta_{2E}^i (immediate), k = t + T i
     if constexpr (FFT2) {
 #pragma unroll
-      for (int i = 0; i < E; ++i) x[i] = ldv(&fr[t + T * i]);
+      for (int i = 0; i < E; ++i) x[i] = ldrow<ST>(&fr[t + T * i]);
 #pragma unroll
-      for (int i = 0; i < E; ++i) y[i] = ldv(&gr[t + T * i]);
+      for (int i = 0; i < E; ++i) y[i] = ldrow<ST>(&gr[t + T * i]);
       fft2<M, E, +1>(x, y, t, xb, xb2, twM, sync);                        // r = 0
 #pragma unroll
       for (int i = 0; i < E; ++i) x[i] = cmul(x[i], y[i]);
       // r = 1: zeta_{2m}^k-shifted streams
       zt = ldtw(&tw2M[t]);
-      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { y[i] = cmul(ldv(&fr[t + T * i]), w); });
-      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { z[i] = cmul(ldv(&gr[t + T * i]), w); });
+      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { y[i] = cmul(ldrow<ST>(&fr[t + T * i]), w); });
+      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { z[i] = cmul(ldrow<ST>(&gr[t + T * i]), w); });
+      refill();
       fft2<M, E, +1>(y, z, t, xb, xb2, twM, sync);
 #pragma unroll
       for (int i = 0; i < E; ++i) y[i] = cmul(y[i], z[i]);
       fft2<M, E, -1>(x, y, t, xb, xb2, twM, sync);                        // forward
     } else {
 #pragma unroll
-      for (int i = 0; i < E; ++i) x[i] = ldv(&fr[t + T * i]);
+      for (int i = 0; i < E; ++i) x[i] = ldrow<ST>(&fr[t + T * i]);
       fft<M, E, +1>(x, t, xb, twM, sync);                                 // r = 0
 #pragma unroll
-      for (int i = 0; i < E; ++i) y[i] = ldv(&gr[t + T * i]);
+      for (int i = 0; i < E; ++i) y[i] = ldrow<ST>(&gr[t + T * i]);
       fft<M, E, +1>(y, t, xb, twM, sync);
 #pragma unroll
       for (int i = 0; i < E; ++i) x[i] = cmul(x[i], y[i]);
       zt = ldtw(&tw2M[t]);
-      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { y[i] = cmul(ldv(&fr[t + T * i]), w); });
+      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { y[i] = cmul(ldrow<ST>(&fr[t + T * i]), w); });
       fft<M, E, +1>(y, t, xb, twM, sync);                                 // r = 1
-      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { z[i] = cmul(ldv(&gr[t + T * i]), w); });
+      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { z[i] = cmul(ldrow<ST>(&gr[t + T * i]), w); });
+      refill();
       fft<M, E, +1>(z, t, xb, twM, sync);
 #pragma unroll
       for (int i = 0; i < E; ++i) y[i] = cmul(y[i], z[i]);
@@ -135,7 +188,7 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
     }
     // recombination and 1/(2m)
     if (ok) {
-      double2* fw = fr;
+      double2* fw = fo;
       for_roots<2 * E, 1, -1, E>(cconj(zt), [&](int i, double2 w) {       // zeta_{2m}^{-k}
         fw[t + T * i] = cscale(cadd(x[i], cmul(y[i], w)), inv);
       });
@@ -359,8 +412,9 @@ cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s, RowS
   const double2* tw2M = zeta_table(2 * M);
   if (!twM || !tw2M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw2M, &rs};
-  const size_t per = (E <= 8 ? 2 : 1) * C::XB;   // exchange buffer(s) only (intermediates in registers)
-  return launch2(k_cconv_rows2<M, E, G>, C::THREADS, (size_t)G * per * 16, nrows, G, s, args);
+  // staged f, g rows (m <= IDC_ROWS2_TMA_MAX) + exchange buffer(s) + mbarriers
+  const size_t per = (M <= IDC_ROWS2_TMA_MAX ? 2 * M : 0) + (E <= 8 ? 2 : 1) * C::XB;
+  return launch2(k_cconv_rows2<M, E, G>, C::THREADS, (size_t)G * per * 16 + (size_t)G * 8, nrows, G, s, args);
 }
 
 template <int M>
