@@ -37,6 +37,12 @@ struct Cfg2 {
 // split has read the stage; above it the rows are read from global memory
 // after an L2 prefetch.  Measured: m = 512 0.66 -> 0.63 ms (cconv3d 512^3
 // 22.0 -> 21.55 ms), m = 64 -3%, m = 1024 +2-5% (so kept off there).
+// K2 with E = 16 from this m up: park the r = 0 result in shared memory
+// instead of keeping it in registers across the r = 1 transforms (removes
+// the spills: m = 4096 1.064 -> 0.983 ms; m = 1024 neutral, m = 2048 +2.5%)
+#ifndef IDC_K2_PARK_MIN
+#define IDC_K2_PARK_MIN 4096
+#endif
 #ifndef IDC_ROWS2_TMA_MAX
 #define IDC_ROWS2_TMA_MAX 512
 #endif
@@ -92,10 +98,12 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
   // ST: per group the staged f and g rows, then the exchange buffer(s); the
   // groups' mbarriers after all groups.  Otherwise exchange buffers only.
   constexpr bool ST = M <= IDC_ROWS2_TMA_MAX;
-  constexpr int PER = (ST ? 2 * M : 0) + (FFT2 ? 2 : 1) * C::XB;
+  constexpr bool PARK = !FFT2 && M >= IDC_K2_PARK_MIN;   // r = 0 result parked in shared memory
+  constexpr int PER = (ST ? 2 * M : 0) + (FFT2 ? 2 : 1) * C::XB + (PARK ? M : 0);
   double2* Fs = smem + grp * PER;
   double2* Gs = Fs + M;
   double2* xb = ST ? Gs + M : Fs;
+  double2* pk = xb + C::XB;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G * PER) + grp;
   const long step = (long)gridDim.x * G;
   auto issue = [&](long r) {   // bulk copies of row r's f and g into the stage
@@ -166,6 +174,32 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
 #pragma unroll
       for (int i = 0; i < E; ++i) y[i] = cmul(y[i], z[i]);
       fft2<M, E, -1>(x, y, t, xb, xb2, twM, sync);                        // forward
+    } else if constexpr (PARK) {
+      // r = 0 stream all the way back first, parked in this thread's own
+      // shared-memory slots while the r = 1 stream is transformed: two
+      // E-vectors live instead of three
+#pragma unroll
+      for (int i = 0; i < E; ++i) x[i] = ldrow<ST>(&fr[t + T * i]);
+      fft<M, E, +1>(x, t, xb, twM, sync);                                 // r = 0
+#pragma unroll
+      for (int i = 0; i < E; ++i) y[i] = ldrow<ST>(&gr[t + T * i]);
+      fft<M, E, +1>(y, t, xb, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) x[i] = cmul(x[i], y[i]);
+      fft<M, E, -1>(x, t, xb, twM, sync);                                 // forward
+#pragma unroll
+      for (int i = 0; i < E; ++i) pk[t + T * i] = x[i];
+      zt = ldtw(&tw2M[t]);
+      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { y[i] = cmul(ldrow<ST>(&fr[t + T * i]), w); });
+      fft<M, E, +1>(y, t, xb, twM, sync);                                 // r = 1
+      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { x[i] = cmul(ldrow<ST>(&gr[t + T * i]), w); });
+      refill();
+      fft<M, E, +1>(x, t, xb, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) y[i] = cmul(y[i], x[i]);
+      fft<M, E, -1>(y, t, xb, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) x[i] = pk[t + T * i];
     } else {
 #pragma unroll
       for (int i = 0; i < E; ++i) x[i] = ldrow<ST>(&fr[t + T * i]);
@@ -413,7 +447,7 @@ cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s, RowS
   if (!twM || !tw2M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw2M, &rs};
   // staged f, g rows (m <= IDC_ROWS2_TMA_MAX) + exchange buffer(s) + mbarriers
-  const size_t per = (M <= IDC_ROWS2_TMA_MAX ? 2 * M : 0) + (E <= 8 ? 2 : 1) * C::XB;
+  const size_t per = (M <= IDC_ROWS2_TMA_MAX ? 2 * M : 0) + (E <= 8 ? 2 : 1) * C::XB + (E > 8 && M >= IDC_K2_PARK_MIN ? M : 0);
   return launch2(k_cconv_rows2<M, E, G>, C::THREADS, (size_t)G * per * 16 + (size_t)G * 8, nrows, G, s, args);
 }
 
