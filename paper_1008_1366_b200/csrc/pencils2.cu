@@ -56,10 +56,21 @@ struct TCfg {
 // 6-8% on tconv2d 2*2048 x 2048 and cconv2d 2048^2, 4096 x 1024: three
 // radix-16 passes instead of four radix-8 ones at the same tile width);
 // E = 8 with 512-thread CTAs at m = 512 (cconv3d 512^3 1.7% faster so).
+// 128-thread CTAs (half-width tiles, several CTAs per SM) for m in
+// [IDC_K56_NARROW_MIN, IDC_K56_NARROW_MAX] (E = 16 sizes only): measured
+// 64 x 256^2 -1.5%, 1024 x 4096 -3.5%, 16 x 1024^2 -2%
+#ifndef IDC_K56_NARROW_MIN
+#define IDC_K56_NARROW_MIN 256
+#endif
+#ifndef IDC_K56_NARROW_MAX
+#define IDC_K56_NARROW_MAX 1024
+#endif
 template <int N>
 constexpr bool k56_wide() { return N == 256 || N >= 1024; }
 template <int N>
-using K56Cfg = TCfg<N, (k56_wide<N>() ? 256 : IDC_PENCIL_THREADS), (k56_wide<N>() ? 16 : IDC_PENCIL_E)>;
+using K56Cfg = TCfg<N, (k56_wide<N>() ? (N >= IDC_K56_NARROW_MIN && N <= IDC_K56_NARROW_MAX ? 128 : 256)
+                                      : IDC_PENCIL_THREADS),
+                   (k56_wide<N>() ? 16 : IDC_PENCIL_E)>;
 
 // K7 / K8 (centered fft0pad pencils): E = 16 with 256-thread CTAs (three
 // radix-16 passes) for 256 <= m <= 4096 -- measured hconv2d 2048^2 -5%,
