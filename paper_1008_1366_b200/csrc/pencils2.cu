@@ -87,11 +87,14 @@ using K56Cfg = TCfg<N, (k56_wide<N>() ? (N >= IDC_K56_NARROW_MIN && N <= IDC_K56
 #ifndef IDC_K78_NARROW_MAX
 #define IDC_K78_NARROW_MAX 1024
 #endif
+#ifndef IDC_K78_WIDE_MIN
+#define IDC_K78_WIDE_MIN 256
+#endif
 #ifndef IDC_K78_WIDE_MAX
 #define IDC_K78_WIDE_MAX 4096
 #endif
 template <int N>
-constexpr bool k78_wide() { return N >= 256 && N <= IDC_K78_WIDE_MAX; }
+constexpr bool k78_wide() { return N >= IDC_K78_WIDE_MIN && N <= IDC_K78_WIDE_MAX; }
 template <int N>
 using K78Cfg = TCfg<N, (k78_wide<N>() ? (N >= IDC_K78_NARROW_MIN && N <= IDC_K78_NARROW_MAX ? 128 : 256)
                                       : IDC_PENCIL0_THREADS),
