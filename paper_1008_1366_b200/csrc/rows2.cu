@@ -447,7 +447,9 @@ cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s, RowS
   if (!twM || !tw2M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw2M, &rs};
   // staged f, g rows (m <= IDC_ROWS2_TMA_MAX) + exchange buffer(s) + mbarriers
-  const size_t per = (M <= IDC_ROWS2_TMA_MAX ? 2 * M : 0) + (E <= 8 ? 2 : 1) * C::XB + (E > 8 && M >= IDC_K2_PARK_MIN ? M : 0);
+  constexpr size_t per = (M <= IDC_ROWS2_TMA_MAX ? 2 * M : 0) + (E <= 8 ? 2 : 1) * C::XB +
+                         (E > 8 && M >= IDC_K2_PARK_MIN ? M : 0);
+  static_assert((size_t)G * per * 16 + (size_t)G * 8 <= 227 * 1024, "K2 configuration exceeds shared memory");
   return launch2(k_cconv_rows2<M, E, G>, C::THREADS, (size_t)G * per * 16 + (size_t)G * 8, nrows, G, s, args);
 }
 
