@@ -140,11 +140,12 @@ __device__ __forceinline__ void load_rows(const CUtensorMap* map, double2* stage
 // shared-memory reads (bulk_wait_read) before xb is written again.
 template <int N, int E, int W, int BR>
 __device__ __forceinline__ void tile_store(const double2 (&v)[E], int t, int c, double2* xb, const CUtensorMap* map,
-                                           long col0, long item) {
+                                           long col0, long item, bool drain_first = false) {
   constexpr int T = N / E;
 #pragma unroll
   for (int i = 0; i < E; ++i) xb[(t + T * i) * W + c] = v[i];
   fence_proxy_async_smem();
+  if (drain_first && threadIdx.x == 0) bulk_wait_read();   // earlier stores (other buffer) done reading
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int r0 = 0; r0 < N; r0 += BR) tma_store_3d(map, (int)(2 * col0), r0, (int)item, xb + (long)r0 * W);
@@ -163,6 +164,18 @@ __device__ __forceinline__ void tile_store(const double2 (&v)[E], int t, int c, 
 #define IDC_K56_TMA_STORE_MAXW 2
 #endif
 
+// K5 with TMA-stored outputs: a second exchange buffer where it fits, so the
+// odd stream's store drains while the even stream transforms
+#ifndef IDC_K5_DOUBLE_XB
+#define IDC_K5_DOUBLE_XB 1
+#endif
+template <int N>
+constexpr bool k5_double_xb() {
+  using C = K56Cfg<N>;
+  return IDC_K5_DOUBLE_XB && C::W <= IDC_K56_TMA_STORE_MAXW &&
+         ((size_t)N * C::W + 2 * (size_t)C::XB) * 16 + 16 <= 227 * 1024;
+}
+
 // ------------------------------------------------------------------- K5 --
 template <int N>
 __global__ void __launch_bounds__(K56Cfg<N>::THREADS, IDC_PENCIL_MINB)
@@ -173,10 +186,12 @@ k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
   using C = K56Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   constexpr bool TS = W <= IDC_K56_TMA_STORE_MAXW;   // outputs by TMA stores
+  constexpr bool DB = k5_double_xb<N>();              // second exchange buffer for the even stream
   extern __shared__ __align__(128) double2 smem[];
   double2* stage = smem;                       // N x W
   double2* xb = stage + N * W;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(xb + C::XB);
+  double2* xb1 = DB ? xb + C::XB : xb;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(xb1 + C::XB);
   const int c = threadIdx.x % W, t = threadIdx.x / W;
   const Slot2<W> xs{c};
   constexpr uint32_t BYTES = (uint32_t)N * W * 16;
@@ -205,7 +220,10 @@ k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
     double2 x0[E], v[E];
 #pragma unroll
     for (int i = 0; i < E; ++i) x0[i] = stage[(t + T * i) * W + c];
-    if (TS && threadIdx.x == 0) bulk_wait_read();   // the last tile's output stores have read xb
+    if (TS && threadIdx.x == 0) {   // the last tile's odd-stream store has read xb
+      if constexpr (DB) bulk_wait_read_but1();
+      else bulk_wait_read();
+    }
     __syncthreads();
     const long nx = tau + gridDim.x;
     if (threadIdx.x == 0 && nx < tl.ntiles) {
@@ -219,11 +237,18 @@ k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
     for_roots<2 * E, 1, +1, E>(cmul(ldtw(&tw2N[t]), ophase), [&](int i, double2 w) { v[i] = cmul(x0[i], w); });
     fft<N, E, +1>(v, t, xb, twN, CtaSync{}, xs);
     if constexpr (TS) {
-      tile_store<N, E, W, BR>(v, t, c, xb, in == 0 ? &mU : &mV, col0, item);
-      if (threadIdx.x == 0) bulk_wait_read();
-      __syncthreads();
-      fft<N, E, +1>(x0, t, xb, twN, CtaSync{}, xs);   // even stream, in place
-      tile_store<N, E, W, BR>(x0, t, c, xb, in == 0 ? &mf : &mg, col0, item);
+      if constexpr (DB) {
+        // odd stream out of xb while the even stream transforms in xb1; the
+        // wait for xb1's previous store (a whole transform ago) rides on the
+        // store's barrier
+        tile_store<N, E, W, BR>(v, t, c, xb, in == 0 ? &mU : &mV, col0, item, true);
+      } else {
+        tile_store<N, E, W, BR>(v, t, c, xb, in == 0 ? &mU : &mV, col0, item);
+        if (threadIdx.x == 0) bulk_wait_read();
+        __syncthreads();
+      }
+      fft<N, E, +1>(x0, t, xb1, twN, CtaSync{}, xs);   // even stream, in place
+      tile_store<N, E, W, BR>(x0, t, c, xb1, in == 0 ? &mf : &mg, col0, item);
     } else {
       const long rs = (long)T * tl.ncols;   // pointer step between a thread's rows
       if (ok) {
@@ -657,7 +682,7 @@ cudaError_t pad_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nco
   if (!encode_pencil_map(&mU, U, ncols, N, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
   if (!encode_pencil_map(&mV, g ? V : U, ncols, N, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
   void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw2N, &ophase, &mU, &mV};
-  const size_t smem = ((size_t)N * C::W + C::XB) * 16 + 16;
+  const size_t smem = ((size_t)N * C::W + (k5_double_xb<N>() ? 2 : 1) * (size_t)C::XB) * 16 + 16;
   return launch_t(k_pad_bwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
 }
 

@@ -12,7 +12,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
 src = os.path.join(ROOT, "gpurun_out")
-dst = os.path.join(ROOT, "profiles")
+dst = os.environ.get("PROFILES_OUT", os.path.join(ROOT, "profiles"))   # run on the GPU box: a gpurun_out/ subdir
 os.makedirs(dst, exist_ok=True)
 
 for w in ["c2", "c1", "c3a", "c3b", "c4", "c4adv", "c4t", "c5a", "c5b", "ref"]:
@@ -82,7 +82,9 @@ ND = [("c4_rows", "K3 hconv rows3<2048>, C4 (6143 rows, both x-streams)"),
       ("c4_k7", "K7 fft0padBackward<2048>, C4 x pass"), ("c4_k8", "K8 fft0padForward<2048>, C4 x pass"),
       ("c5a_k5x", "K5 fftpadBackward<512>, C5a x pass (all (y,z) columns)"),
       ("c5a_rows", "K2 cconv rows2<512>, C5a first slab group"), ("c5b_k7x", "K7 fft0padBackward<512>, C5b x pass"),
-      ("c5b_rows", "K3 hconv rows3<512>, C5b first slab group")]
+      ("c5b_rows", "K3 hconv rows3<512>, C5b first slab group"),
+      ("c4t_k5", "K5 fftpadBackward<4096>, C4t x pass (f, g)"), ("c4t_rows", "K4 tconv rows3<2048>, C4t"),
+      ("c3a_k5", "K5 fftpadBackward<1024>, C3a x pass"), ("c3a_rows", "K2 cconv rows2<1024>, C3a")]
 nd = [f"# {tag}: ncu --set full captures of the dominant 2D / 3D kernels", "",
       "Command: `tools/prof_nd_full.sh` (first launch of each kernel in one call of the config, `ncu --set full "
       "--import-source on --clock-control none -k regex:<kernel> -c 1`, cold cache, replayed). Reports stay in "

@@ -9,3 +9,7 @@ bash tools/prof_pencil.sh ${t}_c5a_k5x cconv3d 512,512,512 pad_bwd
 bash tools/prof_pencil.sh ${t}_c5a_rows cconv3d 512,512,512 cconv_rows
 bash tools/prof_pencil.sh ${t}_c5b_k7x hconv3d 1023,1023,512 pad0_bwd
 bash tools/prof_pencil.sh ${t}_c5b_rows hconv3d 1023,1023,512 hconv_rows3
+bash tools/prof_pencil.sh ${t}_c4t_k5 tconv2d 4096,2048 pad_bwd
+bash tools/prof_pencil.sh ${t}_c4t_rows tconv2d 4096,2048 tconv_rows3
+bash tools/prof_pencil.sh ${t}_c3a_k5 cconv2d 1,1024,1024 pad_bwd
+bash tools/prof_pencil.sh ${t}_c3a_rows cconv2d 1,1024,1024 cconv_rows
