@@ -115,7 +115,7 @@ for short, label in ND:
               f"{raw('sm__warps_active.avg.pct_of_peak_sustained_active'):.0f}% | "
               f"{raw('launch__registers_per_thread'):.0f} | {raw('smsp__sass_inst_executed_op_local_ld.sum'):.0f} | "
               + ", ".join(f"{a} {100 * b / tot:.0f}%" for a, b in stalls[:3]) + " |")
-if len(nd) > 6:
+if len(nd) == 6 + len(ND):   # only a complete capture set replaces the committed summary
     with open(os.path.join(dst, f"{tag}_ncu_nd_summary.md"), "w") as fh:
         fh.write("\n".join(nd) + "\n")
 print("wrote", dst, sorted(os.listdir(dst)))
