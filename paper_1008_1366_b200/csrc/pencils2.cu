@@ -76,17 +76,17 @@ using K56Cfg = TCfg<N, (k56_wide<N>() ? (N >= IDC_K56_NARROW_MIN && N <= IDC_K56
 // radix-16 passes) for 256 <= m <= 4096 -- measured hconv2d 2048^2 -5%,
 // hconv3d 512^3 -1.5%, hconv2d 8191 x 512 (m = 4096) -6% against E = 8 /
 // 512 threads.
-// 128-thread CTAs (half-width tiles, two CTAs per SM) for m in
-// [IDC_K78_NARROW_MIN, IDC_K78_NARROW_MAX]: at m = 1024 (2-column tiles)
-// hconv2d 2047 x 2048 0.332 -> 0.320 ms; at m = 512 (4-column tiles)
-// hconv3d 59.5 -> 70.8 ms, at m = 2048 (1-column tiles) hconv2d 4095 x
-// 2048 0.61 -> 0.80 ms -- the DRAM row segment width decides
-#ifndef IDC_K78_NARROW_MIN
-#define IDC_K78_NARROW_MIN 1024
+// 128-thread CTAs (half-width tiles, two CTAs per SM) for the m whose
+// log2 bit is set in IDC_K78_NARROW_MASK: m = 1024 (2-column tiles, hconv2d
+// 2047 x 2048 0.332 -> 0.320 ms) and m = 256 (8-column tiles, hconv2d 511 x
+// 4096 0.190 -> 0.184 ms); not m = 512 (4-column tiles: hconv3d 59.5 ->
+// 70.8 ms) nor m = 2048 (1-column tiles: hconv2d 4095 x 2048 0.61 ->
+// 0.80 ms) -- the DRAM row segment width decides
+#ifndef IDC_K78_NARROW_MASK
+#define IDC_K78_NARROW_MASK ((1 << 10) | (1 << 8))
 #endif
-#ifndef IDC_K78_NARROW_MAX
-#define IDC_K78_NARROW_MAX 1024
-#endif
+template <int N>
+constexpr bool k78_narrow() { return ((IDC_K78_NARROW_MASK) >> ilog2(N)) & 1; }
 #ifndef IDC_K78_WIDE_MIN
 #define IDC_K78_WIDE_MIN 256
 #endif
@@ -96,7 +96,7 @@ using K56Cfg = TCfg<N, (k56_wide<N>() ? (N >= IDC_K56_NARROW_MIN && N <= IDC_K56
 template <int N>
 constexpr bool k78_wide() { return N >= IDC_K78_WIDE_MIN && N <= IDC_K78_WIDE_MAX; }
 template <int N>
-using K78Cfg = TCfg<N, (k78_wide<N>() ? (N >= IDC_K78_NARROW_MIN && N <= IDC_K78_NARROW_MAX ? 128 : 256)
+using K78Cfg = TCfg<N, (k78_wide<N>() ? (k78_narrow<N>() ? 128 : 256)
                                       : IDC_PENCIL0_THREADS),
                    (k78_wide<N>() ? 16 : IDC_PENCIL_E)>;
 
