@@ -2,22 +2,36 @@
 """Benchmark of the implicitly dealiased convolution hot path on B200.
 
 Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` prints ONE
-JSON line on rank 0.  Default workload = BASELINE.json configs[1]: the 1D
-centered Hermitian convolution (hconv1d) and the 1D centered Hermitian
-ternary convolution (tconv1d) at m = 4096, B = 4096 rows each, complex128.
-One step = one hconv1d call over its batch + one tconv1d call over its
-batch (every row of the §8(a) 1D path: twiddle split, backward FFTs,
-products, forward FFTs, recombination), inputs resident in HBM.  The arrays
-(0.5-0.75 GB per call) exceed the 126 MB L2 and are restored from pristine
-copies before every step (the call is in place), which also flushes L2.
+JSON line on rank 0.
 
-Multi-GPU: the rows are independent problems, so every rank runs its own
-batch (different seeded items) with no collective on the data path;
-``scaling`` = "weak", value = all ranks' convolutions / max-over-ranks time.
+Headline (``value``): config 5b -- the 3D centered Hermitian convolution
+hconv3d of 512^3 modes, (2*512-1)^2 x 512 complex128 arrays, the largest
+single-GPU configuration of BASELINE.json.  One step = one idc_hconv3d call
+(every row of SURVEY 8(a): the x-pencil fft0pad backward, the per-x-residue
+slab 2D convolutions -- y pencils, z rows -- and the forward passes), inputs
+resident in HBM.  Every other config (C1 cconv1d, C2a hconv1d, C2b tconv1d,
+C3a / C3b cconv2d, C4 hconv2d, C5a cconv3d) is measured the same way and
+reported in ``parts``, each with its own roofline and CPU-oracle baseline.
 
-``--impl reference`` times the oracle (oracle/, plain C direct sums, the
-CPU reference of this tier) on the host cores on a bounded sample of the same
-workload, and prints the same JSON line with ``"impl": "reference"``.
+Timing: W warm-up calls, then K timed calls, each bracketed by CUDA events on
+the launch stream; before every call (outside the events) the inputs are
+restored from pristine device copies (the call is in place) and a 256 MB
+buffer is written (L2 flush).  The library's per-kernel-class event profiler
+(idc_profile_begin/end) runs during the timed calls and gives each kernel's
+device time, from which the dominant kernel's achieved algorithmic bytes or
+flops per launch are computed (``roofline``).
+
+Multi-GPU (``--gpus N``; under torchrun, or self-spawned through
+torch.distributed.run when launched directly): the headline becomes ONE
+config-5b convolution slab-sharded over the N ranks (idc_hconv3d_dist: y
+pencils, ncclAlltoAll, per-residue (x, z) convolutions, ncclAlltoAll back;
+"scaling": "strong"); C5a likewise through idc_cconv3d_dist; the 1D/2D
+configs are independent problems -> replicas on every rank ("weak").
+Times are device times, max over ranks.
+
+``--impl reference`` times the CPU oracle (oracle/: direct sums, the
+reference arm of this tier) on the host cores on a bounded sample of the
+headline workload per step, extrapolated to whole convolutions.
 """
 from __future__ import annotations
 
@@ -39,12 +53,13 @@ import synthgen  # noqa: E402  (seeded inputs; no method arithmetic)
 
 METRIC = "dealiased convolutions/sec (fp64) and achieved HBM GB/s vs B200 peak"
 W = 16  # bytes per complex128 word
+HEADLINE = "c5b"
+DEFAULT_PARTS = "c1,c2a,c2b,c3a,c3b,c4,c5a"
 
 
 def peaks():
     """Roofline denominators: HBM from MEASURED_PEAKS.json (driver-written),
-    fp64 from the unit count x max clock (DESIGN.md "Peaks")."""
-    hbm = 6548.8
+    fp64 from the unit count x max clock (DESIGN.md section 6)."""
     src = "MEASURED_PEAKS.json"
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -54,12 +69,13 @@ def peaks():
         hbm = 6650.0
     # 148 SMs x 64 fp64 FMA lanes x 2 flop x 1.965 GHz (measured DFMA loop: 34.2 TF/s, profiles/r01_peaks.txt)
     fp64 = 148 * 64 * 2 * 1.965e9 / 1e12
-    return {"hbm_gbs": hbm, "hbm_src": src, "fp64_tflops": fp64}
+    return {"hbm_gbs": hbm, "hbm_src": src, "fp64_tflops": fp64,
+            "fp64_src": "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md); measured DFMA loop 34.2"}
 
 
-# --------------------------------------------------------------- workloads --
+# ------------------------------------------------------------------ configs --
 
-def flops_rfft(n):      # 2.5 n log2 n per real transform (SURVEY §8(d))
+def flops_rfft(n):      # 2.5 n log2 n per real transform (SURVEY 8(d))
     return 2.5 * n * np.log2(n) if n > 1 else 0.0
 
 
@@ -67,27 +83,22 @@ def flops_cfft(n):      # 5 n log2 n per complex transform
     return 5.0 * n * np.log2(n) if n > 1 else 0.0
 
 
-WORKLOADS = {
-    # name: parts, each one C-ABI call per step over its batch
-    "c2": dict(desc="configs[1]: hconv1d m=4096 B=4096 + tconv1d m=4096 B=4096", parts=[
-        dict(kind="hconv1d", m=4096, batch=4096, narr=2),
-        dict(kind="tconv1d", m=4096, batch=4096, narr=3)]),
-    "c1": dict(desc="configs[0]: cconv1d m=1024 B=32768", parts=[
-        dict(kind="cconv1d", m=1024, batch=32768, narr=2)]),
-    "c3a": dict(desc="configs[2]: cconv2d 1024x1024", parts=[
-        dict(kind="cconv2d", m=(1024, 1024), batch=1, narr=2)]),
-    "c3b": dict(desc="configs[2]: cconv2d batch 64 x 256x256", parts=[
-        dict(kind="cconv2d", m=(256, 256), batch=64, narr=2)]),
-    "c4": dict(desc="configs[3]: hconv2d mx=my=2048 ((2mx-1) x my)", parts=[
-        dict(kind="hconv2d", m=(2048, 2048), batch=1, narr=2)]),
-    "c4adv": dict(desc="NEXT-1: 2D Euler advective term (M=2 dot-product conv2, P:867-876), mx=my=2048", parts=[
-        dict(kind="advection2d", m=(2048, 2048), batch=1, narr=2)]),
-    "c4t": dict(desc="NEXT-2: 2D centered Hermitian ternary (Function tconv2, P:1087-1109), mx=my=2048", parts=[
-        dict(kind="tconv2d", m=(2048, 2048), batch=1, narr=3)]),
-    "c5a": dict(desc="configs[4]: cconv3d 512^3", parts=[
-        dict(kind="cconv3d", m=(512, 512, 512), batch=1, narr=2)]),
-    "c5b": dict(desc="configs[4]: hconv3d 512^3 modes ((2m-1)^2 x m)", parts=[
-        dict(kind="hconv3d", m=(512, 512, 512), batch=1, narr=2)]),
+CONFIGS = {
+    "c1": dict(kind="cconv1d", m=1024, batch=32768, narr=2, desc="configs[0] C1: cconv1d m=1024, B=32768 rows"),
+    "c2a": dict(kind="hconv1d", m=4096, batch=4096, narr=2, desc="configs[1] C2a: hconv1d m=4096, B=4096 rows"),
+    "c2b": dict(kind="tconv1d", m=4096, batch=4096, narr=3, desc="configs[1] C2b: tconv1d m=4096, B=4096 rows"),
+    "c3a": dict(kind="cconv2d", m=(1024, 1024), batch=1, narr=2, desc="configs[2] C3a: cconv2d 1024x1024"),
+    "c3b": dict(kind="cconv2d", m=(256, 256), batch=64, narr=2, desc="configs[2] C3b: cconv2d 64 x 256x256"),
+    "c4": dict(kind="hconv2d", m=(2048, 2048), batch=1, narr=2,
+               desc="configs[3] C4: hconv2d mx=my=2048, (2mx-1) x my"),
+    "c5a": dict(kind="cconv3d", m=(512, 512, 512), batch=1, narr=2, desc="configs[4] C5a: cconv3d 512^3"),
+    "c5b": dict(kind="hconv3d", m=(512, 512, 512), batch=1, narr=2,
+                desc="configs[4] C5b: hconv3d 512^3 modes, (2m-1)^2 x m"),
+    # SURVEY 8(f) NEXT rows (not part of the default run)
+    "c4adv": dict(kind="advection2d", m=(2048, 2048), batch=1, narr=2,
+                  desc="NEXT-1: 2D Euler advective term (M=2 dot-product conv2, P:867-876), mx=my=2048"),
+    "c4t": dict(kind="tconv2d", m=(2048, 2048), batch=1, narr=3,
+                desc="NEXT-2: 2D centered Hermitian ternary (Function tconv2, P:1087-1109), mx=my=2048"),
 }
 
 
@@ -108,8 +119,15 @@ def shape_of(p):
     raise ValueError(k)
 
 
+def outputs_per_conv(p):
+    """Output values of one convolution (for extrapolating sampled oracle sums)."""
+    shp = shape_of(p)
+    n = int(np.prod(shp))
+    return n // p["batch"] if p["kind"] in ("cconv1d", "hconv1d", "tconv1d", "cconv2d") else n
+
+
 def part_model(p):
-    """Algorithmic HBM bytes and convention flops per convolution (SURVEY §8(d) d.2):
+    """Algorithmic HBM bytes and convention flops per convolution (SURVEY 8(d) d.2):
     bytes = the method's minimum traffic with one HBM round trip per dependent
     phase and per-row work on chip; flops = 5 n log2 n per complex FFT(n),
     2.5 n log2 n per real FFT(n), counted with the paper's transform counts."""
@@ -129,13 +147,10 @@ def part_model(p):
         fl = 9 * my * flops_cfft(mx) + 3 * mx * 9 * flops_rfft(my)
         return W * (3 * (2 * mx - 1) * my + 18 * mx * my), fl
     if kind == "advection2d":
-        # input build (read w, write 4 arrays), M = 2 dot-product conv2 (x pass over
-        # 4 arrays, rows over 2 pairs, x-forward of one), copy out
         mx, my = m
         fl = 15 * my * flops_cfft(mx) + 3 * mx * 15 * flops_rfft(my)
         return W * (12 * (2 * mx - 1) * my + 30 * mx * my), fl
     if kind == "tconv2d":
-        # x: 3 inputs -> 2 streams of 2mx (K5), rows: 2 x 2mx ternary rows, x forward (K6)
         mx, my = m
         fl = 8 * my * flops_cfft(2 * mx) + 4 * mx * 8 * flops_rfft(2 * my)
         return 20 * W * 2 * mx * my, fl
@@ -151,7 +166,28 @@ def part_model(p):
     raise ValueError(kind)
 
 
-# -------------------------------------------------------------- GPU clocks --
+# Per-kernel algorithmic model: bytes and convention
+# flops per UNIT of a launch (a row for the row kernels, a column for the
+# pencils), n = the kernel's transform size.
+def kernel_model(tag, n):
+    lg = np.log2(n) if n > 1 else 0.0
+    base = tag.rstrip("s").replace("v1", "")
+    if base == "K2":        # Function cconv per row: read f, g, write f; 6 FFT(m)
+        return 3 * W * n, 6 * 5 * n * lg
+    if base == "K3":        # centered Hermitian conv per row: 9 real FFT(m)
+        return 3 * W * n, 9 * 2.5 * n * lg
+    if base == "K4":        # ternary per row: read f, g, h, write f; 8 real FFT(2m)
+        return 4 * W * n, 8 * 2.5 * 2 * n * np.log2(2 * n)
+    if base == "K5":        # fftpadBackward per column: read m, write 2 streams of m; 2 FFT(m)
+        return 3 * W * n, 2 * 5 * n * lg
+    if base == "K6":        # fftpadForward per column: read 2m, write m
+        return 3 * W * n, 2 * 5 * n * lg
+    if base in ("K7", "K8"):  # fft0pad per column: 2m-1 <-> 3 streams of m; 3 FFT(m)
+        return W * (5 * n - 1), 3 * 5 * n * lg
+    return None, None
+
+
+# ------------------------------------------------------------ GPU clocks --
 
 class ClockSampler:
     FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
@@ -208,9 +244,32 @@ def dist_env():
     return ws, rank, local
 
 
+def timing_stats(t):
+    """Median and the paper's one-sided standard deviations of per-call times
+    (P:258-262, AMB-5): sigma_L/H = sqrt(sum_{t_i < T / t_i > T} (t_i - T)^2 / (n/2 - 1)),
+    T the mean of the n samples."""
+    n = len(t)
+    T = sum(t) / n
+    d = max(n / 2 - 1, 1)
+    lo = sum((x - T) ** 2 for x in t if x < T)
+    hi = sum((x - T) ** 2 for x in t if x > T)
+    return {"n": n, "mean_ms": T, "median_ms": statistics.median(t), "sigma_L_ms": (lo / d) ** 0.5,
+            "sigma_H_ms": (hi / d) ** 0.5}
+
+
+def load_traffic():
+    """ncu DRAM bytes per unit of each kernel class (profiles/traffic.json,
+    written by tools/collect_traffic.py from one `ncu --set full` capture)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
 def make_inputs(idc, torch, p, rank, dev):
-    """Seeded device inputs for one part (the config's recipe, DESIGN.md "Input
-    recipe"); item ids offset by rank (weak scaling)."""
+    """Seeded device inputs for one config; batch
+    item ids offset by rank (replicas at N > 1)."""
     kind, B, narr = p["kind"], p["batch"], p["narr"]
     if kind == "tconv2d":       # paper layout: a zero kx = -mx row, then the hconv2d recipe
         q = dict(p, kind="hconv2d")
@@ -221,7 +280,7 @@ def make_inputs(idc, torch, p, rank, dev):
     for role in range(narr):
         a = torch.empty(shp, dtype=torch.complex128, device=dev)
         if kind.endswith("1d") or kind == "cconv2d":
-            for b in range(B):
+            for b in range(B):              # one seeded stream per batch item (array_id = role + 4 item)
                 idc.fill_uniform(a[b], synthgen.array_id(role, rank * B + b), synthgen.SEED)
         else:
             idc.fill_uniform(a, synthgen.array_id(role, rank), synthgen.SEED)
@@ -237,6 +296,7 @@ def make_inputs(idc, torch, p, rank, dev):
                 axes.append(k)
             k2 = sum((ax ** 2).reshape([-1 if i == j else 1 for i in range(len(shp))]) for j, ax in enumerate(axes))
             a /= (1.0 + k2)
+            del k2
             if kind in ("hconv2d", "advection2d"):     # ky = 0 line conjugate-symmetric, U_00 real
                 c = (shp[0] - 1) // 2
                 a[:c, 0] = torch.conj(torch.flip(a[c + 1:, 0], dims=(0,)))
@@ -251,265 +311,20 @@ def make_inputs(idc, torch, p, rank, dev):
     return arrs
 
 
-def call(idc, p, arrs):
-    if p["kind"] == "advection2d":                      # (w, out); device-only call
-        if arrs[0].is_cuda:
-            return idc.advection2d(arrs[0], out=arrs[1])
-        out = idc.advection2d(arrs[0].to("cuda", non_blocking=True))
-        arrs[0].copy_(out, non_blocking=True)            # result back to the host buffer
-        return arrs[0]
-    return getattr(idc, p["kind"])(*arrs)
-
-
-# -------------------------------------------------------------- our arm ----
-
-def run_ours(args):
-    import torch
-    import torch.distributed as tdist
-    from paper_1008_1366_b200 import idconv as idc
-
-    ws, rank, local = dist_env()
-    if ws > 1:
-        tdist.init_process_group("nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    wl = WORKLOADS[args.workload]
-    parts = wl["parts"]
-
-    pristine = [make_inputs(idc, torch, p, rank, dev) for p in parts]
-    work = [[torch.empty_like(a) for a in arrs] for arrs in pristine]
-    torch.cuda.synchronize()
-
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 2x L2
-
-    def restore():
-        for src, dst in zip(pristine, work):
-            for s, d in zip(src, dst):
-                d.copy_(s)
-        flush.zero_()                                                  # cold L2 for every step
-
-    clk = ClockSampler(local).__enter__()   # sample from warm-up through the timed loop
-    time.sleep(0.3)
-    for _ in range(args.warmup):
-        restore()
-        for p, arrs in zip(parts, work):
-            call(idc, p, arrs)
-    torch.cuda.synchronize()
-
-    stream = torch.cuda.current_stream(dev)
-    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in parts]
-           for _ in range(args.steps)]
-    if ws > 1:
-        tdist.barrier()
-    torch.cuda.synchronize()
-    n_launch0 = idc.launch_count()
-    t_wall0 = time.perf_counter()
-    for k in range(args.steps):
-        restore()
-        for j, (p, arrs) in enumerate(zip(parts, work)):
-            evs[k][j][0].record(stream)
-            call(idc, p, arrs)
-            evs[k][j][1].record(stream)
-    torch.cuda.synchronize()
-    launches = idc.launch_count() - n_launch0          # our kernels inside the timed region
-    t_wall = time.perf_counter() - t_wall0
-    time.sleep(0.25)
-    clk.__exit__()
-    if ws > 1:
-        tdist.barrier()
-    samples = [[evs[k][j][0].elapsed_time(evs[k][j][1]) for k in range(args.steps)] for j in range(len(parts))]
-    part_ms = [sum(x) for x in samples]
-    total_ms = sum(part_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-    total_ms_max = float(t.item())
-    convs_per_step = sum(p["batch"] for p in parts) * ws
-    value = convs_per_step * args.steps / (total_ms_max / 1e3)
-
-    # per-part model and roofline of the dominant kernel
-    pk = peaks()
-    part_info = []
-    for p, ms in zip(parts, part_ms):
-        b, fl = part_model(p)
-        sec = ms / 1e3 / args.steps
-        t_b = b * p["batch"] / (pk["hbm_gbs"] * 1e9)
-        t_f = fl * p["batch"] / (pk["fp64_tflops"] * 1e12)
-        part_info.append(dict(kind=p["kind"], m=p["m"], batch=p["batch"], ms_per_call=sec * 1e3,
-                              call_stats=timing_stats(samples[len(part_info)]),
-                              conv_per_s=p["batch"] / sec, hbm_gbs_alg=b * p["batch"] / sec / 1e9,
-                              fp64_tflops_alg=fl * p["batch"] / sec / 1e12, t_roof_ms=max(t_b, t_f) * 1e3,
-                              roofline_frac=max(t_b, t_f) / sec, bound="hbm" if t_b >= t_f else "alu"))
-    dom = max(range(len(parts)), key=lambda j: part_ms[j])
-    d = part_info[dom]
-    if d["bound"] == "hbm":
-        roof = {"bound": "hbm", "achieved": d["hbm_gbs_alg"], "peak": pk["hbm_gbs"], "unit": "GB/s"}
-    else:
-        roof = {"bound": "alu", "achieved": d["fp64_tflops_alg"], "peak": pk["fp64_tflops"], "unit": "TFLOP/s"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["kernel"] = d["kind"] + ("" if d["kind"].endswith("1d") else " (pencil + row kernels)")
-    roof["hbm_frac"] = d["hbm_gbs_alg"] / pk["hbm_gbs"]
-    roof["traffic"] = load_traffic(d["kind"], d["m"])
-    roof["units_per_launch"] = d["batch"]
-    roof["peak_src"] = pk["hbm_src"] if roof["bound"] == "hbm" else \
-        "148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md); measured DFMA loop 34.2"
-
-    # ---------------------------------------------------------- e2e arm --
-    e2e = run_e2e(args, idc, torch, parts, pristine, dev, ws)
-
-    out = None
-    if rank == 0:
-        out = {
-            "metric": METRIC, "value": value, "unit": "conv/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl["desc"], "parallelism": f"replicas{ws}",
-                       "l2": "L2 flushed (256 MB write) and inputs restored from pristine copies before every step",
-                       "seed": synthgen.SEED},
-            "parts": part_info, "roofline": roof, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "wall_s_timed_loop": t_wall,
-        }
-        if not args.no_cpu_baseline and ws == 1:
-            out["cpu_baseline"] = cpu_baseline(args, parts)
-        elif ws > 1:
-            out["cpu_baseline"] = None
-    if ws > 1:
-        tdist.barrier()
-        tdist.destroy_process_group()
-    return out
-
-
-def timing_stats(t):
-    """Median and the paper's one-sided standard deviations of per-call times
-    (P:258-262, AMB-5): sigma_L/H = sqrt(sum_{t_i < T / t_i > T} (t_i - T)^2 / (n/2 - 1)),
-    T the mean of the n samples."""
-    n = len(t)
-    T = sum(t) / n
-    d = max(n / 2 - 1, 1)
-    lo = sum((x - T) ** 2 for x in t if x < T)
-    hi = sum((x - T) ** 2 for x in t if x > T)
-    return {"n": n, "mean_ms": T, "median_ms": statistics.median(t), "sigma_L_ms": (lo / d) ** 0.5,
-            "sigma_H_ms": (hi / d) ** 0.5}
-
-
-def load_traffic(kind, m):
-    """dram bytes per launch from the committed ncu --set full capture, if any."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return json.load(fh).get(f"{kind}:{m if isinstance(m, int) else 'x'.join(map(str, m))}")
-    except Exception:
-        return None
-
-
-def run_e2e(args, idc, torch, parts, pristine, dev, ws):
-    """Same metric through the public API with HOST (pinned) buffers: the
-    H2D copy of every input and the D2H copy of the result are inside the
-    timed region of every step."""
-    host = [[a.cpu().pin_memory() for a in arrs] for arrs in pristine]
-    host_f0 = [arrs[0].clone() for arrs in host]
-    stream = torch.cuda.current_stream(dev)
-    steps = max(1, min(args.steps, args.e2e_steps))
-    bi = sum(a.numel() * 16 for p, arrs in zip(parts, host)
-             for a in (arrs[:1] if p["kind"] == "advection2d" else arrs))
-    bo = sum(arrs[0].numel() * 16 for arrs in host)
-    # warm-up once
-    for p, arrs in zip(parts, host):
-        call(idc, p, arrs)
-    torch.cuda.synchronize()
-    ms = 0.0
-    for _ in range(steps):
-        for arrs, f0 in zip(host, host_f0):
-            arrs[0].copy_(f0)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for p, arrs in zip(parts, host):
-            call(idc, p, arrs)  # H2D inputs, kernel, D2H result into the pinned f
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ms += e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        import torch.distributed as tdist
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-    convs = sum(p["batch"] for p in parts) * ws * steps
-    return {"value": convs / (float(t.item()) / 1e3), "unit": "conv/s", "h2d_bytes_per_step": bi,
-            "d2h_bytes_per_step": bo, "steps": steps}
-
-
-# ----------------------------------------------------------- oracle (CPU) --
-
-def oracle_sample(parts, budget_s):
-    """Time the oracle (direct sums) on a bounded sample of the workload's rows.
-    Returns (conv/s over the sample, description, threads)."""
-    import oracle
-    from oracle import direct
-    fns = {"cconv1d": direct.cconv1d, "hconv1d": direct.hconv1d, "tconv1d": direct.tconv1d}
-    # calibrate on one row of each part, then size the sample to the budget
-    per_row = []
-    for p in parts:
-        arrs = [np.stack([synthgen.uniform_complex(p["m"], synthgen.array_id(r, 0))]) for r in range(p["narr"])]
-        t0 = time.perf_counter()
-        fns[p["kind"]](*arrs)
-        per_row.append(time.perf_counter() - t0)
-    share = budget_s / len(parts)
-    convs, secs, desc = 0, 0.0, []
-    for p, pr in zip(parts, per_row):
-        n = int(max(1, min(p["batch"], share / max(pr, 1e-6))))
-        arrs = [np.stack([synthgen.uniform_complex(p["m"], synthgen.array_id(r, b)) for b in range(n)])
-                for r in range(p["narr"])]
-        t0 = time.perf_counter()
-        fns[p["kind"]](*arrs)
-        secs += time.perf_counter() - t0
-        convs += n
-        desc.append(f"{n} of {p['batch']} {p['kind']} rows (m={p['m']})")
-    # the step's mix: time per step = sum over parts of batch * per-row time
-    return convs, secs, "; ".join(desc)
-
-
-def cpu_baseline(args, parts):
-    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    convs, secs, desc = oracle_sample(parts, args.cpu_budget)
-    return {"value": convs / secs, "unit": "conv/s", "cores": threads, "kind": "oracle",
-            "sample": desc + " -- oracle direct sums (TwoProd+Neumaier, OpenMP), oracle/direct.c"}
-
-
-# ------------------------------------------------- distributed 3D (--dist) --
-
-def run_dist3d(args):
-    """Strong scaling of one 3D convolution over all ranks: rank r
-    holds x-planes [r nx, (r+1) nx) of the global config-5 arrays (hconv3d: the
-    2mx-1 planes padded to 2mx), idc_{c,h}conv3d_dist does the y-pass,
-    ncclAlltoAll, the per-residue (x, z) 2D convolutions, the all-to-all back
-    and the y-forward.  value = convolutions / max-over-ranks time."""
-    import torch
-    import torch.distributed as tdist
-    from paper_1008_1366_b200 import idconv as idc
-
-    ws, rank, local = dist_env()
-    wl = WORKLOADS[args.workload]
-    p = wl["parts"][0]
-    kind = p["kind"]
-    if kind not in ("cconv3d", "hconv3d"):
-        raise SystemExit("--dist applies to the 3D workloads (c5a, c5b)")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    import datetime
-    if not tdist.is_initialized():
-        tmo = datetime.timedelta(seconds=120)
-        if "MASTER_ADDR" in os.environ:                      # launched by torchrun: env:// rendezvous
-            tdist.init_process_group("nccl" if ws > 1 else "gloo", timeout=tmo)
-        else:
-            tdist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % (29650 + os.getpid() % 300),
-                                     rank=0, world_size=1, timeout=tmo)
-    comm = idc.Comm()
+def make_dist_inputs(idc, torch, p, rank, ws, dev):
+    """This rank's x-slab of the config-5 arrays (hconv3d: the 2mx-1 planes
+    padded to 2mx with a zero plane), generated index-addressably with the
+    config's 1/(1+|k|^2) scaling.  Timing input: the kz = 0 plane is not
+    re-symmetrised across ranks (the call convolves its Hermitian projection,
+    AMB-7; the arithmetic is the same)."""
     mx, my, mz = p["m"]
-    herm = kind == "hconv3d"
+    herm = p["kind"] == "hconv3d"
     planes = 2 * mx if herm else mx
     nx = planes // ws
     x0 = rank * nx
     ny = 2 * my - 1 if herm else my
     plane = ny * mz
-    pristine = []
+    out = []
     for role in range(2):
         a = torch.empty((nx, ny, mz), dtype=torch.complex128, device=dev)
         idc.fill_uniform(a, synthgen.array_id(role, 0), synthgen.SEED, start=x0 * plane)
@@ -519,112 +334,415 @@ def run_dist3d(args):
         a /= 1.0 + kx[:, None, None] ** 2 + kyv[None, :, None] ** 2 + kz[None, None, :] ** 2
         if herm and x0 + nx == planes:
             a[-1].zero_()                                  # padding plane
-        pristine.append(a)
+        out.append(a)
+    return out
+
+
+def call(idc, p, arrs):
+    if p["kind"] == "advection2d":                      # (w, out); device-only call
+        if arrs[0].is_cuda:
+            return idc.advection2d(arrs[0], out=arrs[1])
+        out = idc.advection2d(arrs[0].to("cuda", non_blocking=True))
+        arrs[0].copy_(out, non_blocking=True)
+        return arrs[0]
+    return getattr(idc, p["kind"])(*arrs)
+
+
+def kernel_table(p, prof, steps, pk, traffic):
+    """Per-kernel-class device time of one call and its achieved algorithmic
+    bytes / flops (DESIGN.md section 6 models)."""
+    tot = sum(r["ms"] for r in prof) or 1.0
+    rows = []
+    for r in prof:
+        b_u, f_u = kernel_model(r["tag"], r["n"])
+        d = dict(kernel=f"{r['tag']}<{r['n']}>", launches_per_call=r["launches"] / steps,
+                 ms_per_call=r["ms"] / steps, share=r["ms"] / tot, units_per_launch=r["units"] / r["launches"])
+        if b_u is not None:
+            sec = r["ms"] / 1e3
+            d["hbm_gbs_alg"] = b_u * r["units"] / sec / 1e9
+            d["fp64_tflops_alg"] = f_u * r["units"] / sec / 1e12
+            d["hbm_frac"] = d["hbm_gbs_alg"] / pk["hbm_gbs"]
+            d["fp64_frac"] = d["fp64_tflops_alg"] / pk["fp64_tflops"]
+            t_b = b_u / (pk["hbm_gbs"] * 1e9)
+            t_f = f_u / (pk["fp64_tflops"] * 1e12)
+            d["bound"] = "hbm" if t_b >= t_f else "alu"
+            tpu = traffic.get(f"{r['tag']}:{r['n']}")
+            d["traffic_per_launch"] = tpu * d["units_per_launch"] if tpu else None
+        rows.append(d)
+    rows.sort(key=lambda d: -d["ms_per_call"])
+    return rows
+
+
+def dominant_roofline(kt, pk):
+    """roofline object of the contract for the dominant kernel of a call."""
+    for d in kt:
+        if "bound" not in d:
+            continue
+        if d["bound"] == "hbm":
+            r = {"bound": "hbm", "achieved": d["hbm_gbs_alg"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                 "peak_src": pk["hbm_src"]}
+        else:
+            r = {"bound": "alu", "achieved": d["fp64_tflops_alg"], "peak": pk["fp64_tflops"], "unit": "TFLOP/s",
+                 "peak_src": pk["fp64_src"]}
+        r["frac"] = r["achieved"] / r["peak"]
+        r["traffic"] = d.get("traffic_per_launch")
+        r["kernel"] = d["kernel"]
+        r["share_of_step"] = d["share"]
+        r["units_per_launch"] = d["units_per_launch"]
+        r["hbm_frac"] = d["hbm_frac"]
+        r["fp64_frac"] = d["fp64_frac"]
+        return r
+    return None
+
+
+# -------------------------------------------------------------- our arm ----
+
+def measure(idc, torch, tdist, name, args, rank, ws, dev, comm=None, want_e2e=False):
+    """Time one config: W warm-up calls, K timed calls (restore + L2 flush
+    before each, outside the events), kernel profile over the timed calls."""
+    p = CONFIGS[name]
+    dist3d = comm is not None and p["kind"] in ("cconv3d", "hconv3d")
+    if dist3d:
+        pristine = make_dist_inputs(idc, torch, p, rank, ws, dev)
+        mx, my, mz = p["m"]
+        fn = idc.hconv3d_dist if p["kind"] == "hconv3d" else idc.cconv3d_dist
+
+        def run(arrs):
+            fn(comm, arrs[0], arrs[1], mx, my, mz)
+    else:
+        pristine = make_inputs(idc, torch, p, rank, dev)
+
+        def run(arrs):
+            call(idc, p, arrs)
     work = [torch.empty_like(a) for a in pristine]
-    fn = idc.hconv3d_dist if herm else idc.cconv3d_dist
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 2x L2
+    stream = torch.cuda.current_stream(dev)
 
     def restore():
-        for src, dst in zip(pristine, work):
-            dst.copy_(src)
+        for s_, d_ in zip(pristine, work):
+            d_.copy_(s_)
         flush.zero_()
 
     for _ in range(args.warmup):
         restore()
-        fn(comm, work[0], work[1], mx, my, mz)
+        run(work)
     torch.cuda.synchronize()
-    tdist.barrier()
-    ms = 0.0
+    if ws > 1:
+        tdist.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clk = ClockSampler(dev.index or 0).__enter__()
+    time.sleep(0.2)
+    torch.cuda.synchronize()
     n0 = idc.launch_count()
-    for _ in range(args.steps):
+    idc.profile_begin()
+    t_wall0 = time.perf_counter()
+    for k in range(args.steps):
         restore()
+        evs[k][0].record(stream)
+        run(work)
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall0
+    prof = idc.profile_end()
+    launches = idc.launch_count() - n0
+    time.sleep(0.2)
+    clk.__exit__()
+    samples = [e0.elapsed_time(e1) for e0, e1 in evs]
+    tot = torch.tensor([sum(samples)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        tdist.all_reduce(tot, op=tdist.ReduceOp.MAX)
+    total_ms = float(tot.item())
+    sec = total_ms / 1e3 / args.steps
+    pk = peaks()
+    b, fl = part_model(p)
+    convs = p["batch"] * (1 if dist3d else ws)        # strong (3D dist) or replicas (weak)
+    ngpu_peak = ws
+    t_b = b * convs / (pk["hbm_gbs"] * 1e9 * ngpu_peak)
+    t_f = fl * convs / (pk["fp64_tflops"] * 1e12 * ngpu_peak)
+    kt = kernel_table(p, prof, args.steps, pk, load_traffic())
+    out = dict(config=name, workload=p["desc"], kind=p["kind"], m=p["m"], batch=p["batch"],
+               scaling="strong" if dist3d else "weak", ms_per_call=sec * 1e3, call_stats=timing_stats(samples),
+               conv_per_s=convs / sec, hbm_gbs_alg=b * convs / sec / 1e9, fp64_tflops_alg=fl * convs / sec / 1e12,
+               t_roof_ms=max(t_b, t_f) * 1e3, roofline_frac=max(t_b, t_f) / sec,
+               bound="hbm" if t_b >= t_f else "alu", gpu_launches=launches, kernels=kt,
+               roofline=dominant_roofline(kt, pk), clocks=clk.summary(), wall_s_timed_loop=t_wall)
+    del work, flush
+    if want_e2e and not dist3d:
+        out["e2e"] = run_e2e(args, idc, torch, p, pristine, dev, ws, tdist)
+    del pristine
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_e2e(args, idc, torch, p, pristine, dev, ws, tdist):
+    """Same metric through the public API with HOST (pinned) buffers: the
+    H2D copy of every input and the D2H copy of the result are inside the
+    timed region of every step."""
+    host = [a.cpu().pin_memory() for a in pristine]
+    f0 = host[0].clone()
+    stream = torch.cuda.current_stream(dev)
+    steps = max(1, min(args.steps, args.e2e_steps))
+    bi = sum(a.numel() * 16 for a in (host[:1] if p["kind"] == "advection2d" else host))
+    bo = host[0].numel() * 16
+    call(idc, p, host)                                  # warm-up
+    torch.cuda.synchronize()
+    ms = 0.0
+    for _ in range(steps):
+        host[0].copy_(f0)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        fn(comm, work[0], work[1], mx, my, mz)
-        e1.record()
+        e0.record(stream)
+        call(idc, p, host)  # H2D inputs, kernels, D2H result into the pinned f
+        e1.record(stream)
         torch.cuda.synchronize()
         ms += e0.elapsed_time(e1)
-    launches = idc.launch_count() - n0
-    tdist.barrier()
-    t = torch.tensor([ms], dtype=torch.float64, device=dev if ws > 1 else "cpu")
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if ws > 1:
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = args.steps / (ms_max / 1e3)
-    b, fl = part_model(p)
-    pk = peaks()
-    sec = ms_max / 1e3 / args.steps
-    t_b = b / (pk["hbm_gbs"] * 1e9 * ws)
-    t_f = fl / (pk["fp64_tflops"] * 1e12 * ws)
+    convs = p["batch"] * ws * steps
+    del host, f0
+    return {"value": convs / (float(t.item()) / 1e3), "unit": "conv/s", "h2d_bytes_per_step": bi,
+            "d2h_bytes_per_step": bo, "steps": steps}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as tdist
+    from paper_1008_1366_b200 import idconv as idc
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if ws > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")            # communicator lines (NVLS, nranks) on stderr
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        tdist.init_process_group("nccl", device_id=dev)
+        comm = idc.Comm()
+    parts_names = [x for x in args.parts.split(",") if x] if args.parts else []
+    parts_names = [x for x in parts_names if x != args.workload]
+    parts = []
+    for name in parts_names:
+        parts.append(measure(idc, torch, tdist, name, args, rank, ws, dev, comm=comm,
+                             want_e2e=(not args.no_e2e and ws == 1 and CONFIGS[name]["kind"].endswith("1d"))))
+    head = measure(idc, torch, tdist, args.workload, args, rank, ws, dev, comm=comm, want_e2e=not args.no_e2e)
+    if comm is not None:
+        comm.close()
     out = None
     if rank == 0:
-        bound = "hbm" if t_b >= t_f else "alu"
+        hp = CONFIGS[args.workload]
         out = {
-            "metric": METRIC, "value": value, "unit": "conv/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl["desc"] + f" -- slab-sharded over {ws} rank(s), idc_{kind}_dist",
-                       "parallelism": f"x-slabs{ws}", "seed": synthgen.SEED,
-                       "l2": "L2 flushed (256 MB write) and inputs restored before every step"},
-            "roofline": {"bound": bound,
-                         "achieved": (b / sec / 1e9) if bound == "hbm" else (fl / sec / 1e12),
-                         "peak": pk["hbm_gbs"] * ws if bound == "hbm" else pk["fp64_tflops"] * ws,
-                         "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
-                         "frac": max(t_b, t_f) / sec, "kernel": kind + "_dist (all phases, aggregate peak)",
-                         "traffic": None},
-            "gpu_launches": launches, "cpu_baseline": None,
+            "metric": METRIC, "value": head["conv_per_s"], "unit": "conv/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": head["ms_per_call"], "higher_is_better": True,
+            "scaling": head["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": head["workload"], "kind": hp["kind"], "m": hp["m"], "batch": hp["batch"],
+                       "parallelism": (f"x-slabs{ws} (NCCL all-to-all)" if head["scaling"] == "strong" and ws > 1
+                                       else f"replicas{ws}"),
+                       "l2": "inputs (> L2) restored from pristine device copies and a 256 MB buffer written "
+                             "(L2 flush) before every timed call",
+                       "seed": synthgen.SEED},
+            "roofline": head["roofline"],
+            "call_roofline": {"bound": head["bound"], "frac": head["roofline_frac"], "t_roof_ms": head["t_roof_ms"],
+                              "hbm_gbs_alg": head["hbm_gbs_alg"], "fp64_tflops_alg": head["fp64_tflops_alg"]},
+            "e2e": head.get("e2e"), "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
+            "call_stats": head["call_stats"], "kernels": head["kernels"],
+            "wall_s_timed_loop": head["wall_s_timed_loop"], "parts": parts,
         }
-    comm.close()
-    tdist.barrier()
-    tdist.destroy_process_group()
+        if ws > 1:
+            out["nccl"] = {"backend": "nccl", "nranks": ws, "version": ".".join(map(str, torch.cuda.nccl.version())),
+                           "debug": os.environ.get("NCCL_DEBUG")}
+    if ws == 1 and rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.workload, args.cpu_budget)
+        for pt in parts:
+            pt["cpu_baseline"] = cpu_baseline(pt["config"], args.cpu_budget_part)
+    elif out is not None:
+        out["cpu_baseline"] = None
+    if ws > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
     return out
+
+
+# ----------------------------------------------------------- oracle (CPU) --
+
+def _oracle_inputs(p):
+    kind = p["kind"]
+    if kind in ("cconv2d",):
+        f, g = synthgen.cconv2d_inputs(*p["m"], 1)
+        return [f[0], g[0]]
+    if kind == "hconv2d":
+        return list(synthgen.hconv2d_inputs(*p["m"]))
+    if kind == "cconv3d":
+        return list(synthgen.cconv3d_inputs(*p["m"]))
+    if kind == "hconv3d":
+        return list(synthgen.hconv3d_inputs(*p["m"]))
+    raise ValueError(kind)
+
+
+class OracleSampler:
+    """The CPU oracle (direct sums, oracle/direct.c) on bounded samples of a
+    config: 1D kinds a number of whole rows; 2D/3D kinds random output points
+    (3D: random (x, y) lines with several z each), extrapolated to whole
+    convolutions from the measured time per output point."""
+
+    def __init__(self, name):
+        from oracle import direct
+        self.d = direct
+        self.p = CONFIGS[name]
+        self.name = name
+        self.rs = np.random.default_rng(1008)
+        kind = self.p["kind"]
+        if kind.endswith("1d"):
+            self.arrs = None
+        else:
+            self.arrs = _oracle_inputs(self.p)
+
+    def sample(self, budget_s):
+        """Run the oracle for about budget_s seconds; returns (convs, secs, desc)."""
+        p, kind, d = self.p, self.p["kind"], self.d
+        t_end = time.perf_counter() + budget_s
+        secs, done = 0.0, 0
+        if kind.endswith("1d"):
+            fn = {"cconv1d": d.cconv1d, "hconv1d": d.hconv1d, "tconv1d": d.tconv1d}[kind]
+            while True:
+                rows = [self.rs.integers(0, p["batch"])]
+                arrs = [np.stack([synthgen.uniform_complex(p["m"], synthgen.array_id(r, b)) for b in rows])
+                        for r in range(p["narr"])]
+                if kind != "cconv1d":
+                    for a in arrs:
+                        a[:, 0] = a[:, 0].real
+                t0 = time.perf_counter()
+                fn(*arrs)
+                secs += time.perf_counter() - t0
+                done += 1
+                if time.perf_counter() > t_end:
+                    break
+            return done, secs, f"{done} whole rows of {p['batch']} ({kind}, m={p['m']})"
+        f, g = self.arrs
+        npts = 0
+        while True:
+            if kind == "cconv2d":
+                idx = self.rs.choice(f.size, 4, replace=False)
+                t0 = time.perf_counter()
+                d.cconv_nd_at(f, g, idx)
+            elif kind == "hconv2d":
+                idx = self.rs.choice(f.size, 4, replace=False)
+                t0 = time.perf_counter()
+                d.hconv2d_at(f, g, idx)
+            elif kind == "cconv3d":
+                idx = self.rs.choice(f.size, 4, replace=False)
+                t0 = time.perf_counter()
+                d.cconv3d_at_large(f, g, idx)
+            else:   # hconv3d: one random (x, y) line, 4 random z on it
+                i, j = self.rs.integers(0, f.shape[0]), self.rs.integers(0, f.shape[1])
+                kz = self.rs.choice(f.shape[2], 4, replace=False)
+                idx = np.ravel_multi_index((np.full(4, i), np.full(4, j), kz), f.shape)
+                t0 = time.perf_counter()
+                d.hconv3d_at_lines(f, g, idx)
+            secs += time.perf_counter() - t0
+            npts += len(idx)
+            if time.perf_counter() > t_end:
+                break
+        per_pt = secs / npts
+        convs = secs / (per_pt * outputs_per_conv(p))   # whole convolutions' worth of oracle time
+        return convs, secs, (f"{npts} random outputs of the {'x'.join(map(str, shape_of(p)))} output "
+                             f"({kind}), direct sums, {per_pt * 1e3:.1f} ms per output; "
+                             f"EXTRAPOLATED to {outputs_per_conv(p)} outputs per convolution")
+
+
+def cpu_baseline(name, budget):
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    s = OracleSampler(name)
+    convs, secs, desc = s.sample(budget)
+    return {"value": convs / secs, "unit": "conv/s", "cores": threads, "kind": "oracle",
+            "sample": desc + " -- oracle/direct.c (TwoProd + Neumaier / Dot2 compensated, OpenMP)"}
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return None
-    wl = WORKLOADS[args.workload]
-    parts = wl["parts"]
+    p = CONFIGS[args.workload]
     threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    budget = max(2.0, args.cpu_budget / max(1, args.steps + args.warmup))
+    s = OracleSampler(args.workload)
+    budget = max(1.0, args.cpu_budget / max(1, args.steps + args.warmup))
     for _ in range(args.warmup):
-        oracle_sample(parts, budget)
-    convs, secs, desc = 0, 0.0, ""
+        s.sample(budget)
+    convs, secs, desc = 0.0, 0.0, ""
     for _ in range(args.steps):
-        c, s, desc = oracle_sample(parts, budget)
+        c, t, desc = s.sample(budget)
         convs += c
-        secs += s
+        secs += t
     value = convs / secs
     return {"metric": METRIC, "value": value, "unit": "conv/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": wl["desc"], "parallelism": "host cores", "seed": synthgen.SEED},
+            "config": {"workload": p["desc"], "kind": p["kind"], "m": p["m"], "batch": p["batch"],
+                       "parallelism": "host cores", "seed": synthgen.SEED},
             "cpu_baseline": {"value": value, "unit": "conv/s", "cores": threads, "kind": "oracle",
                              "sample": desc + " per step"},
             "e2e": {"value": value, "unit": "conv/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
-def main():
+# --------------------------------------------------- multi-process launch --
+
+def spawn(args, argv):
+    """--gpus N launched directly (no torchrun env): re-launch this script
+    under torch.distributed.run with N local ranks on 127.0.0.1."""
+    import random
+    port = 29500 + random.randrange(0, 2000)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd)
+
+
+def dry_run(args):
+    """Rendezvous check without GPUs: every rank joins a gloo group and
+    reports itself; rank 0 prints the plan as one JSON line."""
+    import torch
+    import torch.distributed as tdist
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        tdist.init_process_group("gloo")
+        t = torch.zeros(ws, dtype=torch.int64)
+        t[rank] = os.getpid()
+        tdist.all_reduce(t)
+        pids = t.tolist()
+        tdist.destroy_process_group()
+    else:
+        pids = [os.getpid()]
+    if rank == 0:
+        return {"dry_run": True, "n_gpus": args.gpus, "world_size": ws, "rank_pids": pids,
+                "headline": args.workload, "parts": args.parts,
+                "plan": ("3D configs slab-sharded over the ranks (idc_*conv3d_dist), 1D/2D replicas"
+                         if ws > 1 else "single GPU")}
+    return None
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="idconv", choices=["idconv", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle CPU work")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--workload", default=HEADLINE, choices=sorted(CONFIGS), help="headline config")
+    ap.add_argument("--parts", default=DEFAULT_PARTS, help="comma-separated configs measured besides the headline")
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle CPU work (headline)")
+    ap.add_argument("--cpu-budget-part", type=float, default=3.0, help="seconds of oracle CPU work per part")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--dist", action="store_true",
-                    help="3D workloads: one convolution slab-sharded over all ranks (strong scaling)")
-    args = ap.parse_args()
-    if args.warmup < 3 and args.impl == "idconv":
-        print("warning: the contract asks for >= 3 warm-up steps", file=sys.stderr)
-    if args.impl == "reference":
+    ap.add_argument("--dry-run", action="store_true", help="spawn/rendezvous check only (no GPU)")
+    args = ap.parse_args(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args, argv))
+    if args.dry_run:
+        out = dry_run(args)
+    elif args.impl == "reference":
         out = run_reference(args)
-    elif args.dist:
-        out = run_dist3d(args)
     else:
+        if args.warmup < 3:
+            print("warning: the contract asks for >= 3 warm-up steps", file=sys.stderr)
         out = run_ours(args)
     if out is not None:
         print(json.dumps(out), flush=True)

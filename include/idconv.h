@@ -88,6 +88,19 @@ IDC_API const char* idc_version(void);
  * caller count the kernels inside a timed region. */
 IDC_API long long idc_launch_count(void);
 
+/* Opt-in per-kernel profiler (instrumentation, not the method).  After
+ * idc_profile_begin() every hot-path launch is bracketed by two CUDA events
+ * recorded on its own stream.  idc_profile_end() stops recording, waits for
+ * those events and writes one line per kernel class
+ *     "<tag> <n> <launches> <units> <milliseconds>\n"
+ * (tag = kernel class of DESIGN.md section 6, e.g. K3 or K7; n = transform
+ * size; units = rows or pencil columns processed in total) into buf (at most
+ * len bytes, NUL-terminated).  Returns the bytes needed including the NUL,
+ * or -1 if an event could not be read.  Not thread-safe against concurrent
+ * begin/end pairs; calls from other threads while profiling are recorded. */
+IDC_API idc_status idc_profile_begin(void);
+IDC_API long idc_profile_end(char* buf, size_t len);
+
 /* Bytes of device workspace `work` the call of kind k needs for the given
  * sizes (unused sizes are ignored; pass 1).  1D: m0 = m.  2D: (m0, m1) =
  * (mx, my).  3D: (m0, m1, m2) = (mx, my, mz).  Returns 0 for unsupported

@@ -49,12 +49,29 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 
 
+def _cpu_has(*flags) -> bool:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            have = set()
+            for line in fh:
+                if line.startswith("flags"):
+                    have = set(line.split(":", 1)[1].split())
+                    break
+        return all(f in have for f in flags)
+    except OSError:
+        return False
+
+
 def build(force: bool = False) -> str:
     """Compile oracle/direct.c into oracle/liboracle.so (gcc, OpenMP)."""
     so = os.path.join(_HERE, "liboracle.so")
     src = os.path.join(_HERE, "direct.c")
     if force or not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
-        cmd = f"gcc -O2 -fopenmp -ffp-contract=off -fPIC -shared -o {so} {src} -lm"
+        # hardware FMA keeps TwoProd exact and fast (a libm fma() call is
+        # ~20x slower); -ffp-contract=off keeps the compiler from fusing the
+        # error-free transforms themselves
+        isa = "-mavx2 -mfma" if _cpu_has("avx2", "fma") else ""
+        cmd = f"gcc -O3 {isa} -fopenmp -ffp-contract=off -fPIC -shared -o {so} {src} -lm"
         if os.system(cmd) != 0:
             raise RuntimeError("oracle build failed: " + cmd)
     return so
@@ -76,6 +93,7 @@ def lib():
             "orc_hconv2d_at": [P, P, I, I, P, I, P],
             "orc_hconv3d_at_mirror": [P, P, I, I, I, P, I, P],
             "orc_cconv3d_at_par": [P, P, I, I, I, P, I, P],
+            "orc_hconv3d_at_zlist": [P, P, I, I, I, I, I, P, I, P],
         }.items():
             fn = getattr(_LIB, name)
             fn.argtypes = args
@@ -211,6 +229,27 @@ class direct:
         out = np.empty(idx.size, dtype=np.complex128)
         _check(lib().orc_hconv3d_at_mirror(_ptr(f), _ptr(g), mx, my, mz, _ptr(idx), idx.size, _ptr(out)),
                "hconv3d_at_large")
+        return out
+
+    @staticmethod
+    def hconv3d_at_lines(f, g, idx):
+        """D7 at sampled outputs of a large array (O5 for config 5b): the same
+        terms as hconv3d_at, read in place from the stored half-space (mirror
+        and kz = 0 projection resolved per z run, AMB-7) and summed as Dot2
+        compensated dot products; outputs sharing (kx, ky) share one pass
+        over the x-y plane (oracle/direct.c orc_hconv3d_at_zlist)."""
+        f, g = _c(f), _c(g)
+        mx, my, mz = (f.shape[0] + 1) // 2, (f.shape[1] + 1) // 2, f.shape[2]
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        i, j, l = np.unravel_index(idx, f.shape)
+        out = np.empty(idx.size, dtype=np.complex128)
+        for (a, b) in sorted(set(zip(i.tolist(), j.tolist()))):
+            sel = np.nonzero((i == a) & (j == b))[0]
+            kz = np.ascontiguousarray(l[sel], dtype=np.int64)
+            res = np.empty(kz.size, dtype=np.complex128)
+            _check(lib().orc_hconv3d_at_zlist(_ptr(f), _ptr(g), mx, my, mz, a - (mx - 1), b - (my - 1), _ptr(kz),
+                                              kz.size, _ptr(res)), "hconv3d_at_lines")
+            out[sel] = res
         return out
 
     @staticmethod
@@ -680,6 +719,37 @@ class application:
                 Wq = np.where(ok, W[np.clip(qx + mx - 1, 0, nx - 1), np.clip(qy + my - 1, 0, ny - 1)], 0.0)
                 term = (px * ky - py * kx) * inv * W * Wq
                 out[kx + mx - 1, ky] = term.sum()
+        return out
+
+
+    @staticmethod
+    def euler_sum_at(w, idx):
+        """S_k of euler_sum at the given linear output indices of
+        the (2mx-1, my) storage, for large sizes: for each k the sum over p is
+        taken over the rectangle where both p and k - p lie in the centered
+        box (the same terms euler_sum masks), with numpy array slices."""
+        W = application.hermitian_full2d(w)
+        nx, ny = W.shape
+        mx, my = (nx + 1) // 2, (ny + 1) // 2
+        out = np.empty(len(idx), dtype=np.complex128)
+        for o, lin in enumerate(np.asarray(idx, dtype=np.int64)):
+            kx, ky = int(lin) // my - (mx - 1), int(lin) % my
+            # p in [lo, hi] per axis with |p| <= m-1 and |k - p| <= m-1
+            px0, px1 = max(-(mx - 1), kx - (mx - 1)), min(mx - 1, kx + (mx - 1))
+            py0, py1 = max(-(my - 1), ky - (my - 1)), min(my - 1, ky + (my - 1))
+            if px0 > px1 or py0 > py1:
+                out[o] = 0.0
+                continue
+            px = np.arange(px0, px1 + 1)[:, None]
+            py = np.arange(py0, py1 + 1)[None, :]
+            Wp = W[px0 + mx - 1: px1 + mx, py0 + my - 1: py1 + my]
+            # W_{k-p}: rows kx - px, columns ky - py, i.e. a reversed slice
+            Wq = W[kx - px0 + mx - 1: kx - px1 + mx - 2 if kx - px1 + mx - 2 >= 0 else None: -1,
+                   ky - py0 + my - 1: ky - py1 + my - 2 if ky - py1 + my - 2 >= 0 else None: -1]
+            qx, qy = kx - px, ky - py
+            q2 = (qx * qx + qy * qy).astype(np.float64)
+            inv = np.where(q2 > 0, 1.0 / np.where(q2 > 0, q2, 1.0), 0.0)
+            out[o] = ((px * ky - py * kx) * inv * Wp * Wq).sum()
         return out
 
 

@@ -402,3 +402,144 @@ int orc_cconv3d_at_par(const double *f, const double *g, int64_t n0, int64_t n1,
   }
   return 0;
 }
+
+/* ------------------------------------------------ D7 sampled, line form -- */
+/* D7 at sampled outputs of a large array (config 5b, O5): the same terms as
+ * orc_hconv3d_at / orc_hconv3d_at_mirror, organised for speed without
+ * changing what is summed.  For each output k and each (px, py) with
+ * (qx, qy) = (kx - px, ky - py) in range, the z sum
+ *   sum_{pz} U^f_{px,py,pz} U^g_{qx,qy,kz-pz},   |pz|, |kz-pz| <= mz-1,
+ * with U_{.,.,-z} = conj U_{-px,-py,z} and the z = 0 entries projected
+ * (AMB-7), is cut where pz or kz - pz changes sign into runs of stored
+ * entries read in place (a = U^f_{px,py,.}, b = U^f_{-px,-py,.},
+ * c = U^g_{qx,qy,.}, d = U^g_{-qx,-qy,.}):
+ *   pz = -u < 0 (u = 1..mz-1-kz):  conj(b[u]) * c[kz+u]
+ *   pz = 0:                         P(a,b)[0] * (kz > 0 ? c[kz] : P(c,d)[0])
+ *   0 < pz < kz:                    a[pz] * c[kz-pz]
+ *   pz = kz > 0:                    a[kz] * P(c,d)[0]
+ *   kz < pz <= mz-1:                a[pz] * conj(d[pz-kz])
+ * (P(a,b)[0] = (a[0] + conj b[0])/2).  Accumulation: Ogita-Rump-Oishi Dot2
+ * (TwoProd + TwoSum: the result as if computed in twice the working
+ * precision) in 8 independent lanes, combined with Neumaier summation
+ * (AMB-20). */
+typedef struct { double p[8], s[8]; } dot8_t;
+
+#define DOT2_LANE(D, l, x, y)                                  \
+  do {                                                         \
+    double h_ = (x) * (y), r_ = fma((x), (y), -h_);            \
+    double t_ = (D)->p[l] + h_, z_ = t_ - (D)->p[l];           \
+    double q_ = ((D)->p[l] - (t_ - z_)) + (h_ - z_);           \
+    (D)->p[l] = t_;                                            \
+    (D)->s[l] += q_ + r_;                                      \
+  } while (0)
+
+static inline void cmac2(dot8_t *re, dot8_t *im, double xr, double xi, double yr, double yi) {
+  DOT2_LANE(re, 0, xr, yr);
+  DOT2_LANE(re, 0, -xi, yi);
+  DOT2_LANE(im, 0, xr, yi);
+  DOT2_LANE(im, 0, xi, yr);
+}
+
+/* sum_{j<n} (x_j^cx) (y_{SY j}^cy), x ascending, y ascending (SY = 1) or
+ * descending (SY = -1); cx, cy = +1 (as stored) or -1 (conjugate) */
+#define CDOT2_BODY(SY)                                                                   \
+  double rp[8], rs[8], ip[8], is[8];                                                     \
+  for (int l = 0; l < 8; ++l) { rp[l] = re->p[l]; rs[l] = re->s[l]; ip[l] = im->p[l]; is[l] = im->s[l]; } \
+  int64_t j = 0;                                                                         \
+  for (; j + 8 <= n; j += 8) {                                                           \
+    _Pragma("omp simd")                                                                  \
+    for (int l = 0; l < 8; ++l) {                                                        \
+      const double xr = x[2 * (j + l)], xi = cx * x[2 * (j + l) + 1];                    \
+      const double yr = y[2 * (SY) * (j + l)], yi = cy * y[2 * (SY) * (j + l) + 1];      \
+      double h, r, t, z, q;                                                              \
+      D2(rp[l], rs[l], xr, yr) D2(rp[l], rs[l], -xi, yi)                                 \
+      D2(ip[l], is[l], xr, yi) D2(ip[l], is[l], xi, yr)                                  \
+    }                                                                                    \
+  }                                                                                      \
+  for (int l = 0; l < 8; ++l) { re->p[l] = rp[l]; re->s[l] = rs[l]; im->p[l] = ip[l]; im->s[l] = is[l]; } \
+  for (; j < n; ++j)                                                                     \
+    cmac2(re, im, x[2 * j], cx * x[2 * j + 1], y[2 * (SY) * j], cy * y[2 * (SY) * j + 1]);
+#define D2(P, S, a, b) h = (a) * (b); r = fma((a), (b), -h); t = P + h; z = t - P; q = (P - (t - z)) + (h - z); P = t; S += q + r;
+static void cdot2_fwd(const double *restrict x, double cx, const double *restrict y, double cy, int64_t n,
+                      dot8_t *re, dot8_t *im) {
+  CDOT2_BODY(1)
+}
+static void cdot2_rev(const double *restrict x, double cx, const double *restrict y, double cy, int64_t n,
+                      dot8_t *re, dot8_t *im) {
+  CDOT2_BODY(-1)
+}
+#undef D2
+
+/* the z sum above for one (px, py) pair and output kz, added to (re, im) */
+static void zsum(const double *a, const double *b, const double *c, const double *d, int64_t mz, int64_t kz,
+                 dot8_t *re, dot8_t *im) {
+  const double a0r = 0.5 * (a[0] + b[0]), a0i = 0.5 * (a[1] - b[1]);   /* projected z = 0 */
+  const double c0r = 0.5 * (c[0] + d[0]), c0i = 0.5 * (c[1] - d[1]);
+  if (mz - 1 - kz > 0) cdot2_fwd(b + 2, -1.0, c + 2 * (kz + 1), 1.0, mz - 1 - kz, re, im);   /* pz < 0 */
+  if (kz > 0) {
+    cmac2(re, im, a0r, a0i, c[2 * kz], c[2 * kz + 1]);                                     /* pz = 0 */
+    if (kz > 1) cdot2_rev(a + 2, 1.0, c + 2 * (kz - 1), 1.0, kz - 1, re, im);             /* 0 < pz < kz */
+    cmac2(re, im, a[2 * kz], a[2 * kz + 1], c0r, c0i);                                     /* pz = kz */
+  } else {
+    cmac2(re, im, a0r, a0i, c0r, c0i);                                                      /* pz = kz = 0 */
+  }
+  if (mz - 1 - kz > 0) cdot2_fwd(a + 2 * (kz + 1), 1.0, d + 2, -1.0, mz - 1 - kz, re, im);   /* pz > kz */
+}
+
+/* D7 at the outputs (kx, ky, kz[t]), t < nkz, of one (kx, ky) line: the
+ * x-y loop is shared by all kz (each pair of z lines is read once for all
+ * of them -- the sampled config-5b check is memory-bound otherwise). */
+int orc_hconv3d_at_zlist(const double *f, const double *g, int64_t mx, int64_t my, int64_t mz, int64_t kx,
+                         int64_t ky, const int64_t *kz, int64_t nkz, double *out) {
+  if (mx < 1 || my < 1 || mz < 1 || nkz < 0 || kx < -(mx - 1) || kx > mx - 1 || ky < -(my - 1) || ky > my - 1)
+    return -2;
+  for (int64_t t = 0; t < nkz; ++t)
+    if (kz[t] < 0 || kz[t] > mz - 1) return -2;
+  const int64_t ny = 2 * my - 1, nth = 2 * mx - 1;
+  if (over_cap((double)nth * (double)ny * (double)(2 * mz - 1) * (double)nkz)) return -1;
+  double *part = (double *)calloc((size_t)nth * nkz * 4, sizeof(double));
+  if (!part) return -2;
+#pragma omp parallel
+  {
+    dot8_t *re = (dot8_t *)malloc(sizeof(dot8_t) * (nkz ? nkz : 1));
+    dot8_t *im = (dot8_t *)malloc(sizeof(dot8_t) * (nkz ? nkz : 1));
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t pxi = 0; pxi < nth; ++pxi) {
+      const int64_t px = pxi - (mx - 1), qx = kx - px;
+      if (qx < -(mx - 1) || qx > mx - 1) continue;
+      memset(re, 0, sizeof(dot8_t) * nkz);
+      memset(im, 0, sizeof(dot8_t) * nkz);
+      for (int64_t py = -(my - 1); py <= my - 1; ++py) {
+        const int64_t qy = ky - py;
+        if (qy < -(my - 1) || qy > my - 1) continue;
+        const double *a = f + 2 * (((px + mx - 1) * ny + (py + my - 1)) * mz);
+        const double *b = f + 2 * (((-px + mx - 1) * ny + (-py + my - 1)) * mz);
+        const double *c = g + 2 * (((qx + mx - 1) * ny + (qy + my - 1)) * mz);
+        const double *d = g + 2 * (((-qx + mx - 1) * ny + (-qy + my - 1)) * mz);
+        for (int64_t t = 0; t < nkz; ++t) zsum(a, b, c, d, mz, kz[t], &re[t], &im[t]);
+      }
+      for (int64_t t = 0; t < nkz; ++t) {
+        acc_t R = {0, 0}, I = {0, 0};
+        for (int l = 0; l < 8; ++l) {
+          acc_add(&R, re[t].p[l]); acc_add(&R, re[t].s[l]);
+          acc_add(&I, im[t].p[l]); acc_add(&I, im[t].s[l]);
+        }
+        double *q = part + 4 * (pxi * nkz + t);
+        q[0] = R.s; q[1] = R.c; q[2] = I.s; q[3] = I.c;
+      }
+    }
+    free(re); free(im);
+  }
+  for (int64_t t = 0; t < nkz; ++t) {
+    acc_t R = {0, 0}, I = {0, 0};
+    for (int64_t p = 0; p < nth; ++p) {
+      const double *q = part + 4 * (p * nkz + t);
+      acc_add(&R, q[0]); acc_add(&R, q[1]);
+      acc_add(&I, q[2]); acc_add(&I, q[3]);
+    }
+    out[2 * t] = acc_val(&R);
+    out[2 * t + 1] = acc_val(&I);
+  }
+  free(part);
+  return 0;
+}

@@ -12,6 +12,7 @@
 #include <atomic>
 
 #include "fft_dev.cuh"
+#include "launch.cuh"
 #include "kernels.cuh"
 #include "tables.cuh"
 
@@ -331,7 +332,7 @@ namespace {
 
 template <class K>
 cudaError_t launch_persistent(K kernel, int threads, size_t smem, long nrows, int groups, cudaStream_t s,
-                              void** args) {
+                              void** args, const char* tag, int m) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -342,8 +343,7 @@ cudaError_t launch_persistent(K kernel, int threads, size_t smem, long nrows, in
   long grid = (long)num_sms() * per_sm;
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
-  count_launch();
-  return cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s);
+  return launch_kernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s, {tag, m, nrows});
 }
 
 template <int M>
@@ -359,7 +359,7 @@ cudaError_t cconv_m(double2* f, double2* g, long nrows, double2* work, cudaStrea
   const double2* tw2M = zeta_table(2 * M);
   if (!twM || !tw2M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw2M, &work};
-  return launch_persistent(k_cconv_rows<M, SC::GLOBAL>, C::THREADS, SC::SMEM_BYTES, nrows, C::G, s, args);
+  return launch_persistent(k_cconv_rows<M, SC::GLOBAL>, C::THREADS, SC::SMEM_BYTES, nrows, C::G, s, args, "K2v1", M);
 }
 
 template <int M>
@@ -370,7 +370,7 @@ cudaError_t hconv_m(double2* f, double2* g, long nrows, double2* work, cudaStrea
   const double2* tw3M = zeta_table(3 * M);
   if (!twM || !tw3M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw3M, &work};
-  return launch_persistent(k_hconv_rows<M, SC::GLOBAL>, C::THREADS, SC::SMEM_BYTES, nrows, C::G, s, args);
+  return launch_persistent(k_hconv_rows<M, SC::GLOBAL>, C::THREADS, SC::SMEM_BYTES, nrows, C::G, s, args, "K3v1", M);
 }
 
 template <int M>
@@ -381,7 +381,7 @@ cudaError_t tconv_m(double2* f, double2* g, double2* h, long nrows, double2* wor
   const double2* tw4M = zeta_table(4 * M);
   if (!twM || !tw4M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &h, &nrows, &twM, &tw4M, &work};
-  return launch_persistent(k_tconv_rows<M, SC::GLOBAL>, C::THREADS, SC::SMEM_BYTES, nrows, C::G, s, args);
+  return launch_persistent(k_tconv_rows<M, SC::GLOBAL>, C::THREADS, SC::SMEM_BYTES, nrows, C::G, s, args, "K4v1", M);
 }
 
 template <int M, int STASH>

@@ -17,6 +17,8 @@ constexpr int kSlots = 3;
 struct HostPool {
   cudaStream_t s[kSlots];
   cudaEvent_t fork, done[kSlots];
+  std::mutex enq;      // held from the fork record to the last join: concurrent
+                       // host threads must not interleave their fork/join events
   bool ok = false;
 };
 
@@ -95,6 +97,7 @@ idc_status idc_conv1d_host(idc_kind k, const idc_c128* const* in_host, idc_c128*
   if ((reinterpret_cast<uintptr_t>(work) & 255u) != 0) return IDC_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   HostPool& P = host_pool();
+  std::lock_guard<std::mutex> enq(P.enq);
   const size_t arr = align256(chunk_rows * m * sizeof(idc_c128));
   const size_t per_slot = nin * arr + align256(row_work(k, (int)m));
   if (cudaEventRecord(P.fork, s) != cudaSuccess) return IDC_ERR_CUDA;

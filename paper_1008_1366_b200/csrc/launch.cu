@@ -1,0 +1,127 @@
+// launch.cu -- kernel launch + opt-in per-kernel-class profiler, see launch.cuh.
+#include <cstdio>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/idconv.h"
+#include "kernels.cuh"
+#include "launch.cuh"
+
+namespace idc {
+
+namespace {
+struct Rec {
+  const char* tag;
+  int n;
+  long units;
+  cudaEvent_t a, b;
+};
+std::mutex g_mu;
+bool g_on = false;
+std::vector<Rec> g_recs;
+std::vector<cudaEvent_t> g_free;   // recycled events
+
+cudaEvent_t get_event() {
+  if (!g_free.empty()) {
+    cudaEvent_t e = g_free.back();
+    g_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+cudaError_t launch_kernel(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s,
+                          const LaunchTag& tag) {
+  count_launch();
+  bool on;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    on = g_on;
+  }
+  if (!on) return cudaLaunchKernel(fn, grid, block, args, smem, s);
+  cudaEvent_t a, b;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    a = get_event();
+    b = get_event();
+  }
+  cudaEventRecord(a, s);
+  const cudaError_t e = cudaLaunchKernel(fn, grid, block, args, smem, s);
+  cudaEventRecord(b, s);
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_recs.push_back(Rec{tag.tag, tag.n, tag.units, a, b});
+  return e;
+}
+
+}  // namespace idc
+
+extern "C" {
+
+idc_status idc_profile_begin(void) {
+  std::lock_guard<std::mutex> lk(idc::g_mu);
+  for (auto& r : idc::g_recs) {
+    idc::g_free.push_back(r.a);
+    idc::g_free.push_back(r.b);
+  }
+  idc::g_recs.clear();
+  idc::g_on = true;
+  return IDC_OK;
+}
+
+// Aggregates the records of the last begin..end window (once) and copies the
+// text into buf; a second call with a larger buffer returns the same text.
+long idc_profile_end(char* buf, size_t len) {
+  static std::string last;
+  static bool last_ok = true;
+  std::vector<idc::Rec> recs;
+  bool had;
+  {
+    std::lock_guard<std::mutex> lk(idc::g_mu);
+    had = idc::g_on || !idc::g_recs.empty();
+    idc::g_on = false;
+    recs.swap(idc::g_recs);
+  }
+  if (had) {
+    // (tag, n) -> launches, units, ms
+    std::map<std::pair<std::string, int>, std::tuple<long, long, double>> agg;
+    bool ok = true;
+    for (auto& r : recs) {
+      float ms = 0.f;
+      if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) ok = false;
+      auto& t = agg[{r.tag, r.n}];
+      std::get<0>(t) += 1;
+      std::get<1>(t) += r.units;
+      std::get<2>(t) += ms;
+    }
+    {
+      std::lock_guard<std::mutex> lk(idc::g_mu);
+      for (auto& r : recs) {
+        idc::g_free.push_back(r.a);
+        idc::g_free.push_back(r.b);
+      }
+    }
+    last.clear();
+    char line[256];
+    for (auto& kv : agg) {
+      snprintf(line, sizeof line, "%s %d %ld %ld %.6f\n", kv.first.first.c_str(), kv.first.second,
+               std::get<0>(kv.second), std::get<1>(kv.second), std::get<2>(kv.second));
+      last += line;
+    }
+    last_ok = ok;
+  }
+  if (!last_ok) return -1;
+  if (buf && len > 0) {
+    const size_t n = last.size() < len - 1 ? last.size() : len - 1;
+    last.copy(buf, n);
+    buf[n] = 0;
+  }
+  return (long)last.size() + 1;
+}
+
+}  // extern "C"

@@ -17,6 +17,7 @@
 // HBM.  All launches are stream-ordered on the caller's stream.
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 
 #include "kernels.cuh"
 #include "nd.cuh"
@@ -69,12 +70,15 @@ int slab_streams() {
 struct Pool {
   cudaStream_t s[kMaxSlabStreams];
   cudaEvent_t fork, done[kMaxSlabStreams];
+  std::mutex enq;      // held from the fork record to the last join (concurrent callers)
   bool ok = false;
 };
 Pool& pool() {
   static Pool p[16];
+  static std::mutex mu;
   int dev = 0;
   cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
   Pool& q = p[dev & 15];
   if (!q.ok) {
     for (int i = 0; i < kMaxSlabStreams; ++i) {
@@ -219,6 +223,7 @@ cudaError_t run_cconv3d(double2* f, double2* g, int mx, int my, int mz, double2*
   const long per_elems = 2 * G * slab + (long)(cconv_rows_work_bytes(mz) / W16);
   IDC_TRY(launch_pad_bwd(f, g, U, V, mx, slab, 1, 0, 0, s));              // x: fftpadBackward over all (y,z)
   Pool& P = pool();
+  std::lock_guard<std::mutex> enq(P.enq);
   IDC_TRY(cudaEventRecord(P.fork, s));
   for (int i = 0; i < slab_streams(); ++i) IDC_TRY(cudaStreamWaitEvent(P.s[i], P.fork, 0));
   long gi = 0;
@@ -256,6 +261,7 @@ cudaError_t run_hconv3d(double2* f, double2* g, int mx, int my, int mz, double2*
   const long per_elems = 2 * G * uslab + (long)(hconv_rows_work_bytes(mz) / W16);
   IDC_TRY(launch_pad0_bwd(f, g, U, V, mx, slab, 1, 0, 0, s));             // x: fft0padBackward
   Pool& P = pool();
+  std::lock_guard<std::mutex> enq(P.enq);
   IDC_TRY(cudaEventRecord(P.fork, s));
   for (int i = 0; i < slab_streams(); ++i) IDC_TRY(cudaStreamWaitEvent(P.s[i], P.fork, 0));
   long gi = 0;

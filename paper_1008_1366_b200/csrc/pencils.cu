@@ -20,6 +20,7 @@
 //   r = +1: rows m-1..2m-2 of f;  r = 0: rows 0..m-2 of f and row m of U;
 //   r = -1: rows 0..m-1 of U.  (U has m+1 rows.)
 #include "fft_dev.cuh"
+#include "launch.cuh"
 #include "kernels.cuh"
 #include "nd_internal.cuh"
 #include "tables.cuh"
@@ -238,11 +239,10 @@ struct PTune {
 };
 
 template <class K>
-cudaError_t launchp(K kernel, int threads, size_t smem, dim3 grid, cudaStream_t s, void** args) {
+cudaError_t launchp(K kernel, int threads, size_t smem, dim3 grid, cudaStream_t s, void** args, const LaunchTag& tag) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  count_launch();
-  return cudaLaunchKernel((const void*)kernel, grid, dim3(threads), args, smem, s);
+  return launch_kernel((const void*)kernel, grid, dim3(threads), args, smem, s, tag);
 }
 
 template <int N>
@@ -256,7 +256,7 @@ cudaError_t pad_bwd_n(double2* f, double2* g, double2* U, double2* V, long ncols
   Pencil pc{ncols, bstride, ustride};
   void* args[] = {&f, &g, &U, &V, &pc, &twN, &tw2N, &ophase};
   dim3 grid((unsigned)((ncols + W - 1) / W), (unsigned)batch, g ? 2 : 1);
-  return launchp(k_pad_bwd<N, E, W>, C::THREADS, (size_t)C::XB * 16, grid, s, args);
+  return launchp(k_pad_bwd<N, E, W>, C::THREADS, (size_t)C::XB * 16, grid, s, args, {"K5s", N, ncols * batch * (g ? 2 : 1)});
 }
 
 template <int N>
@@ -270,7 +270,7 @@ cudaError_t pad_fwd_n(double2* f, const double2* U, long ncols, long batch, long
   Pencil pc{ncols, bstride, ustride};
   void* args[] = {&f, &U, &pc, &twN, &tw2N, &ophase};
   dim3 grid((unsigned)((ncols + W - 1) / W), (unsigned)batch, 1);
-  return launchp(k_pad_fwd<N, E, W>, C::THREADS, (size_t)C::XB * 16, grid, s, args);
+  return launchp(k_pad_fwd<N, E, W>, C::THREADS, (size_t)C::XB * 16, grid, s, args, {"K6s", N, ncols * batch});
 }
 
 template <int N>
@@ -284,7 +284,7 @@ cudaError_t pad0_bwd_n(double2* f, double2* g, double2* U, double2* V, long ncol
   Pencil pc{ncols, bstride, ustride};
   void* args[] = {&f, &g, &U, &V, &pc, &twN, &tw3N};
   dim3 grid((unsigned)((ncols + W - 1) / W), (unsigned)batch, g ? 2 : 1);
-  return launchp(k_pad0_bwd<N, E, W>, C::THREADS, (size_t)C::XB * 16, grid, s, args);
+  return launchp(k_pad0_bwd<N, E, W>, C::THREADS, (size_t)C::XB * 16, grid, s, args, {"K7s", N, ncols * batch * (g ? 2 : 1)});
 }
 
 template <int N>
@@ -298,7 +298,7 @@ cudaError_t pad0_fwd_n(double2* f, const double2* U, long ncols, long batch, lon
   Pencil pc{ncols, bstride, ustride};
   void* args[] = {&f, &U, &pc, &twN, &tw3N};
   dim3 grid((unsigned)((ncols + W - 1) / W), (unsigned)batch, 1);
-  return launchp(k_pad0_fwd<N, E, W>, C::THREADS, (size_t)C::XB * 16, grid, s, args);
+  return launchp(k_pad0_fwd<N, E, W>, C::THREADS, (size_t)C::XB * 16, grid, s, args, {"K8s", N, ncols * batch});
 }
 
 }  // namespace

@@ -15,6 +15,7 @@
 #include <cstring>
 
 #include "fft_dev.cuh"
+#include "launch.cuh"
 #include "kernels.cuh"
 #include "nd_internal.cuh"
 #include "tables.cuh"
@@ -358,6 +359,9 @@ k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
 #ifndef IDC_K7_TMA_STORE
 #define IDC_K7_TMA_STORE 1
 #endif
+#ifndef IDC_K7_KEEP_RAW
+#define IDC_K7_KEEP_RAW 1
+#endif
 // K8: both output halves through TMA stores (2; measured hconv3d -2.3%), U_k only
 // (1), or per-thread stores (0)
 #ifndef IDC_K8_TMA_STORE
@@ -413,6 +417,26 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
     // issued after the last residue's read.
     double2 v[E];
     const long nx = tau + gridDim.x;
+    // IDC_K7_KEEP_RAW: U_k, U_{k-m} read from the stage once into registers
+    // (the three residue splits re-read nothing) and the stage is refilled
+    // with the next tile right away, overlapping all three transforms
+    constexpr bool KEEP = IDC_K7_KEEP_RAW;
+    double2 A[KEEP ? E : 1], B[KEEP ? E : 1];
+    if constexpr (KEEP) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int k = t + T * i;
+        A[i] = stage[(N - 1 + k) * W + c];                                // U_k
+        B[i] = (i == 0 && t == 0) ? make_double2(0, 0) : stage[(k - 1) * W + c];   // U_{k-m}
+      }
+      __syncthreads();
+      if (threadIdx.x == 0 && nx < tl.ntiles) {
+        int in2; long item2, c2;
+        tile_coords(tl, nx, W, in2, item2, c2);
+        mbar_arrive_expect_tx(bar, BYTES);
+        load_rows<W, BR>(in2 == 0 ? &mf : &mg, stage, c2, 0, 2 * N - 1, item2, bar);
+      }
+    }
 #pragma unroll 1
     for (int rr = 0; rr < 3; ++rr) {
       const int r = rr - 1;
@@ -420,11 +444,11 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
       // zeta_{3m}^{rk}, k = t + T i: zeta_{3m}^{rt} x zeta_{3E}^{ri} (immediate)
       auto split = [&](int i, double2 zr) {
         const int k = t + T * i;
-        const double2 up = stage[(N - 1 + k) * W + c];                    // U_k
+        const double2 up = KEEP ? A[i] : stage[(N - 1 + k) * W + c];     // U_k
         if (i == 0 && t == 0) {
           v[i] = up;
         } else {
-          const double2 un = stage[(k - 1) * W + c];                      // U_{k-m}
+          const double2 un = KEEP ? B[i] : stage[(k - 1) * W + c];        // U_{k-m}
           v[i] = cmul(zr, cadd(up, cmul(z3, un)));
         }
       };
@@ -437,7 +461,7 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
       } else {
         for_roots<3 * E, 1, -1, E>(cconj(zt), split);
       }
-      if (rr == 2) {
+      if (!KEEP && rr == 2) {
         __syncthreads();
         if (threadIdx.x == 0 && nx < tl.ntiles) {
           int in2; long item2, c2;
@@ -639,7 +663,8 @@ k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
 namespace {
 
 template <class K>
-cudaError_t launch_t(K kernel, int threads, size_t smem, long ntiles, cudaStream_t s, void** args) {
+cudaError_t launch_t(K kernel, int threads, size_t smem, long ntiles, cudaStream_t s, void** args,
+                     const LaunchTag& tag) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 1;
@@ -648,8 +673,7 @@ cudaError_t launch_t(K kernel, int threads, size_t smem, long ntiles, cudaStream
   long grid = (long)num_sms() * per_sm;
   if (ntiles < grid) grid = ntiles;
   if (grid < 1) grid = 1;
-  count_launch();
-  return cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s);
+  return launch_kernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s, tag);
 }
 
 template <int W>
@@ -683,7 +707,7 @@ cudaError_t pad_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nco
   if (!encode_pencil_map(&mV, g ? V : U, ncols, N, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
   void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw2N, &ophase, &mU, &mV};
   const size_t smem = ((size_t)N * C::W + (k5_double_xb<N>() ? 2 : 1) * (size_t)C::XB) * 16 + 16;
-  return launch_t(k_pad_bwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
+  return launch_t(k_pad_bwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args, {"K5", N, ncols * batch * (g ? 2 : 1)});
 }
 
 template <int N>
@@ -699,7 +723,7 @@ cudaError_t pad_fwd_tma(double2* f, const double2* U, long ncols, long batch, lo
   Tiles tl = make_tiles<C::W>(ncols, batch, 1, bstride, ustride);
   void* args[] = {&mf, &mu, &f, &tl, &twN, &tw2N, &ophase};
   const size_t smem = (2 * (size_t)N * C::W + C::XB) * 16 + 32;
-  return launch_t(k_pad_fwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
+  return launch_t(k_pad_fwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args, {"K6", N, ncols * batch});
 }
 
 template <int N>
@@ -733,7 +757,7 @@ cudaError_t pad0_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nc
 #endif
   void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw3N, &sm};
   const size_t smem = ((size_t)R2 * C::W + C::XB) * 16 + 16;
-  return launch_t(k_pad0_bwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
+  return launch_t(k_pad0_bwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args, {"K7", N, ncols * batch * (g ? 2 : 1)});
 }
 
 template <int N>
@@ -754,7 +778,7 @@ cudaError_t pad0_fwd_tma(double2* f, const double2* U, long ncols, long batch, l
     return cudaErrorNotSupported;
   void* args[] = {&mf, &mu, &mu1, &f, &tl, &twN, &tw3N, &mflo, &mfhi};
   const size_t smem = (2 * (size_t)N * C::W + 32 + C::XB) * 16 + 32;
-  return launch_t(k_pad0_fwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args);
+  return launch_t(k_pad0_fwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args, {"K8", N, ncols * batch});
 }
 
 #define IDC_INST_T(N)                                                                                           \

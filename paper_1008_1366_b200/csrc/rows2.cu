@@ -10,6 +10,7 @@
 //     Stockham exchange buffer (plus, for tconv, the f*g stream products), so
 //     the row's inputs stay L1-resident for the mirrored (U_{m-k}) loads.
 #include "fft_dev.cuh"
+#include "launch.cuh"
 #include "kernels.cuh"
 #include "tables.cuh"
 #include "tma.cuh"
@@ -405,7 +406,8 @@ k_tconv_rows2(double2* __restrict__ f, double2* __restrict__ g, double2* __restr
 namespace {
 
 template <class K>
-cudaError_t launch2(K kernel, int threads, size_t smem, long nrows, int groups, cudaStream_t s, void** args) {
+cudaError_t launch2(K kernel, int threads, size_t smem, long nrows, int groups, cudaStream_t s, void** args,
+                    const char* tag, int m) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -416,8 +418,7 @@ cudaError_t launch2(K kernel, int threads, size_t smem, long nrows, int groups, 
   long grid = (long)num_sms() * per_sm;
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
-  count_launch();
-  return cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s);
+  return launch_kernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s, {tag, m, nrows});
 }
 
 // elements per thread and rows per CTA of the v2 kernels
@@ -450,7 +451,7 @@ cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s, RowS
   constexpr size_t per = (M <= IDC_ROWS2_TMA_MAX ? 2 * M : 0) + (E <= 8 ? 2 : 1) * C::XB +
                          (E > 8 && M >= IDC_K2_PARK_MIN ? M : 0);
   static_assert((size_t)G * per * 16 + (size_t)G * 8 <= 227 * 1024, "K2 configuration exceeds shared memory");
-  return launch2(k_cconv_rows2<M, E, G>, C::THREADS, (size_t)G * per * 16 + (size_t)G * 8, nrows, G, s, args);
+  return launch2(k_cconv_rows2<M, E, G>, C::THREADS, (size_t)G * per * 16 + (size_t)G * 8, nrows, G, s, args, "K2", M);
 }
 
 template <int M>
@@ -462,7 +463,7 @@ cudaError_t hconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s) {
   if (!twM || !tw3M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw3M};
   return launch2(k_hconv_rows2<M, E, G>, C::THREADS, (size_t)G * (C::XB + M + (M + 1) / 2) * 16, nrows, G, s,
-                 args);
+                 args, "K3", M);
 }
 
 template <int M>
@@ -473,7 +474,7 @@ cudaError_t tconv_rows2(double2* f, double2* g, double2* h, long nrows, cudaStre
   const double2* tw4M = zeta_table(4 * M);
   if (!twM || !tw4M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &h, &nrows, &twM, &tw4M};
-  return launch2(k_tconv_rows2<M, E, G>, C::THREADS, (size_t)G * (C::XB + 2 * M) * 16, nrows, G, s, args);
+  return launch2(k_tconv_rows2<M, E, G>, C::THREADS, (size_t)G * (C::XB + 2 * M) * 16, nrows, G, s, args, "K4", M);
 }
 
 #define IDC_INST2(M)                                                                        \

@@ -16,6 +16,7 @@
 //     parks the first residue pair's partial sum in the (already staged)
 //     global f row and finishes it with the second pair.
 #include "fft_dev.cuh"
+#include "launch.cuh"
 #include "kernels.cuh"
 #include "tables.cuh"
 #include "tma.cuh"
@@ -299,7 +300,8 @@ k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const doub
 // ================================================================ launchers ==
 namespace {
 template <class K>
-cudaError_t launch3(K kernel, int threads, size_t smem, long nrows, int groups, cudaStream_t s, void** args) {
+cudaError_t launch3(K kernel, int threads, size_t smem, long nrows, int groups, cudaStream_t s, void** args,
+                    const char* tag, int m) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   long need = (nrows + groups - 1) / groups;
@@ -309,8 +311,7 @@ cudaError_t launch3(K kernel, int threads, size_t smem, long nrows, int groups, 
   long grid = (long)num_sms() * per_sm;
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
-  count_launch();
-  return cudaLaunchKernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s);
+  return launch_kernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s, {tag, m, nrows});
 }
 }  // namespace
 
@@ -321,7 +322,7 @@ cudaError_t hconv_rows3(double2* f, double2* g, long nrows, cudaStream_t s, RowS
   const double2* tw3M = zeta_table(3 * M);
   if (!twM || !tw3M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw3M, &rs};
-  return launch3(k_hconv_rows3<M>, C::THREADS, C::SMEM, nrows, C::G, s, args);
+  return launch3(k_hconv_rows3<M>, C::THREADS, C::SMEM, nrows, C::G, s, args, "K3", M);
 }
 
 template <int M>
@@ -331,7 +332,7 @@ cudaError_t tconv_rows3(double2* f, double2* g, double2* h, long nrows, cudaStre
   const double2* tw4M = zeta_table(4 * M);
   if (!twM || !tw4M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &h, &nrows, &twM, &tw4M};
-  return launch3(k_tconv_rows3<M>, C::THREADS, C::SMEM, nrows, C::G, s, args);
+  return launch3(k_tconv_rows3<M>, C::THREADS, C::SMEM, nrows, C::G, s, args, "K4", M);
 }
 
 #define IDC_INST3(M)                                                                        \

@@ -17,6 +17,7 @@
 // Layout: pair i's rows start at f + i * istride (g likewise); row j of pair
 // i is f + i * istride + j * m.  The result goes to pair 0's rows (f).
 #include "fft_dev.cuh"
+#include "launch.cuh"
 #include "kernels.cuh"
 #include "tables.cuh"
 #include "tma.cuh"
@@ -467,8 +468,8 @@ cudaError_t hconv_dot_rows(double2* f, const double2* g, int npairs, long istrid
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
   void* args[] = {&f, &g, &npairs, &istride, &nrows, &twM, &tw3M};
-  count_launch();
-  return cudaLaunchKernel((const void*)k_hconv_dot_rows<M>, dim3((unsigned)grid), dim3(C::THREADS), args, smem, s);
+  return launch_kernel((const void*)k_hconv_dot_rows<M>, dim3((unsigned)grid), dim3(C::THREADS), args, smem, s,
+                       {"K3d", M, nrows * npairs});
 }
 
 cudaError_t launch_hconv_dot_rows(double2* f, const double2* g, int npairs, long istride, int m, long nrows,
@@ -503,8 +504,8 @@ cudaError_t cconv_dot_rows(double2* f, const double2* g, int npairs, long istrid
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
   void* args[] = {&f, &g, &npairs, &istride, &nrows, &twM, &tw2M};
-  count_launch();
-  return cudaLaunchKernel((const void*)k_cconv_dot_rows<M>, dim3((unsigned)grid), dim3(C::THREADS), args, smem, s);
+  return launch_kernel((const void*)k_cconv_dot_rows<M>, dim3((unsigned)grid), dim3(C::THREADS), args, smem, s,
+                       {"K2d", M, nrows * npairs});
 }
 
 template <int M>
@@ -521,8 +522,8 @@ cudaError_t tconv_dot_rows(double2* f, const double2* g, const double2* h, int n
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
   void* args[] = {&f, &g, &h, &npairs, &istride, &nrows, &twM, &tw4M};
-  count_launch();
-  return cudaLaunchKernel((const void*)k_tconv_dot_rows<M>, dim3((unsigned)grid), dim3(C::THREADS), args, smem, s);
+  return launch_kernel((const void*)k_tconv_dot_rows<M>, dim3((unsigned)grid), dim3(C::THREADS), args, smem, s,
+                       {"K4d", M, nrows * npairs});
 }
 
 cudaError_t launch_cconv_dot_rows(double2* f, const double2* g, int npairs, long istride, int m, long nrows,
@@ -581,8 +582,8 @@ cudaError_t cconv_pq_rows(double2* f, const double2* g, int q, long nrows, cudaS
   if (need < grid) grid = need;
   if (grid < 1) grid = 1;
   void* args[] = {&f, &g, &q, &nrows, &twM, &twqM};
-  count_launch();
-  return cudaLaunchKernel((const void*)k_cconv_pq_rows<M, P>, dim3((unsigned)grid), dim3(C::THREADS), args, smem, s);
+  return launch_kernel((const void*)k_cconv_pq_rows<M, P>, dim3((unsigned)grid), dim3(C::THREADS), args, smem, s,
+                       {"K2pq", M, nrows});
 }
 
 template <int P>
@@ -616,9 +617,9 @@ cudaError_t launch_enforce_symmetry_2d(double2* a, int mx, int my, long batch, c
   long blocks = (n + threads - 1) / threads;
   if (blocks > 4L * num_sms() * 8) blocks = 4L * num_sms() * 8;
   if (blocks < 1) blocks = 1;
-  count_launch();
-  k_enforce_symmetry_2d<<<(unsigned)blocks, threads, 0, s>>>(a, mx, my, batch);
-  return cudaGetLastError();
+  void* args[] = {&a, &mx, &my, &batch};
+  return launch_kernel((const void*)k_enforce_symmetry_2d, dim3((unsigned)blocks), dim3(threads), args, 0, s,
+                       {"Ksym", my, (long)(2 * mx - 1) * batch});
 }
 
 cudaError_t launch_advection2d_inputs(const double2* w, double2* f, double2* g, int mx, int my, cudaStream_t s) {
@@ -627,9 +628,9 @@ cudaError_t launch_advection2d_inputs(const double2* w, double2* f, double2* g, 
   long blocks = (n + threads - 1) / threads;
   if (blocks > 16L * num_sms()) blocks = 16L * num_sms();
   if (blocks < 1) blocks = 1;
-  count_launch();
-  k_advection2d_inputs<<<(unsigned)blocks, threads, 0, s>>>(w, f, g, mx, my);
-  return cudaGetLastError();
+  void* args[] = {&w, &f, &g, &mx, &my};
+  return launch_kernel((const void*)k_advection2d_inputs, dim3((unsigned)blocks), dim3(threads), args, 0, s,
+                       {"Kadv", my, (long)(2 * mx - 1)});
 }
 
 }  // namespace idc

@@ -76,8 +76,9 @@ const double2* zeta_table(int N) {
   }
   double2* d = nullptr;
   if (cudaMalloc(&d, sizeof(double2) * (size_t)N) != cudaSuccess) return nullptr;
-  if (cudaMemcpy(d, h.data(), sizeof(double2) * (size_t)N, cudaMemcpyHostToDevice) != cudaSuccess) {
-    cudaFree(d);
+  if (cudaMemcpy(d, h.data(), sizeof(double2) * (size_t)N, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {   // a pageable upload may return before its DMA lands;
+    cudaFree(d);                                  // launches on non-blocking streams are not ordered after it
     return nullptr;
   }
   g_tables[key] = d;
@@ -113,7 +114,8 @@ const double2* pass_table(int N, int E) {
   if (h.empty()) h.push_back(make_double2(1.0, 0.0));
   double2* d = nullptr;
   if (cudaMalloc(&d, sizeof(double2) * h.size()) != cudaSuccess) return nullptr;
-  if (cudaMemcpy(d, h.data(), sizeof(double2) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+  if (cudaMemcpy(d, h.data(), sizeof(double2) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {   // see zeta_table
     cudaFree(d);
     return nullptr;
   }

@@ -31,6 +31,8 @@ SIGNATURES = {
     "idc_status_string": ([_I], ctypes.c_char_p),
     "idc_version": ([], ctypes.c_char_p),
     "idc_launch_count": ([], ctypes.c_longlong),
+    "idc_profile_begin": ([], _I),
+    "idc_profile_end": ([ctypes.c_char_p, _S], ctypes.c_long),
     "idc_workspace_bytes": ([_I, _S, _S, _S, _S], _S),
     "idc_cconv1d": ([_P, _P, _S, _S, _P, _S, _P], _I),
     "idc_hconv1d": ([_P, _P, _S, _S, _P, _S, _P], _I),
@@ -116,20 +118,29 @@ def workspace_bytes(kind: int, m0: int, m1: int = 1, m2: int = 1, batch: int = 1
 _work_cache: dict = {}
 
 
-def _workspace(nbytes: int, device, work):
+def _workspace(nbytes: int, device, work, stream=None):
+    """Caller-provided workspace, or a cached one owned by the KERNEL stream.
+
+    The cache is keyed by (device, stream): calls on different streams never
+    share a work buffer (they may run concurrently).  The buffer is allocated
+    while that stream is current, so the caching allocator orders its reuse
+    after the work queued on it -- replacing a too-small buffer frees the old
+    one stream-ordered, never under a running kernel."""
     if nbytes == 0:
         return None, 0
     if work is not None:
         if work.numel() * work.element_size() < nbytes:
             raise IdcError(ERR_WORKSPACE, "workspace")
         return work, work.numel() * work.element_size()
-    key = (device, nbytes)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    key = (str(device), int(s.cuda_stream))
     w = _work_cache.get(key)
-    if w is None:
-        _work_cache.clear()
-        w = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    if w is None or w.numel() < nbytes:
+        _work_cache.pop(key, None)
+        with torch.cuda.stream(s):
+            w = torch.empty(nbytes, dtype=torch.uint8, device=device)
         _work_cache[key] = w
-    return w, nbytes
+    return w, w.numel()
 
 
 def _stream_ptr(stream, device):
@@ -143,6 +154,10 @@ def _prep(arrs):
             raise TypeError("idconv expects torch.complex128 tensors")
         if not a.is_contiguous():
             raise ValueError("idconv expects contiguous tensors")
+    # the C ABI sizes every array from f: a smaller g/h would be read and
+    # written out of bounds, so every array must have f's shape
+    if any(a.shape != arrs[0].shape for a in arrs[1:]):
+        raise ValueError(f"all arrays must have the same shape, got {[tuple(a.shape) for a in arrs]}")
     dev = arrs[0].device
     if any(a.device != dev for a in arrs):
         raise ValueError("all arrays must be on the same device")
@@ -168,7 +183,7 @@ def _run_host_1d(arrs, kind, m, batch, stream):
     nb = int(lib().idc_host_workspace_bytes(kind, m, chunk))
     if nb == 0:
         raise IdcError(ERR_UNSUPPORTED, "idc_conv1d_host")
-    w, wb = _workspace(nb + 256, device, None)
+    w, wb = _workspace(nb + 256, device, None, stream)
     base = (w.data_ptr() + 255) // 256 * 256
     ins = (ctypes.c_void_p * len(arrs))(*[a.data_ptr() for a in arrs])
     _check(lib().idc_conv1d_host(kind, ins, ctypes.c_void_p(arrs[0].data_ptr()), m, batch, chunk,
@@ -184,17 +199,27 @@ def _run(arrs, kind, sizes, batch, call, work, stream):
     if not on_dev and kind in (CCONV1D, HCONV1D, TCONV1D):
         return _run_host_1d(arrs, kind, sizes[0], batch, stream)
     if on_dev:
-        dev_arrs = arrs
         device = arrs[0].device
-    else:
-        device = torch.device("cuda", torch.cuda.current_device())
+        w, wb = _workspace(workspace_bytes(kind, *sizes, batch=batch), device, work, stream)
+        ptrs = [ctypes.c_void_p(a.data_ptr()) for a in arrs]
+        _check(call(ptrs, ctypes.c_void_p(w.data_ptr()) if w is not None else None, wb, _stream_ptr(stream, device)),
+               "idconv")
+        return arrs[0]
+    # host tensors (end-to-end path): the copies, the call and the copy back
+    # are all ordered on the kernel stream; the device temporaries are freed
+    # stream-ordered on it as well
+    device = torch.device("cuda", torch.cuda.current_device())
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    with torch.cuda.stream(s):
         dev_arrs = [a.to(device, non_blocking=True) for a in arrs]
-    w, wb = _workspace(workspace_bytes(kind, *sizes, batch=batch), device, work)
-    ptrs = [ctypes.c_void_p(a.data_ptr()) for a in dev_arrs]
-    code = call(ptrs, ctypes.c_void_p(w.data_ptr()) if w is not None else None, wb, _stream_ptr(stream, device))
-    _check(code, call.__name__ if hasattr(call, "__name__") else "idconv")
-    if not on_dev:
+        w, wb = _workspace(workspace_bytes(kind, *sizes, batch=batch), device, work, s)
+        ptrs = [ctypes.c_void_p(a.data_ptr()) for a in dev_arrs]
+        _check(call(ptrs, ctypes.c_void_p(w.data_ptr()) if w is not None else None, wb, ctypes.c_void_p(s.cuda_stream)),
+               "idconv")
         arrs[0].copy_(dev_arrs[0], non_blocking=True)
+        del dev_arrs
+    if stream is None:                      # host results are complete on return
+        s.synchronize()
     return arrs[0]
 
 
@@ -242,6 +267,8 @@ def tconv2d(f, g, h, work=None, stream=None):
     """Function tconv2 on (2mx, my) arrays (row 0 = kx -mx, read as
     zero); f rows 1..2mx-1 <- the centered Hermitian ternary convolution."""
     nx, my = f.shape[-2], f.shape[-1]
+    if nx % 2:
+        raise ValueError(f"tconv2d takes (2mx, my) arrays, got {nx} rows")
     mx = nx // 2
     L = lib()
     return _run([f, g, h], TCONV2D, (mx, my, 1), 1,
@@ -251,6 +278,8 @@ def tconv2d(f, g, h, work=None, stream=None):
 def hconv2d(f, g, work=None, stream=None):
     """Function conv2 on (2mx-1, my); f <- result."""
     nx, my = f.shape[-2], f.shape[-1]
+    if nx % 2 == 0 or f.dim() != 2:
+        raise ValueError(f"hconv2d takes one (2mx-1, my) array pair, got shape {tuple(f.shape)}")
     mx = (nx + 1) // 2
     L = lib()
     return _run([f, g], HCONV2D, (mx, my, 1), 1,
@@ -261,7 +290,9 @@ def hconv2d(f, g, work=None, stream=None):
 
 def cconv3d(f, g, work=None, stream=None):
     """Function cconv3 on (mx, my, mz); f <- result."""
-    mx, my, mz = f.shape[-3:]
+    if f.dim() != 3:
+        raise ValueError(f"cconv3d takes one (mx, my, mz) array pair, got shape {tuple(f.shape)}")
+    mx, my, mz = f.shape
     L = lib()
     return _run([f, g], CCONV3D, (mx, my, mz), 1,
                 lambda p, w, wb, s: L.idc_cconv3d(p[0], p[1], mx, my, mz, w, wb, s), work, stream)
@@ -270,6 +301,8 @@ def cconv3d(f, g, work=None, stream=None):
 def hconv3d(f, g, work=None, stream=None):
     """Centered Hermitian 3D (AMB-9) on (2mx-1, 2my-1, mz)."""
     nx, ny, mz = f.shape[-3:]
+    if nx % 2 == 0 or ny % 2 == 0 or f.dim() != 3:
+        raise ValueError(f"hconv3d takes one (2mx-1, 2my-1, mz) array pair, got shape {tuple(f.shape)}")
     mx, my = (nx + 1) // 2, (ny + 1) // 2
     L = lib()
     return _run([f, g], HCONV3D, (mx, my, mz), 1,
@@ -285,6 +318,26 @@ def fill_uniform(out, array_id: int, seed: int, start: int = 0, stream=None):
         raise ValueError("fill_uniform writes device memory")
     _check(lib().idc_fill_uniform(ctypes.c_void_p(out.data_ptr()), out.numel(), seed, array_id, start,
                                   _stream_ptr(stream, out.device)), "idc_fill_uniform")
+    return out
+
+
+def profile_begin():
+    """Start the library's per-kernel-class event profiler (idc_profile_begin)."""
+    _check(lib().idc_profile_begin(), "idc_profile_begin")
+
+
+def profile_end() -> list:
+    """Stop it; returns [{"tag", "n", "launches", "units", "ms"}] per kernel class."""
+    L = lib()
+    need = int(L.idc_profile_end(None, 0))
+    if need < 0:
+        raise IdcError(ERR_CUDA, "idc_profile_end")
+    buf = ctypes.create_string_buffer(max(need, 1))
+    L.idc_profile_end(buf, len(buf))   # same text (kept by the library until the next window)
+    out = []
+    for line in buf.value.decode().splitlines():
+        tag, n, launches, units, ms = line.split()
+        out.append(dict(tag=tag, n=int(n), launches=int(launches), units=int(units), ms=float(ms)))
     return out
 
 
@@ -337,7 +390,7 @@ def cconv2d_dot(f, g, work=None, stream=None):
     nb = int(lib().idc_dot_workspace_bytes(CCONV2D, M, mx, my))
     if nb == 0:
         raise IdcError(ERR_UNSUPPORTED, "idc_cconv2d_dot")
-    w, wb = _workspace(nb, f.device, work)
+    w, wb = _workspace(nb, f.device, work, stream)
     _check(lib().idc_cconv2d_dot(ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(g.data_ptr()), M, mx, my,
                                  ctypes.c_void_p(w.data_ptr()), wb, _stream_ptr(stream, f.device)), "idc_cconv2d_dot")
     return f[0]
@@ -364,7 +417,7 @@ def hconv2d_dot(f, g, work=None, stream=None):
     nb = int(lib().idc_dot_workspace_bytes(HCONV2D, M, mx, my))
     if nb == 0:
         raise IdcError(ERR_UNSUPPORTED, "idc_hconv2d_dot")
-    w, wb = _workspace(nb, f.device, work)
+    w, wb = _workspace(nb, f.device, work, stream)
     _check(lib().idc_hconv2d_dot(ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(g.data_ptr()), M, mx, my,
                                  ctypes.c_void_p(w.data_ptr()), wb, _stream_ptr(stream, f.device)), "idc_hconv2d_dot")
     return f[0]
@@ -385,13 +438,16 @@ def advection2d(w, out=None, work=None, stream=None):
      on a (2mx-1, my) centered Hermitian vorticity spectrum."""
     _need_cuda([w])
     nx, my = w.shape
+    if nx % 2 == 0:
+        raise ValueError(f"advection2d takes a (2mx-1, my) array, got {tuple(w.shape)}")
     mx = (nx + 1) // 2
     if out is None:
         out = torch.empty_like(w)
+    _need_cuda([w, out])
     nb = int(lib().idc_advection2d_workspace_bytes(mx, my))
     if nb == 0:
         raise IdcError(ERR_UNSUPPORTED, "idc_advection2d")
-    wk, wb = _workspace(nb, w.device, work)
+    wk, wb = _workspace(nb, w.device, work, stream)
     _check(lib().idc_advection2d(ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(out.data_ptr()), mx, my,
                                  ctypes.c_void_p(wk.data_ptr()), wb, _stream_ptr(stream, w.device)), "idc_advection2d")
     return out
@@ -439,11 +495,15 @@ class Comm:
 
 
 def _dist(kind, name, comm, f, g, mx, my, mz, work, stream):
-    _prep([f, g])
+    _need_cuda([f, g])
+    planes = 2 * mx if kind == HCONV3D else mx
+    want = (planes // comm.size, 2 * my - 1 if kind == HCONV3D else my, mz)
+    if planes % comm.size or tuple(f.shape) != want:
+        raise ValueError(f"{name}: this rank's slab must have shape {want}, got {tuple(f.shape)}")
     nb = int(lib().idc_dist_workspace_bytes(kind, mx, my, mz, comm.size))
     if nb == 0:
         raise IdcError(ERR_UNSUPPORTED, name)
-    w, wb = _workspace(nb, f.device, work)
+    w, wb = _workspace(nb, f.device, work, stream)
     _check(getattr(lib(), name)(comm.handle, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(g.data_ptr()),
                                 mx, my, mz, ctypes.c_void_p(w.data_ptr()), wb, _stream_ptr(stream, f.device)), name)
     return f
@@ -466,6 +526,8 @@ def _emulated(kind, name, f_slabs, g_slabs, mx, my, mz, stream):
     nb = int(lib().idc_dist_emulated_workspace_bytes_kind(kind, mx, my, mz, P))
     if nb == 0:
         raise IdcError(ERR_UNSUPPORTED, name)
+    if len(g_slabs) != P:
+        raise ValueError("one g slab per f slab")
     w = torch.empty(nb, dtype=torch.uint8, device=f_slabs[0].device)
     fp = (ctypes.c_void_p * P)(*[a.data_ptr() for a in f_slabs])
     gp = (ctypes.c_void_p * P)(*[a.data_ptr() for a in g_slabs])

@@ -56,6 +56,25 @@ def test_euler_sum_is_minus_the_papers_call():
     assert rel_l2(call, -application.euler_sum(w)) < 1e-14
 
 
+@pytest.mark.parametrize("mx,my", [(1, 1), (2, 3), (5, 4), (7, 9)])
+def test_euler_sum_at_equals_euler_sum(mx, my):
+    """The sliced large-size evaluation sums the same terms as euler_sum."""
+    w = synthgen.hconv2d_inputs(mx, my, roles=(0,))[0]
+    ref = application.euler_sum(w).reshape(-1)
+    idx = np.arange(ref.size)
+    assert np.abs(application.euler_sum_at(w, idx) - ref).max() <= 1e-15 * max(np.abs(ref).max(), 1.0)
+
+
+def test_euler_sum_at_two_modes_closed_form():
+    mx, my = 6, 6
+    p, q, a, b = (1, 1), (2, 3), 0.3 - 0.4j, 0.5 + 0.1j
+    w = _mode_field(mx, my, [(p[0], p[1], a), (q[0], q[1], b)])
+    k = (p[0] + q[0], p[1] + q[1])
+    ref = (p[0] * q[1] - p[1] * q[0]) * (1.0 / (q[0] ** 2 + q[1] ** 2) - 1.0 / (p[0] ** 2 + p[1] ** 2)) * a * b
+    S = application.euler_sum_at(w, [(k[0] + mx - 1) * my + k[1]])
+    assert abs(S[0] - ref) < 1e-15
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("m,B,M", [(2, 3, 1), (16, 3, 2), (512, 5, 3), (4096, 2, 2)])
 def test_hconv1d_dot_gpu(m, B, M):
@@ -165,3 +184,50 @@ def test_dot_2d_tiny_gpu(mx, my):
     out = idconv.advection2d(torch.from_numpy(w.copy()).cuda()).cpu().numpy()
     ref = -application.euler_sum(w)
     assert np.linalg.norm(out - ref) <= 1e-13 * max(np.linalg.norm(ref), 1.0)
+
+
+# ------------------------------------------- dot products at TMA pencil sizes --
+# x axes of 64..4096 points run the TMA pencil kernels K7/K8 on 2*M arrays
+# (K3d rows between them): element by element at 64^2 / 128 x 64, sampled at
+# the c4adv benchmark size 2048^2.
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mx,my,M", [(64, 64, 2), (128, 64, 3), (64, 512, 2)])
+def test_hconv2d_dot_tma_gpu(mx, my, M):
+    import torch
+    from paper_1008_1366_b200 import idconv
+    fs = [synthgen.hconv2d_inputs(mx, my, roles=(2 * i, 2 * i + 1)) for i in range(M)]
+    F = torch.from_numpy(np.stack([a for a, b in fs])).cuda()
+    G = torch.from_numpy(np.stack([b for a, b in fs])).cuda()
+    idconv.hconv2d_dot(F, G)
+    ref = sum(direct.hconv2d(a, b) for a, b in fs)
+    assert rel_l2(F[0].cpu().numpy(), ref) < 1e-14
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mx,my", [(64, 64), (128, 32)])
+def test_advection2d_tma_gpu(mx, my):
+    import torch
+    from paper_1008_1366_b200 import idconv
+    w = synthgen.hconv2d_inputs(mx, my, roles=(0,))[0]
+    out = idconv.advection2d(torch.from_numpy(w.copy()).cuda()).cpu().numpy()
+    assert rel_l2(out, -application.euler_sum(w)) < 1e-13
+
+
+@pytest.mark.gpu
+def test_advection2d_c4adv_sampled_gpu():
+    """The c4adv benchmark workload (mx = my = 2048): sampled outputs plus the
+    corners and the block around the origin vs the oracle's Euler sum."""
+    import torch
+    from paper_1008_1366_b200 import idconv
+    mx = my = 2048
+    w = synthgen.hconv2d_inputs(mx, my, roles=(0,))[0]
+    out = idconv.advection2d(torch.from_numpy(w.copy()).cuda()).cpu().numpy().reshape(-1)
+    shape = w.shape
+    rs = np.random.default_rng(17)
+    pts = [(0, 0), (0, my - 1), (2 * mx - 2, 0), (2 * mx - 2, my - 1), (mx - 1, 0), (mx - 1, 1), (mx, 0),
+           (mx - 2, 1), (mx, 2), (mx - 1, my - 1)]
+    idx = np.unique(np.concatenate([[np.ravel_multi_index(p, shape) for p in pts],
+                                    rs.choice(w.size, 20, replace=False)]).astype(np.int64))
+    ref = -application.euler_sum_at(w, idx)
+    assert rel_l2(out[idx], ref) < 1e-13

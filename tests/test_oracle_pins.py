@@ -442,6 +442,33 @@ def test_large_sampled_oracles_agree(rng):
     assert rel_l2(direct.cconv3d_at_large(a, b, idx), direct.cconv_nd_at(a, b, idx)) < 1e-15
 
 
+@pytest.mark.parametrize("ms", [(1, 1, 1), (4, 3, 5), (2, 5, 9), (3, 2, 1), (5, 6, 7), (2, 2, 16)])
+def test_hconv3d_at_lines_equals_plain(ms):
+    """The z-run / Dot2 sampled D7 (O5 for config 5b) sums the same terms as
+    the plain extended-array loop: agreement to rounding at every output."""
+    f, g = synthgen.hconv3d_inputs(*ms)
+    idx = np.arange(f.size)
+    assert rel_l2(direct.hconv3d_at_lines(f, g, idx), direct.hconv3d_at(f, g, idx)) < 1e-15
+
+
+def test_hconv3d_at_lines_closed_family_and_scipy(rng):
+    """Pinned against the closed form (2mx-1-|kx|)(2my-1-|ky|)(2mz-1-kz) FG
+    e^{i(kx+ky+kz)} and against scipy's direct convolution of the extended
+    arrays, independently of the plain loop."""
+    f, g, H = closed.hconv_nd((6, 5, 12))
+    idx = np.arange(f.size)
+    assert rel_l2(direct.hconv3d_at_lines(f, g, idx), H.reshape(-1)) < 1e-15
+    mx, my, mz = 3, 2, 5
+    X = crand(rng, 2 * mx - 1, 2 * my - 1, 2 * mz - 1)
+    X = 0.5 * (X + np.conj(X[::-1, ::-1, ::-1]))
+    Y = crand(rng, 2 * mx - 1, 2 * my - 1, 2 * mz - 1)
+    Y = 0.5 * (Y + np.conj(Y[::-1, ::-1, ::-1]))
+    ref = scipy.signal.convolve(X, Y, method="direct")[mx - 1: 3 * mx - 2, my - 1: 3 * my - 2, 2 * mz - 2: 3 * mz - 2]
+    a, b = X[:, :, mz - 1:].copy(), Y[:, :, mz - 1:].copy()
+    idx = np.arange(a.size)
+    assert rel_l2(direct.hconv3d_at_lines(a, b, idx), ref.reshape(-1)) < 1e-14
+
+
 def test_fast_generator_bitwise():
     for aid, start, n in [(0, 0, 1000), (9, 77, 5000)]:
         assert np.array_equal(synthgen.uniform_complex_fast(n, aid, start=start),

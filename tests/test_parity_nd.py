@@ -6,8 +6,9 @@ import numpy as np
 import pytest
 import torch
 
+import oracle
 import synthgen
-from oracle import closed, direct, rel_l2
+from oracle import closed, direct, explicit, rel_l2
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-14
@@ -148,13 +149,36 @@ def test_config4_hconv2d_2048(idc):
     assert rel_l2(out, direct.hconv2d_at(f, g, idx)) < TOL
 
 
+def c5_sample(shape, centered, n_lines=64, per_line=8, seed=23):
+    """O5 sample of a 3D output: n_lines random (x, y)
+    lines with per_line random z each (>= 512 random outputs; outputs that
+    share (x, y) share the oracle's pass over the x-y plane), plus every
+    corner / edge / center point -- each axis at its extremes and its origin
+    (0, m-1 for complex axes; -(m-1), 0, m-1 for centered ones) with z at
+    0, 1, m-1."""
+    rs = np.random.default_rng(seed)
+    nx, ny, nz = shape
+    i = rs.integers(0, nx, n_lines)
+    j = rs.integers(0, ny, n_lines)
+    rand = [np.ravel_multi_index((np.full(per_line, a), np.full(per_line, b),
+                                  rs.choice(nz, per_line, replace=False)), shape) for a, b in zip(i, j)]
+    def ext(n, c):
+        return [0, (n - 1) // 2, n - 1] if c else [0, n - 1]
+    edge = [np.ravel_multi_index((a, b, c), shape) for a in ext(nx, centered) for b in ext(ny, centered)
+            for c in sorted({0, min(1, nz - 1), nz - 1})]
+    return np.unique(np.concatenate(rand + [np.asarray(edge)]).astype(np.int64))
+
+
 def test_config5a_cconv3d_512(idc):
-    """C5a at full size (512^3, scaled 1/(1+|k|^2)); sampled outputs vs direct sums."""
+    """C5a at full size (512^3, scaled 1/(1+|k|^2)) in the bench's launch
+    configuration; >= 512 sampled outputs + corners/edges vs direct sums."""
     m = 512
     f, g = synthgen.cconv3d_inputs(m, m, m)
     F, G = dev(f), dev(g)
     idc.cconv3d(F, G)
-    idx = sample_idx((m, m, m), 6, origin=(0, 0, 0))
+    idx = c5_sample(f.shape, centered=False)
+    assert idx.size >= 512 + 8
+    oracle.set_work_cap(1e12)
     out = F.cpu().numpy().reshape(-1)[idx]
     del F, G
     torch.cuda.empty_cache()
@@ -162,22 +186,48 @@ def test_config5a_cconv3d_512(idc):
 
 
 def test_config5b_hconv3d_512(idc):
-    """C5b at full size ((2*512-1)^2 x 512 Hermitian, scaled); sampled outputs."""
+    """C5b at full size ((2*512-1)^2 x 512 Hermitian, scaled); >= 512 sampled
+    outputs + corners/edges vs direct sums (O5, Dot2-compensated)."""
     m = 512
     f, g = synthgen.hconv3d_inputs(m, m, m)
     F, G = dev(f), dev(g)
     idc.hconv3d(F, G)
-    shape = f.shape
-    rs = np.random.default_rng(5)
-    idx = np.unique(np.concatenate([
-        [np.ravel_multi_index((m - 1, m - 1, 0), shape), np.ravel_multi_index((m - 1, m - 1, 1), shape),
-         np.ravel_multi_index((m, m - 2, 0), shape), np.ravel_multi_index((0, 0, 0), shape),
-         np.ravel_multi_index((2 * m - 2, 2 * m - 2, m - 1), shape)],
-        rs.choice(f.size, 3, replace=False)]).astype(np.int64))
+    idx = c5_sample(f.shape, centered=True)
+    assert idx.size >= 512 + 18
+    oracle.set_work_cap(1e13)
     out = F.cpu().numpy().reshape(-1)[idx]
     del F, G
     torch.cuda.empty_cache()
-    assert rel_l2(out, direct.hconv3d_at_large(f, g, idx)) < TOL
+    assert rel_l2(out, direct.hconv3d_at_lines(f, g, idx)) < TOL
+
+
+# ------------------------------- 3D on the TMA pencils, element by element --
+# Every axis of 64..4096 points runs the TMA pencil kernels (K5/K6 complex,
+# K7/K8 centered) and 512-point z rows run the config-5 row kernels (K2/K3);
+# these sizes reach each of them on x, y and z, element by element against
+# the oracle's naive-DFT explicitly padded convolution (O2).
+
+@pytest.mark.parametrize("shape", [(64, 64, 64), (128, 64, 64), (64, 128, 32), (512, 8, 8), (8, 512, 8),
+                                   (8, 8, 512), (256, 64, 8)])
+def test_cconv3d_tma_vs_explicit(idc, shape):
+    f, g = synthgen.cconv3d_inputs(*shape)
+    ref = explicit.cconv3d(f, g)
+    F, G = dev(f), dev(g)
+    idc.cconv3d(F, G)
+    assert rel_l2(F.cpu().numpy(), ref) < TOL
+
+
+@pytest.mark.parametrize("ms", [(64, 64, 32), (32, 64, 64), (512, 4, 4), (4, 512, 4), (4, 4, 512), (64, 64, 16),
+                                (128, 64, 8)])
+def test_hconv3d_tma_vs_explicit(idc, ms):
+    f, g = synthgen.hconv3d_inputs(*ms)
+    ref = explicit.hconv3d(f, g)
+    F, G = dev(f), dev(g)
+    idc.hconv3d(F, G)
+    out = F.cpu().numpy()
+    assert rel_l2(out, ref) < TOL
+    p = out[:, :, 0]                          # kz = 0 plane stays Hermitian (P:774, S:419)
+    assert np.max(np.abs(p - np.conj(p[::-1, ::-1]))) < 1e-13 * np.max(np.abs(out))
 
 
 # ------------------------------------------------ tall pencils (m >= 1024) --
