@@ -348,17 +348,23 @@ def call(idc, p, arrs):
     return getattr(idc, p["kind"])(*arrs)
 
 
-def kernel_table(p, prof, steps, pk, traffic):
+def kernel_table(p, prof, steps, pk, traffic, step_ms):
     """Per-kernel-class device time of one call and its achieved algorithmic
-    bytes / flops (DESIGN.md section 6 models)."""
+    bytes / flops (DESIGN.md section 6 models).  The 3D calls run slab groups
+    on concurrent streams, so their kernels' event times overlap and sum to
+    more than the step; each kernel is then attributed its share of the step
+    (ms_attributed = step x share), and achieved = its algorithmic bytes or
+    flops / ms_attributed."""
     tot = sum(r["ms"] for r in prof) or 1.0
+    overlap = max(1.0, tot / steps / step_ms)
     rows = []
     for r in prof:
         b_u, f_u = kernel_model(r["tag"], r["n"])
         d = dict(kernel=f"{r['tag']}<{r['n']}>", launches_per_call=r["launches"] / steps,
-                 ms_per_call=r["ms"] / steps, share=r["ms"] / tot, units_per_launch=r["units"] / r["launches"])
+                 ms_per_call=r["ms"] / steps, share=r["ms"] / tot, units_per_launch=r["units"] / r["launches"],
+                 ms_attributed=r["ms"] / steps / overlap, overlap=overlap)
         if b_u is not None:
-            sec = r["ms"] / 1e3
+            sec = r["ms"] / overlap / 1e3
             d["hbm_gbs_alg"] = b_u * r["units"] / sec / 1e9
             d["fp64_tflops_alg"] = f_u * r["units"] / sec / 1e12
             d["hbm_frac"] = d["hbm_gbs_alg"] / pk["hbm_gbs"]
@@ -459,7 +465,7 @@ def measure(idc, torch, tdist, name, args, rank, ws, dev, comm=None, want_e2e=Fa
     ngpu_peak = ws
     t_b = b * convs / (pk["hbm_gbs"] * 1e9 * ngpu_peak)
     t_f = fl * convs / (pk["fp64_tflops"] * 1e12 * ngpu_peak)
-    kt = kernel_table(p, prof, args.steps, pk, load_traffic())
+    kt = kernel_table(p, prof, args.steps, pk, load_traffic(), sec * 1e3)
     out = dict(config=name, workload=p["desc"], kind=p["kind"], m=p["m"], batch=p["batch"],
                scaling="strong" if dist3d else "weak", ms_per_call=sec * 1e3, call_stats=timing_stats(samples),
                conv_per_s=convs / sec, hbm_gbs_alg=b * convs / sec / 1e9, fp64_tflops_alg=fl * convs / sec / 1e12,

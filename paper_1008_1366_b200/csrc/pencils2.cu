@@ -13,6 +13,7 @@
 #include <cuda.h>
 
 #include <cstring>
+#include <type_traits>
 
 #include "fft_dev.cuh"
 #include "launch.cuh"
@@ -100,6 +101,15 @@ template <int N>
 using K78Cfg = TCfg<N, (k78_wide<N>() ? (k78_narrow<N>() ? 128 : 256)
                                       : IDC_PENCIL0_THREADS),
                    (k78_wide<N>() ? 16 : IDC_PENCIL_E)>;
+
+// K8 alone: E = 8 with 512-thread CTAs for m <= IDC_K8_E8_MAX (three live
+// E-vectors -- the stream being transformed and the U_k / U_{k-m}
+// accumulators -- fit 128 registers at E = 8; at E = 16 they spill)
+#ifndef IDC_K8_E8_MAX
+#define IDC_K8_E8_MAX 0
+#endif
+template <int N>
+using K8Cfg = std::conditional_t<(N <= IDC_K8_E8_MAX && N >= 64), TCfg<N, 512, 8>, K78Cfg<N>>;
 
 template <int W>
 struct Slot2 {
@@ -512,12 +522,12 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
 // 0..N-1), q = 1 (r = 0: f rows 0..N-2 and U row N, the latter through a
 // one-row box into a separate tail slot), q = 2 (r = +1: f rows N-1..2N-2).
 template <int N>
-__global__ void __launch_bounds__(K78Cfg<N>::THREADS, IDC_PENCIL_MINB)
+__global__ void __launch_bounds__(K8Cfg<N>::THREADS, IDC_PENCIL_MINB)
 k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mu,
                const __grid_constant__ CUtensorMap mu1, double2* __restrict__ f, Tiles tl,
                const double2* __restrict__ twN, const double2* __restrict__ tw3N,
                const __grid_constant__ CUtensorMap mflo, const __grid_constant__ CUtensorMap mfhi) {
-  using C = K78Cfg<N>;
+  using C = K8Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   extern __shared__ __align__(128) double2 smem[];
   double2* st[2] = {smem, smem + N * W};
@@ -763,7 +773,7 @@ cudaError_t pad0_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nc
 template <int N>
 cudaError_t pad0_fwd_tma(double2* f, const double2* U, long ncols, long batch, long bstride, long ustride,
                          cudaStream_t s) {
-  using C = K78Cfg<N>;
+  using C = K8Cfg<N>;
   const double2* twN = pass_table(N, C::E);
   const double2* tw3N = zeta_table(3 * N);
   if (!twN || !tw3N) return cudaErrorMemoryAllocation;

@@ -21,6 +21,12 @@
 #include "tables.cuh"
 #include "tma.cuh"
 
+// K3: elements per thread up to which all three residue streams come from one
+// read of the staged row (the r = -1 stream held in registers)
+#ifndef IDC_K3_ONE_SPLIT_MAXE
+#define IDC_K3_ONE_SPLIT_MAXE 8
+#endif
+
 namespace idc {
 
 namespace {
@@ -104,22 +110,41 @@ k_hconv_rows3(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
     phase ^= 1;
     double2 v[E], Q[E];
     double p0[E];
-    // residues r = 0 and r = 1 from ONE read of the staged pair:
-    // P_k = f_k + i g_k, R_k = conj f_{m-k} + i conj g_{m-k};
-    // v = P + R (r = 0), Q = zeta_{3m}^{k} (P + zeta_3^{-1} R) (r = 1)
-    const double2 c1 = make_double2(-0.5, -s3);                 // zeta_3^{-1}
+    // ONE: all three residue streams from one read of the staged pair, the
+    // r = -1 stream kept in registers (E <= 8: room below 255 registers);
+    // halves the split's shared-memory wavefronts and frees the stage for
+    // the next row's bulk copy before the first transform
+    constexpr bool ONE = E <= IDC_K3_ONE_SPLIT_MAXE;
+    double2 Vm[ONE ? E : 1];
+    // residues r = 0 and r = 1 (and r = -1) from ONE read of the staged pair
+    // (P:531-537): P_k = f_k + i g_k, R_k = conj f_{m-k} + i conj g_{m-k};
+    // v = P + R (r = 0), Q = zeta_{3m}^{k} (P + zeta_3^{-1} R) (r = 1),
+    // Vm = zeta_{3m}^{-k} (P + zeta_3 R) (r = -1); with A = P - R/2 and
+    // B = i (sqrt 3 / 2) R: P + zeta_3^{-1} R = A - B, P + zeta_3 R = A + B
     for_roots<3 * E, 1, +1, E>(ldtw(&tw3M[t]), [&](int i, double2 zr) {
       const int k = t + T * i;
       if (i == 0 && t == 0) {
         v[i] = Q[i] = make_double2(F[0].x, Gs[0].x);              // w_{0,r} = Re U_0 (AMB-7)
+        if constexpr (ONE) Vm[i] = v[i];
       } else {
         const double2 fk = F[k], gk = Gs[k], fm = F[M - k], gm = Gs[M - k];
         const double2 P = make_double2(fk.x - gk.y, fk.y + gk.x);
         const double2 R = make_double2(fm.x + gm.y, gm.x - fm.y);
         v[i] = cadd(P, R);
-        Q[i] = cmul(zr, cadd(P, cmul(c1, R)));
+        const double2 A = make_double2(fma(-0.5, R.x, P.x), fma(-0.5, R.y, P.y));
+        const double2 B = make_double2(-s3 * R.y, s3 * R.x);
+        Q[i] = cmul(zr, csub(A, B));
+        if constexpr (ONE) Vm[i] = cmulc(cadd(A, B), zr);          // conj(zeta^k) (A + B)
       }
     });
+    if constexpr (ONE) {
+      sync();
+      if (t == 0 && row + stride < nrows) {
+        mbar_arrive_expect_tx(bar, 2u * M * 16u);
+        tma_load_1d(F, row_ptr(f, rs.f1, rs.n0, row + stride, M), M * 16u, bar);
+        tma_load_1d(Gs, row_ptr(g, rs.g1, rs.n0, row + stride, M), M * 16u, bar);
+      }
+    }
     fft<M, E, +1>(v, t, xb, twM, sync);                         // two c2r in one complex FFT
 #pragma unroll
     for (int i = 0; i < E; ++i) p0[i] = v[i].x * v[i].y;
@@ -127,17 +152,22 @@ k_hconv_rows3(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
 #pragma unroll
     for (int i = 0; i < E; ++i) Q[i] = make_double2(p0[i], Q[i].x * Q[i].y);
     fft<M, E, -1>(Q, t, xb, twM, sync);                         // Q = fft(p_0 + i p_1)
-    // r = -1: the last read of the staged row, then the next row's bulk copy
-    const double2 cm = make_double2(-0.5, s3);                  // zeta_3^{+1}
-    for_roots<3 * E, 1, -1, E>(cconj(ldtw(&tw3M[t])), [&](int i, double2 zr) {
-      if (i == 0 && t == 0) v[i] = make_double2(F[0].x, Gs[0].x);
-      else v[i] = zpair(F, Gs, t + T * i, M - t - T * i, zr, cm);
-    });
-    sync();
-    if (t == 0 && row + stride < nrows) {
-      mbar_arrive_expect_tx(bar, 2u * M * 16u);
-      tma_load_1d(F, row_ptr(f, rs.f1, rs.n0, row + stride, M), M * 16u, bar);
-      tma_load_1d(Gs, row_ptr(g, rs.g1, rs.n0, row + stride, M), M * 16u, bar);
+    if constexpr (ONE) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) v[i] = Vm[i];
+    } else {
+      // r = -1: the last read of the staged row, then the next row's bulk copy
+      const double2 cm = make_double2(-0.5, s3);                // zeta_3^{+1}
+      for_roots<3 * E, 1, -1, E>(cconj(ldtw(&tw3M[t])), [&](int i, double2 zr) {
+        if (i == 0 && t == 0) v[i] = make_double2(F[0].x, Gs[0].x);
+        else v[i] = zpair(F, Gs, t + T * i, M - t - T * i, zr, cm);
+      });
+      sync();
+      if (t == 0 && row + stride < nrows) {
+        mbar_arrive_expect_tx(bar, 2u * M * 16u);
+        tma_load_1d(F, row_ptr(f, rs.f1, rs.n0, row + stride, M), M * 16u, bar);
+        tma_load_1d(Gs, row_ptr(g, rs.g1, rs.n0, row + stride, M), M * 16u, bar);
+      }
     }
     fft<M, E, +1>(v, t, xb, twM, sync);
 #pragma unroll
