@@ -431,19 +431,12 @@ size_t tconv_rows_work_bytes(int m) {
   return 0;
 }
 
-// m = 512 rows on the warp-resident FFT (rows512w.cu) instead of K2 / K3
-#ifndef IDC_ROWS512W
-#define IDC_ROWS512W 0
-#endif
-
 cudaError_t launch_cconv_rows(double2* f, double2* g, int m, long nrows, double2* work, cudaStream_t s) {
-  if (IDC_ROWS512W && m == 512) return cconv_rows512w(f, g, nrows, s);
   if (m <= IDC_V2_MAX_M) { IDC_DISPATCH_M(m, return cconv_rows2<MM>(f, g, nrows, s)); }
   IDC_DISPATCH_M(m, return cconv_m<MM>(f, g, nrows, work, s));
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_hconv_rows(double2* f, double2* g, int m, long nrows, double2* work, cudaStream_t s) {
-  if (IDC_ROWS512W && m == 512) return hconv_rows512w(f, g, nrows, s);
   if (m >= IDC_V3_MIN_M && m <= 4096) {
     switch (m) {
       case 512: return hconv_rows3<512>(f, g, nrows, s);
@@ -476,7 +469,6 @@ cudaError_t launch_tconv_rows(double2* f, double2* g, double2* h, int m, long nr
 cudaError_t launch_cconv_rows_sets(double2* f, double2* g, long n0, double2* f1, double2* g1, long n1, int m,
                                    double2* work, cudaStream_t s) {
   RowSets rs{f1, g1, n0};
-  if (IDC_ROWS512W && m == 512) return cconv_rows512w(f, g, n0 + n1, s, rs);
   if (m <= IDC_V2_MAX_M) { IDC_DISPATCH_M(m, return cconv_rows2<MM>(f, g, n0 + n1, s, rs)); }
   cudaError_t e = launch_cconv_rows(f, g, m, n0, work, s);
   return e != cudaSuccess ? e : launch_cconv_rows(f1, g1, m, n1, work, s);
@@ -484,7 +476,6 @@ cudaError_t launch_cconv_rows_sets(double2* f, double2* g, long n0, double2* f1,
 cudaError_t launch_hconv_rows_sets(double2* f, double2* g, long n0, double2* f1, double2* g1, long n1, int m,
                                    double2* work, cudaStream_t s) {
   RowSets rs{f1, g1, n0};
-  if (IDC_ROWS512W && m == 512) return hconv_rows512w(f, g, n0 + n1, s, rs);
   if (m >= IDC_V3_MIN_M && m <= 4096) {
     switch (m) {
       case 512: return hconv_rows3<512>(f, g, n0 + n1, s, rs);

@@ -48,11 +48,6 @@ template <int M> cudaError_t tconv_rows2(double2* f, double2* g, double2* h, lon
 template <int M> cudaError_t hconv_rows3(double2* f, double2* g, long nrows, cudaStream_t s, RowSets rs = {});
 template <int M> cudaError_t tconv_rows3(double2* f, double2* g, double2* h, long nrows, cudaStream_t s);
 
-// Warp-per-row variants at m = 512 (rows512w.cu; the warp-resident FFT of
-// fft512w.cuh), used for every m = 512 row launch.
-cudaError_t cconv_rows512w(double2* f, double2* g, long nrows, cudaStream_t s, RowSets rs = {});
-cudaError_t hconv_rows512w(double2* f, double2* g, long nrows, cudaStream_t s, RowSets rs = {});
-
 // K3d (rows_dot.cu): centered Hermitian dot-product convolution of npairs
 // row pairs (pair i at f + i*istride, g + i*istride), result in pair 0.
 cudaError_t launch_hconv_dot_rows(double2* f, const double2* g, int npairs, long istride, int m, long nrows,

@@ -123,29 +123,4 @@ const double2* pass_table(int N, int E) {
   return d;
 }
 
-const double2* warp512_table() {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  static std::map<int, double2*> tabs;
-  std::lock_guard<std::mutex> lk(g_mu);
-  auto it = tabs.find(dev);
-  if (it != tabs.end()) return it->second;
-  std::vector<double2> h(15 * 32);
-  for (int k1 = 1; k1 < 16; ++k1)
-    for (int n2 = 0; n2 < 32; ++n2) {
-      double c, s;
-      root((long)n2 * k1, 512, &c, &s);
-      h[(k1 - 1) * 32 + n2] = make_double2(c, s);
-    }
-  double2* d = nullptr;
-  if (cudaMalloc(&d, sizeof(double2) * h.size()) != cudaSuccess) return nullptr;
-  if (cudaMemcpy(d, h.data(), sizeof(double2) * h.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-      cudaDeviceSynchronize() != cudaSuccess) {   // see zeta_table
-    cudaFree(d);
-    return nullptr;
-  }
-  tabs[dev] = d;
-  return d;
-}
-
 }  // namespace idc

@@ -22,9 +22,4 @@ const double2* zeta_table(int N);
 // zeta_table(N), regrouped so that a warp's twiddle loads are contiguous.
 const double2* pass_table(int N, int E);
 
-// Device pointer to the twiddles of the warp-resident 512-point FFT
-// (fft512w.cuh): entry (k1 - 1) * 32 + n2 = exp(+2 pi i n2 k1 / 512),
-// k1 = 1..15, n2 = 0..31.
-const double2* warp512_table();
-
 }  // namespace idc
