@@ -9,6 +9,7 @@
 // P:1079-1083) live in registers / shared memory ("stash"), never in HBM,
 // except for m = 8192 where the stash spills to the caller's workspace
 // (L2-resident).
+#include "config.cuh"
 #include <atomic>
 
 #include "fft_dev.cuh"
@@ -411,29 +412,17 @@ size_t stash_bytes() {
     default: break;                      \
   }
 
-#ifndef IDC_V3_MIN_M
-#define IDC_V3_MIN_M 512
-#endif
-#ifndef IDC_V2_MAX_M
-#define IDC_V2_MAX_M 4096
-#endif
 
-size_t cconv_rows_work_bytes(int m) {
-  IDC_DISPATCH_M(m, return stash_bytes<MM, kCconvStash<MM>>());
-  return 0;
-}
-size_t hconv_rows_work_bytes(int m) {
-  IDC_DISPATCH_M(m, return stash_bytes<MM, kHconvStash<MM>>());
-  return 0;
-}
-size_t tconv_rows_work_bytes(int m) {
-  IDC_DISPATCH_M(m, return stash_bytes<MM, kTconvStash<MM>>());
-  return 0;
-}
+// The v1 kernels of this file (global-memory stash) serve m = 8192 only: up to
+// 4096 the register-resident rows2.cu / TMA-staged rows3.cu kernels run.
+constexpr int kV1M = 8192;
+size_t cconv_rows_work_bytes(int m) { return m == kV1M ? stash_bytes<kV1M, kCconvStash<kV1M>>() : 0; }
+size_t hconv_rows_work_bytes(int m) { return m == kV1M ? stash_bytes<kV1M, kHconvStash<kV1M>>() : 0; }
+size_t tconv_rows_work_bytes(int m) { return m == kV1M ? stash_bytes<kV1M, kTconvStash<kV1M>>() : 0; }
 
 cudaError_t launch_cconv_rows(double2* f, double2* g, int m, long nrows, double2* work, cudaStream_t s) {
   if (m <= IDC_V2_MAX_M) { IDC_DISPATCH_M(m, return cconv_rows2<MM>(f, g, nrows, s)); }
-  IDC_DISPATCH_M(m, return cconv_m<MM>(f, g, nrows, work, s));
+  if (m == kV1M) return cconv_m<kV1M>(f, g, nrows, work, s);
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_hconv_rows(double2* f, double2* g, int m, long nrows, double2* work, cudaStream_t s) {
@@ -446,7 +435,7 @@ cudaError_t launch_hconv_rows(double2* f, double2* g, int m, long nrows, double2
     }
   }
   if (m <= IDC_V2_MAX_M) { IDC_DISPATCH_M(m, return hconv_rows2<MM>(f, g, nrows, s)); }
-  IDC_DISPATCH_M(m, return hconv_m<MM>(f, g, nrows, work, s));
+  if (m == kV1M) return hconv_m<kV1M>(f, g, nrows, work, s);
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_tconv_rows(double2* f, double2* g, double2* h, int m, long nrows, double2* work,
@@ -460,7 +449,7 @@ cudaError_t launch_tconv_rows(double2* f, double2* g, double2* h, int m, long nr
     }
   }
   if (m <= IDC_V2_MAX_M) { IDC_DISPATCH_M(m, return tconv_rows2<MM>(f, g, h, nrows, s)); }
-  IDC_DISPATCH_M(m, return tconv_m<MM>(f, g, h, nrows, work, s));
+  if (m == kV1M) return tconv_m<kV1M>(f, g, h, nrows, work, s);
   return cudaErrorInvalidValue;
 }
 

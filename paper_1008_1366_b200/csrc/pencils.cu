@@ -19,6 +19,7 @@
 // Stream storage of K7/K8 (the paper's layout, AMB-1/AMB-10):
 //   r = +1: rows m-1..2m-2 of f;  r = 0: rows 0..m-2 of f and row m of U;
 //   r = -1: rows 0..m-1 of U.  (U has m+1 rows.)
+#include "config.cuh"
 #include "fft_dev.cuh"
 #include "launch.cuh"
 #include "kernels.cuh"
@@ -322,9 +323,6 @@ cudaError_t pad0_fwd_n(double2* f, const double2* U, long ncols, long batch, lon
     default: break;                                         \
   }
 
-#ifndef IDC_PENCIL_TMA
-#define IDC_PENCIL_TMA 1
-#endif
 #define IDC_TDISPATCH(m, ...)                                       \
   if (IDC_PENCIL_TMA) switch (m) {                                  \
       case 64: { constexpr int NN = 64; __VA_ARGS__; }              \

@@ -10,10 +10,10 @@
 // so the HBM traffic of tile n+1 overlaps the FFTs and stores of tile n.
 // The stage is read as [row][column]: thread (c, t) = c + W*t takes rows
 // t + T*i of column c -- consecutive lanes read consecutive 16-byte words.
+#include "config.cuh"
 #include <cuda.h>
 
 #include <cstring>
-#include <type_traits>
 
 #include "fft_dev.cuh"
 #include "launch.cuh"
@@ -27,22 +27,8 @@ namespace idc {
 
 namespace {
 
-#ifndef IDC_PENCIL_E
-#define IDC_PENCIL_E 8
-#endif
-#ifndef IDC_PENCIL_THREADS
-#define IDC_PENCIL_THREADS 512
-#endif
-#ifndef IDC_PENCIL_MINB
-#define IDC_PENCIL_MINB 1
-#endif
-// K7 (fft0padBackward) may use its own CTA size / CTAs per SM (experiments)
-#ifndef IDC_PENCIL0_THREADS
-#define IDC_PENCIL0_THREADS IDC_PENCIL_THREADS
-#endif
-#ifndef IDC_PENCIL0_MINB
-#define IDC_PENCIL0_MINB IDC_PENCIL_MINB
-#endif
+// tile configuration: E elements per thread, T = N/E threads per column,
+// W columns per CTA (TH threads), TMA boxes of BR rows, XB exchange slots
 template <int N, int TH = IDC_PENCIL_THREADS, int EE = IDC_PENCIL_E>
 struct TCfg {
   static constexpr int E = EE;
@@ -61,12 +47,6 @@ struct TCfg {
 // 128-thread CTAs (half-width tiles, several CTAs per SM) for m in
 // [IDC_K56_NARROW_MIN, IDC_K56_NARROW_MAX] (E = 16 sizes only): measured
 // 64 x 256^2 -1.5%, 1024 x 4096 -3.5%, 16 x 1024^2 -2%
-#ifndef IDC_K56_NARROW_MIN
-#define IDC_K56_NARROW_MIN 256
-#endif
-#ifndef IDC_K56_NARROW_MAX
-#define IDC_K56_NARROW_MAX 1024
-#endif
 template <int N>
 constexpr bool k56_wide() { return N == 256 || N >= 1024; }
 template <int N>
@@ -84,32 +64,14 @@ using K56Cfg = TCfg<N, (k56_wide<N>() ? (N >= IDC_K56_NARROW_MIN && N <= IDC_K56
 // 4096 0.190 -> 0.184 ms); not m = 512 (4-column tiles: hconv3d 59.5 ->
 // 70.8 ms) nor m = 2048 (1-column tiles: hconv2d 4095 x 2048 0.61 ->
 // 0.80 ms) -- the DRAM row segment width decides
-#ifndef IDC_K78_NARROW_MASK
-#define IDC_K78_NARROW_MASK ((1 << 10) | (1 << 8))
-#endif
 template <int N>
 constexpr bool k78_narrow() { return ((IDC_K78_NARROW_MASK) >> ilog2(N)) & 1; }
-#ifndef IDC_K78_WIDE_MIN
-#define IDC_K78_WIDE_MIN 256
-#endif
-#ifndef IDC_K78_WIDE_MAX
-#define IDC_K78_WIDE_MAX 4096
-#endif
 template <int N>
 constexpr bool k78_wide() { return N >= IDC_K78_WIDE_MIN && N <= IDC_K78_WIDE_MAX; }
 template <int N>
 using K78Cfg = TCfg<N, (k78_wide<N>() ? (k78_narrow<N>() ? 128 : 256)
                                       : IDC_PENCIL0_THREADS),
                    (k78_wide<N>() ? 16 : IDC_PENCIL_E)>;
-
-// K8 alone: E = 8 with 512-thread CTAs for m <= IDC_K8_E8_MAX (three live
-// E-vectors -- the stream being transformed and the U_k / U_{k-m}
-// accumulators -- fit 128 registers at E = 8; at E = 16 they spill)
-#ifndef IDC_K8_E8_MAX
-#define IDC_K8_E8_MAX 0
-#endif
-template <int N>
-using K8Cfg = std::conditional_t<(N <= IDC_K8_E8_MAX && N >= 64), TCfg<N, 512, 8>, K78Cfg<N>>;
 
 template <int W>
 struct Slot2 {
@@ -166,20 +128,14 @@ __device__ __forceinline__ void tile_store(const double2 (&v)[E], int t, int c, 
 
 }  // namespace
 
-// K5 / K6: tiles of at most this many columns (16-32-byte row segments,
+// K5 / K6: tiles of at most IDC_K56_TMA_STORE_MAXW columns (16-32-byte row segments,
 // m >= 2048) leave through the exchange buffer by TMA stores (tconv2d
 // 2*2048 x 2048 1.674 -> 1.548 ms, cconv2d 4096 x 1024 0.553 -> 0.502 ms);
 // wider tiles store per thread (measured slower with TMA stores: 4 columns
 // 1.356 -> 1.384 ms on 16 x 1024^2, 8 columns cconv3d 22.05 -> 23.56 ms)
-#ifndef IDC_K56_TMA_STORE_MAXW
-#define IDC_K56_TMA_STORE_MAXW 2
-#endif
 
 // K5 with TMA-stored outputs: a second exchange buffer where it fits, so the
 // odd stream's store drains while the even stream transforms
-#ifndef IDC_K5_DOUBLE_XB
-#define IDC_K5_DOUBLE_XB 1
-#endif
 template <int N>
 constexpr bool k5_double_xb() {
   using C = K56Cfg<N>;
@@ -366,17 +322,8 @@ k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
 // registers of the next store, ncu r01).  Maps: f rows 0..m-2 / m-1..2m-2,
 // the same for g, and U / V rows 0..m-1 (row m = the r = 0 stream's last
 // element, stored directly).
-#ifndef IDC_K7_TMA_STORE
-#define IDC_K7_TMA_STORE 1
-#endif
-#ifndef IDC_K7_KEEP_RAW
-#define IDC_K7_KEEP_RAW 1
-#endif
 // K8: both output halves through TMA stores (2; measured hconv3d -2.3%), U_k only
 // (1), or per-thread stores (0)
-#ifndef IDC_K8_TMA_STORE
-#define IDC_K8_TMA_STORE 2
-#endif
 struct K7StoreMaps {
   CUtensorMap flo, fhi, glo, ghi, u, v;
 };
@@ -522,12 +469,12 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
 // 0..N-1), q = 1 (r = 0: f rows 0..N-2 and U row N, the latter through a
 // one-row box into a separate tail slot), q = 2 (r = +1: f rows N-1..2N-2).
 template <int N>
-__global__ void __launch_bounds__(K8Cfg<N>::THREADS, IDC_PENCIL_MINB)
+__global__ void __launch_bounds__(K78Cfg<N>::THREADS, IDC_PENCIL_MINB)
 k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mu,
                const __grid_constant__ CUtensorMap mu1, double2* __restrict__ f, Tiles tl,
                const double2* __restrict__ twN, const double2* __restrict__ tw3N,
                const __grid_constant__ CUtensorMap mflo, const __grid_constant__ CUtensorMap mfhi) {
-  using C = K8Cfg<N>;
+  using C = K78Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   extern __shared__ __align__(128) double2 smem[];
   double2* st[2] = {smem, smem + N * W};
@@ -773,7 +720,7 @@ cudaError_t pad0_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nc
 template <int N>
 cudaError_t pad0_fwd_tma(double2* f, const double2* U, long ncols, long batch, long bstride, long ustride,
                          cudaStream_t s) {
-  using C = K8Cfg<N>;
+  using C = K78Cfg<N>;
   const double2* twN = pass_table(N, C::E);
   const double2* tw3N = zeta_table(3 * N);
   if (!twN || !tw3N) return cudaErrorMemoryAllocation;

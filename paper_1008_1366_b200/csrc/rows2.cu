@@ -9,6 +9,7 @@
 //     accumulator of tconv) stay in registers; shared memory holds only the
 //     Stockham exchange buffer (plus, for tconv, the f*g stream products), so
 //     the row's inputs stay L1-resident for the mirrored (U_{m-k}) loads.
+#include "config.cuh"
 #include "fft_dev.cuh"
 #include "launch.cuh"
 #include "kernels.cuh"
@@ -27,12 +28,6 @@ struct Cfg2 {
   static constexpr bool NAMED = (T % 32 == 0) && G > 1;
   // cap registers at 128 per thread: 16 warps per SM for 512-thread CTAs,
   // two 256-thread CTAs per SM otherwise
-#ifndef IDC_ROWS_PREFETCH
-#define IDC_ROWS_PREFETCH 1
-#endif
-#ifndef IDC_ROWS_REGS
-#define IDC_ROWS_REGS 255
-#endif
 // K2 up to this m: f and g rows staged in shared memory by bulk copies
 // (mbarrier), the next row's copies issued as soon as the current row's last
 // split has read the stage; above it the rows are read from global memory
@@ -41,12 +36,6 @@ struct Cfg2 {
 // K2 with E = 16 from this m up: park the r = 0 result in shared memory
 // instead of keeping it in registers across the r = 1 transforms (removes
 // the spills: m = 4096 1.064 -> 0.983 ms; m = 1024 neutral, m = 2048 +2.5%)
-#ifndef IDC_K2_PARK_MIN
-#define IDC_K2_PARK_MIN 4096
-#endif
-#ifndef IDC_ROWS2_TMA_MAX
-#define IDC_ROWS2_TMA_MAX 512
-#endif
   static constexpr int MINB = (65536 / (THREADS * IDC_ROWS_REGS)) < 1 ? 1 : 65536 / (THREADS * IDC_ROWS_REGS);
 };
 
@@ -422,14 +411,8 @@ cudaError_t launch2(K kernel, int threads, size_t smem, long nrows, int groups, 
 }
 
 // elements per thread and rows per CTA of the v2 kernels
-#ifndef IDC_ROWS_E
-#define IDC_ROWS_E 16
-#endif
 // E = 8 for m <= 512 (three radix-8 passes at 512; 5-9% faster there),
 // 16 from 1024 up (three passes instead of four)
-#ifndef IDC_ROWS_CTA_THREADS
-#define IDC_ROWS_CTA_THREADS 256
-#endif
 template <int M>
 struct Tune {
   static constexpr int E = M < IDC_ROWS_E ? M : (M <= 512 ? 8 : IDC_ROWS_E);

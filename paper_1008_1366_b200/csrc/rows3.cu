@@ -15,6 +15,7 @@
 //     hconv; the f*g stream products of tconv) lives in registers; tconv
 //     parks the first residue pair's partial sum in the (already staged)
 //     global f row and finishes it with the second pair.
+#include "config.cuh"
 #include "fft_dev.cuh"
 #include "launch.cuh"
 #include "kernels.cuh"
@@ -23,9 +24,6 @@
 
 // K3: elements per thread up to which all three residue streams come from one
 // read of the staged row (the r = -1 stream held in registers)
-#ifndef IDC_K3_ONE_SPLIT_MAXE
-#define IDC_K3_ONE_SPLIT_MAXE 8
-#endif
 
 namespace idc {
 
@@ -41,9 +39,6 @@ struct Cfg3 {
   static constexpr int PER = 2 * M + XB;              // staged f, g + exchange buffer (double2)
   static constexpr size_t SMEM = (size_t)G * PER * 16 + (size_t)G * 16;  // + one mbarrier per group
   static constexpr bool NAMED = G > 1;
-#ifndef IDC_ROWS3_MINB_SMALL
-#define IDC_ROWS3_MINB_SMALL 1
-#endif
   static constexpr int MINB = M <= 512 ? IDC_ROWS3_MINB_SMALL : 1;   // CTAs per SM (register cap)
 };
 
