@@ -101,6 +101,18 @@ IDC_API long long idc_launch_count(void);
 IDC_API idc_status idc_profile_begin(void);
 IDC_API long idc_profile_end(char* buf, size_t len);
 
+/* Transform counter (instrumentation for the transform-count invariant of
+ * Function cconv uses 6 transforms of size m, the
+ * centered Hermitian conv 9 real ones, tconv 8 real ones of size
+ * 2m).  Between begin and end every FFT executed on the device
+ * adds 1 to counter[log2 N]; end synchronizes the device and writes the 16
+ * counters (N = 1 .. 32768) to out.  The counting code exists only in the
+ * debug build libidconv_count.so (same ABI); the product library returns
+ * IDC_ERR_UNSUPPORTED from begin.  Errors: IDC_ERR_CUDA on allocation / copy
+ * failure, IDC_ERR_INVALID if out is NULL or begin was never called. */
+IDC_API idc_status idc_fft_count_begin(void);
+IDC_API idc_status idc_fft_count_end(unsigned long long* out);
+
 /* Bytes of device workspace `work` the call of kind k needs for the given
  * sizes (unused sizes are ignored; pass 1).  1D: m0 = m.  2D: (m0, m1) =
  * (mx, my).  3D: (m0, m1, m2) = (mx, my, mz).  Returns 0 for unsupported

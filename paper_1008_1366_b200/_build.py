@@ -11,6 +11,10 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libidconv.so")
+# debug library: the same sources with the transform counter compiled in
+# (-DIDC_COUNT_FFT=1, fft_dev.cuh); used only by tests/test_transform_counts.py
+OBJ_COUNT = os.path.join(HERE, "build_count")
+LIB_COUNT = os.path.join(HERE, "libidconv_count.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
@@ -48,8 +52,8 @@ def _deps(path, seen=None):
     return seen
 
 
-def _compile(src, extra, force):
-    obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+def _compile(src, extra, force, objdir=OBJ):
+    obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
     newest_dep = max([os.path.getmtime(src)] + [os.path.getmtime(h) for h in _deps(src)])
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= newest_dep:
         return obj
@@ -60,22 +64,33 @@ def _compile(src, extra, force):
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
-    inc, libdir = _nccl_dirs()
-    extra = ["-I" + inc] if inc else []
-    srcs = sources()
-    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, extra, force), srcs))
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        link = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+def _link(lib, objs, libdir, force):
+    if force or not os.path.exists(lib) or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs):
+        link = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart"]
         if libdir:
             link += ["-L" + libdir, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + libdir]
         r = subprocess.run(link, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+
+
+def build(force: bool = False, verbose: bool = False, count_lib: bool = True) -> str:
+    """Build libidconv.so (and the transform-counting debug library)."""
+    inc, libdir = _nccl_dirs()
+    extra = ["-I" + inc] if inc else []
+    srcs = sources()
+    jobs = [(s_, extra, OBJ) for s_ in srcs]
+    if count_lib:
+        jobs += [(s_, extra + ["-DIDC_COUNT_FFT=1"], OBJ_COUNT) for s_ in srcs]
+    for d in {j[2] for j in jobs}:
+        os.makedirs(d, exist_ok=True)
+    with cf.ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(lambda j: _compile(j[0], j[1], force, j[2]), jobs))
+    _link(LIB, objs[:len(srcs)], libdir, force)
+    if count_lib:
+        _link(LIB_COUNT, objs[len(srcs):], libdir, force)
     if verbose:
-        print("built", LIB)
+        print("built", LIB, "and", LIB_COUNT if count_lib else "")
     return LIB
 
 

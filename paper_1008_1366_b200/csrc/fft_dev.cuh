@@ -31,6 +31,38 @@
 
 namespace idc {
 
+// ------------------------------------------------- transform counter (debug) --
+// Instrumentation for the transform-count invariant (6 / 9 /
+// 8 transforms per 1D convolution), compiled
+// only into the debug library libidconv_count.so (-DIDC_COUNT_FFT=1, built by
+// _build.py next to the product library): while idc_fft_count_begin() ..
+// idc_fft_count_end() is active, every transform executed adds 1 (per thread
+// group) to counter[log2 N] in device memory.  The pointer lives in a
+// __constant__ of each translation unit (device code is not relocatable), set
+// through setters the units register at load time.  The product library has
+// no counter code in its kernels (the check cost registers in the row kernels).
+#ifndef IDC_COUNT_FFT
+#define IDC_COUNT_FFT 0
+#endif
+using FftCounterSetter = cudaError_t (*)(unsigned long long*);
+void register_fft_counter_setter(FftCounterSetter);   // launch.cu
+#if IDC_COUNT_FFT
+namespace {
+__constant__ unsigned long long* g_fft_counter;
+cudaError_t set_fft_counter(unsigned long long* p) { return cudaMemcpyToSymbol(g_fft_counter, &p, sizeof(p)); }
+struct FftCounterRegistration {
+  FftCounterRegistration() { register_fft_counter_setter(&set_fft_counter); }
+};
+FftCounterRegistration g_fft_counter_registration;
+}  // namespace
+#endif
+__device__ __forceinline__ void count_fft(int log2n, int t, unsigned n) {
+#if IDC_COUNT_FFT
+  unsigned long long* p = g_fft_counter;
+  if (p != nullptr && t == 0) atomicAdd(p + log2n, (unsigned long long)n);
+#endif
+}
+
 // ------------------------------------------------------------ complex ops --
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -394,6 +426,7 @@ __device__ __forceinline__ void fft(double2 (&v)[E], int t, double2* __restrict_
   // out of the caller's row loop and held live in registers across it.
   int tl;
   asm volatile("mov.b32 %0, %1;" : "=r"(tl) : "r"(t));
+  count_fft(ilog2(N), tl, 1);
   fft_passes<N, E, 1, SIGN>(v, tl, xb, tw, sync, xs, PassTw<N, E, pass_radix(N, E, 1), 1>{});
 }
 
@@ -440,6 +473,7 @@ __device__ __forceinline__ void fft2(double2 (&v)[E], double2 (&w)[E], int t, do
                                      XS xs = XS{}) {
   int tl;
   asm volatile("mov.b32 %0, %1;" : "=r"(tl) : "r"(t));
+  count_fft(ilog2(N), tl, 2);
   fft2_passes<N, E, 1, SIGN>(v, w, tl, xb, xb2, tw, sync, xs, PassTw<N, E, pass_radix(N, E, 1), 1>{});
 }
 

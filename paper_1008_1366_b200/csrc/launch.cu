@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../../include/idconv.h"
+#include "fft_dev.cuh"
 #include "kernels.cuh"
 #include "launch.cuh"
 
@@ -24,6 +25,13 @@ bool g_on = false;
 std::vector<Rec> g_recs;
 std::vector<cudaEvent_t> g_free;   // recycled events
 
+// transform counter: the per-translation-unit pointer setters (fft_dev.cuh)
+std::vector<FftCounterSetter>& counter_setters() {
+  static std::vector<FftCounterSetter> v;
+  return v;
+}
+unsigned long long* g_counter = nullptr;
+
 cudaEvent_t get_event() {
   if (!g_free.empty()) {
     cudaEvent_t e = g_free.back();
@@ -35,6 +43,8 @@ cudaEvent_t get_event() {
   return e;
 }
 }  // namespace
+
+void register_fft_counter_setter(FftCounterSetter f) { counter_setters().push_back(f); }
 
 cudaError_t launch_kernel(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s,
                           const LaunchTag& tag) {
@@ -62,6 +72,34 @@ cudaError_t launch_kernel(const void* fn, dim3 grid, dim3 block, void** args, si
 }  // namespace idc
 
 extern "C" {
+
+// Transform counter (instrumentation, debug library only): see fft_dev.cuh.
+// begin zeroes the 16 counters (index log2 N) and arms every translation
+// unit; end waits for the device, copies them to out[0..15] and disarms.
+idc_status idc_fft_count_begin(void) {
+  std::lock_guard<std::mutex> lk(idc::g_mu);
+  if (idc::counter_setters().empty()) return IDC_ERR_UNSUPPORTED;   // product build: no counter code
+  if (!idc::g_counter && cudaMalloc(&idc::g_counter, 16 * sizeof(unsigned long long)) != cudaSuccess) {
+    idc::g_counter = nullptr;
+    return IDC_ERR_CUDA;
+  }
+  if (cudaMemset(idc::g_counter, 0, 16 * sizeof(unsigned long long)) != cudaSuccess) return IDC_ERR_CUDA;
+  for (auto f : idc::counter_setters())
+    if (f(idc::g_counter) != cudaSuccess) return IDC_ERR_CUDA;
+  return cudaDeviceSynchronize() == cudaSuccess ? IDC_OK : IDC_ERR_CUDA;
+}
+
+idc_status idc_fft_count_end(unsigned long long* out) {
+  if (!out) return IDC_ERR_INVALID;
+  std::lock_guard<std::mutex> lk(idc::g_mu);
+  if (!idc::g_counter) return IDC_ERR_INVALID;
+  if (cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpy(out, idc::g_counter, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return IDC_ERR_CUDA;
+  for (auto f : idc::counter_setters())
+    if (f(nullptr) != cudaSuccess) return IDC_ERR_CUDA;
+  return cudaDeviceSynchronize() == cudaSuccess ? IDC_OK : IDC_ERR_CUDA;
+}
 
 idc_status idc_profile_begin(void) {
   std::lock_guard<std::mutex> lk(idc::g_mu);

@@ -33,6 +33,8 @@ SIGNATURES = {
     "idc_launch_count": ([], ctypes.c_longlong),
     "idc_profile_begin": ([], _I),
     "idc_profile_end": ([ctypes.c_char_p, _S], ctypes.c_long),
+    "idc_fft_count_begin": ([], _I),
+    "idc_fft_count_end": ([ctypes.POINTER(ctypes.c_ulonglong)], _I),
     "idc_workspace_bytes": ([_I, _S, _S, _S, _S], _S),
     "idc_cconv1d": ([_P, _P, _S, _S, _P, _S, _P], _I),
     "idc_hconv1d": ([_P, _P, _S, _S, _P, _S, _P], _I),
@@ -339,6 +341,18 @@ def profile_end() -> list:
         tag, n, launches, units, ms = line.split()
         out.append(dict(tag=tag, n=int(n), launches=int(launches), units=int(units), ms=float(ms)))
     return out
+
+
+def fft_count_begin():
+    """Arm the library's transform counter (idc_fft_count_begin)."""
+    _check(lib().idc_fft_count_begin(), "idc_fft_count_begin")
+
+
+def fft_count_end() -> dict:
+    """Disarm it; returns {N: transforms of size N executed since begin}."""
+    out = (ctypes.c_ulonglong * 16)()
+    _check(lib().idc_fft_count_end(out), "idc_fft_count_end")
+    return {1 << i: int(out[i]) for i in range(16) if out[i]}
 
 
 def launch_count() -> int:
