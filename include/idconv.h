@@ -198,6 +198,11 @@ IDC_API idc_status idc_comm_unique_id(void* id_out);
 
 IDC_API size_t idc_dist_workspace_bytes(idc_kind k, size_t mx, size_t my, size_t mz, int nranks);
 
+/* Test hook (instrumentation): with on != 0 the distributed calls run their
+ * exchange phases and NCCL all-to-alls even on a one-rank communicator, which
+ * otherwise runs the single-GPU composition (there is nothing to exchange). */
+IDC_API idc_status idc_dist_force_exchange(int on);
+
 /* Distributed cconv3d (the decomposition is ours, AMB-19: the
  * paper is single-process).  f, g hold this rank's x-slab
  * [rank*mx/P, (rank+1)*mx/P) of the global mx x my x mz arrays (each rank's

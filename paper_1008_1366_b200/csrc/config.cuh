@@ -15,6 +15,7 @@
 // | IDC_ROWS_PREFETCH       | 1       | rows2.cu: L2 bulk prefetch of the next rows (unstaged m)               |
 // | IDC_ROWS2_TMA_MAX       | 512     | K2 stages f, g rows in shared memory (bulk copies) up to this m         |
 // | IDC_K2_PARK_MIN         | 4096    | K2 parks the r = 0 result in shared memory from this m                  |
+// | IDC_K2_ONE_READ         | 1       | K2 (E = 8, staged rows) builds both residues' streams from one read     |
 // | IDC_K3_ONE_SPLIT_MAXE   | 8       | K3 splits all three residues from one staged read up to this E          |
 // | IDC_ROWS3_MINB_SMALL    | 1       | rows3.cu CTAs per SM for m <= 512                                       |
 // | IDC_PENCIL_TMA          | 1       | 2D/3D pencils use the TMA kernels of pencils2.cu for 64 <= m <= 4096    |
@@ -56,6 +57,9 @@
 #endif
 #ifndef IDC_K2_PARK_MIN
 #define IDC_K2_PARK_MIN 4096
+#endif
+#ifndef IDC_K2_ONE_READ
+#define IDC_K2_ONE_READ 1
 #endif
 #ifndef IDC_K3_ONE_SPLIT_MAXE
 #define IDC_K3_ONE_SPLIT_MAXE 8

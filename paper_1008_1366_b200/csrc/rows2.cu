@@ -147,7 +147,28 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
     // codelet registers spill, so the transforms run one at a time.
     double2 x[E], y[E], z[E];
     double2 zt;   // zeta_{2m}^t; zeta_{2m}^k = zeta_{2m}^t zeta_{2E}^i (immediate), k = t + T i
-    if constexpr (FFT2) {
+    if constexpr (FFT2 && ST && IDC_K2_ONE_READ) {
+      // both residues' streams from one read of the staged rows (the r = 1
+      // pair held in registers, E = 8): the stage is refilled before the
+      // first transform and its reads halve
+      double2 y1[E];
+      zt = ldtw(&tw2M[t]);
+      for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) {
+        const double2 a = fr[t + T * i], b = gr[t + T * i];
+        x[i] = a;
+        y[i] = b;
+        y1[i] = cmul(a, w);                                                 // r = 1
+        z[i] = cmul(b, w);
+      });
+      refill();
+      fft2<M, E, +1>(x, y, t, xb, xb2, twM, sync);                        // r = 0
+#pragma unroll
+      for (int i = 0; i < E; ++i) x[i] = cmul(x[i], y[i]);
+      fft2<M, E, +1>(y1, z, t, xb, xb2, twM, sync);
+#pragma unroll
+      for (int i = 0; i < E; ++i) y[i] = cmul(y1[i], z[i]);
+      fft2<M, E, -1>(x, y, t, xb, xb2, twM, sync);                        // forward
+    } else if constexpr (FFT2) {
 #pragma unroll
       for (int i = 0; i < E; ++i) x[i] = ldrow<ST>(&fr[t + T * i]);
 #pragma unroll

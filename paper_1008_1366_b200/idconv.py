@@ -49,6 +49,7 @@ SIGNATURES = {
     "idc_comm_unique_id": ([_P], _I),
     "idc_dist_workspace_bytes": ([_I, _S, _S, _S, _I], _S),
     "idc_cconv3d_dist": ([_P, _P, _P, _S, _S, _S, _P, _S, _P], _I),
+    "idc_dist_force_exchange": ([_I], _I),
     "idc_fill_uniform": ([_P, _S, _U64, _U64, _U64, _P], _I),
     "idc_dist_plan": ([_S, _S, _S, _I, _I, ctypes.POINTER(ctypes.c_longlong)], _I),
     "idc_dist_emulated_workspace_bytes": ([_S, _S, _S, _I], _S),

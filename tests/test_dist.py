@@ -94,15 +94,19 @@ def test_emulated_ranks_gpu(P, shape):
 
 
 @pytest.mark.gpu
-def test_nccl_single_rank_gpu():
+@pytest.mark.parametrize("exchange", [False, True])
+def test_nccl_single_rank_gpu(exchange):
+    """One rank: the single-GPU composition (exchange=False, the default) and,
+    through the test hook, the y-first phases with the NCCL all-to-alls."""
     import torch
     import torch.distributed as dist
     from paper_1008_1366_b200 import idconv
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29731")
+    os.environ["MASTER_PORT"] = "29731" if exchange else "29735"
     dist.init_process_group("gloo", rank=0, world_size=1)
     try:
         comm = idconv.Comm()
+        idconv.lib().idc_dist_force_exchange(int(exchange))
         shape = (16, 8, 16)
         f, g = synthgen.cconv3d_inputs(*shape)
         F, G = torch.from_numpy(f.copy()).cuda(), torch.from_numpy(g.copy()).cuda()
@@ -111,6 +115,7 @@ def test_nccl_single_rank_gpu():
         assert rel_l2(F.cpu().numpy(), direct.cconv3d(f, g)) < 1e-14
         comm.close()
     finally:
+        idconv.lib().idc_dist_force_exchange(0)
         dist.destroy_process_group()
 
 
@@ -143,15 +148,17 @@ def test_hermitian_emulated_ranks_gpu(P, shape):
 
 
 @pytest.mark.gpu
-def test_hermitian_nccl_single_rank_gpu():
+@pytest.mark.parametrize("exchange", [False, True])
+def test_hermitian_nccl_single_rank_gpu(exchange):
     import torch
     import torch.distributed as dist
     from paper_1008_1366_b200 import idconv
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ["MASTER_PORT"] = "29733"
+    os.environ["MASTER_PORT"] = "29733" if exchange else "29737"
     dist.init_process_group("gloo", rank=0, world_size=1)
     try:
         comm = idconv.Comm()
+        idconv.lib().idc_dist_force_exchange(int(exchange))
         shape = (8, 4, 16)
         f, g = synthgen.hconv3d_inputs(*shape)
         F, G = [torch.from_numpy(a).cuda() for a in _herm_slabs(f, 1)], [torch.from_numpy(a).cuda() for a in _herm_slabs(g, 1)]
@@ -160,4 +167,5 @@ def test_hermitian_nccl_single_rank_gpu():
         assert rel_l2(F[0].cpu().numpy()[:-1], direct.hconv3d(f, g)) < 1e-14
         comm.close()
     finally:
+        idconv.lib().idc_dist_force_exchange(0)
         dist.destroy_process_group()
