@@ -21,7 +21,8 @@ void load_entry() {
 }  // namespace
 
 bool encode_pencil_map(CUtensorMap* map, const void* base, long ncols, long rows, long batch, long bstride, int W,
-                       int BR) {
+                       int BR, bool swizzle128) {
+  if (swizzle128 && W * 16 != 128) return false;
   std::call_once(g_once, load_entry);
   if (!g_encode) return false;
   // fp64 elements; the innermost dimension interleaves (re, im)
@@ -30,7 +31,8 @@ bool encode_pencil_map(CUtensorMap* map, const void* base, long ncols, long rows
   cuuint32_t box[3] = {(cuuint32_t)(2 * W), (cuuint32_t)BR, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
