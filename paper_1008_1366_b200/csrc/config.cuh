@@ -31,7 +31,6 @@
 // | IDC_K78_NARROW_MASK     | m=1024,256 | K7/K8 with 128-thread CTAs for the m whose log2 bit is set           |
 // | IDC_K7_TMA_STORE        | 1       | K7 residue tiles leave through the exchange buffer by TMA stores        |
 // | IDC_K7_KEEP_RAW         | 1       | K7 reads U_k, U_{k-m} once into registers; next tile loaded at once     |
-// | IDC_K7_WARP             | 1       | K7 at m = 512: one warp per column, warp-local exchanges, swizzled tiles |
 // | IDC_K8_TMA_STORE        | 2       | K8: both output halves by TMA stores (1: U_k only, 0: per thread)      |
 #pragma once
 
@@ -112,9 +111,6 @@
 #endif
 #ifndef IDC_K7_KEEP_RAW
 #define IDC_K7_KEEP_RAW 1
-#endif
-#ifndef IDC_K7_WARP
-#define IDC_K7_WARP 1
 #endif
 #ifndef IDC_K8_TMA_STORE
 #define IDC_K8_TMA_STORE 2

@@ -466,118 +466,6 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
 #endif
 }
 
-// ------------------------------------------------------------- K7 (warp) --
-// K7 at m = 512 with one warp per column (E = 16, T = 32, W = 8): the three
-// residue transforms of a column exchange only inside their warp
-// (__syncwarp, a private exchange region per column) instead of eight warps
-// meeting at CTA barriers four times per transform.  The stage and the output
-// tile use the TMA 128-byte swizzle (16-byte chunk c of row r at c ^ (r & 7))
-// so that a warp walking one column of consecutive rows hits eight distinct
-// bank groups.  Per residue: split from the registers, warp-local FFT, one CTA
-// barrier, park the tile (swizzled) and TMA-store it.
-struct WarpSync {
-  __device__ __forceinline__ void operator()() const { __syncwarp(); }
-};
-struct ColSlot {
-  int base;
-  __device__ __forceinline__ int operator()(int i) const { return base + i; }
-};
-__device__ __forceinline__ int sw128(int row, int c) { return row * 8 + (c ^ (row & 7)); }
-
-template <int N>
-__global__ void __launch_bounds__(256, 1)
-k_pad0_bwd_warp(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mg,
-                double2* __restrict__ f, double2* __restrict__ g, double2* __restrict__ U, double2* __restrict__ V,
-                Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw3N,
-                const __grid_constant__ K7StoreMaps sm) {
-  constexpr int E = 16, T = 32, W = 8, BR = 256;
-  static_assert(N == T * E, "one warp per 512-point column");
-  constexpr int R2 = ((2 * N - 1 + BR - 1) / BR) * BR;              // staged rows
-  constexpr int XC = xbuf_elems<N, E>();                             // exchange slots per column
-  extern __shared__ __align__(1024) double2 smem_raw[];
-  // 1024-byte aligned stage (TMA 128-byte swizzle); offset arithmetic on the
-  // shared array keeps the accesses in the shared window (LDS/STS, not generic)
-  double2* stage = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / 16u;
-  double2* xb = stage + R2 * W;                                      // W exchange regions / the output tile
-  uint64_t* bar = reinterpret_cast<uint64_t*>(xb + W * XC);
-  const int t = threadIdx.x & 31, c = threadIdx.x >> 5;
-  const ColSlot xs{c * XC};
-  constexpr uint32_t BYTES = (uint32_t)R2 * W * 16;
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  long tau = blockIdx.x;
-  if (threadIdx.x == 0 && tau < tl.ntiles) {
-    int in; long item, col0;
-    tile_coords(tl, tau, W, in, item, col0);
-    mbar_arrive_expect_tx(bar, BYTES);
-    load_rows<W, BR>(in == 0 ? &mf : &mg, stage, col0, 0, 2 * N - 1, item, bar);
-  }
-  const double s3 = 0.86602540378443864676372317075294;
-  uint32_t phase = 0;
-  for (; tau < tl.ntiles; tau += gridDim.x) {
-    int in; long item, col0;
-    tile_coords(tl, tau, W, in, item, col0);
-    const bool ok = col0 + c < tl.ncols;
-    double2* u = (in == 0 ? U : V) + item * tl.ustride + (ok ? col0 + c : 0);
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    double2 A[E], B[E];                                                // U_k, U_{k-m}
-#pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const int k = t + T * i;
-      A[i] = stage[sw128(N - 1 + k, c)];
-      B[i] = (i == 0 && t == 0) ? make_double2(0, 0) : stage[sw128(k - 1, c)];
-    }
-    __syncthreads();
-    const long nx = tau + gridDim.x;
-    if (threadIdx.x == 0 && nx < tl.ntiles) {                          // the stage is free: next tile now
-      int in2; long item2, c2;
-      tile_coords(tl, nx, W, in2, item2, c2);
-      mbar_arrive_expect_tx(bar, BYTES);
-      load_rows<W, BR>(in2 == 0 ? &mf : &mg, stage, c2, 0, 2 * N - 1, item2, bar);
-    }
-    double2 v[E];
-#pragma unroll 1
-    for (int rr = 0; rr < 3; ++rr) {
-      const int r = rr - 1;
-      const double2 z3 = make_double2(r == 0 ? 1.0 : -0.5, r == 0 ? 0.0 : (r < 0 ? s3 : -s3));  // zeta_3^{-r}
-      auto split = [&](int i, double2 zr) {                           // w_{k,r} (Eqs. fft0backwardA/B)
-        v[i] = (i == 0 && t == 0) ? A[i] : cmul(zr, cadd(A[i], cmul(z3, B[i])));
-      };
-      const double2 zt = ldtw(&tw3N[t]);
-      if (r == 0) {
-#pragma unroll
-        for (int i = 0; i < E; ++i) split(i, make_double2(1, 0));
-      } else if (r > 0) {
-        for_roots<3 * E, 1, +1, E>(zt, split);
-      } else {
-        for_roots<3 * E, 1, -1, E>(cconj(zt), split);
-      }
-      if (threadIdx.x == 0) bulk_wait_read();                          // the previous residue's stores have read xb
-      __syncthreads();
-      fft<N, E, +1>(v, t, xb, twN, WarpSync{}, xs);
-      __syncthreads();                                                 // every column's exchanges are done
-#pragma unroll
-      for (int i = 0; i < E; ++i) xb[sw128(t + T * i, c)] = v[i];      // park the tile (swizzled)
-      if (r == 0 && t == T - 1 && ok) u[(long)N * tl.ncols] = v[E - 1];   // l = m-1 -> U row m
-      fence_proxy_async_smem();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const CUtensorMap* mp = r == -1 ? (in == 0 ? &sm.u : &sm.v)
-                              : r == 0  ? (in == 0 ? &sm.flo : &sm.glo)
-                                        : (in == 0 ? &sm.fhi : &sm.ghi);
-        const int rows = r == 0 ? N - 1 : N;
-        for (int b = 0; b < rows; b += BR) tma_store_3d(mp, (int)(2 * col0), b, (int)item, xb + (long)b * W);
-        bulk_commit();
-      }
-    }
-  }
-  if (threadIdx.x == 0) bulk_wait_all();
-}
-
 // ------------------------------------------------------------------- K8 --
 // Streams staged one at a time (double buffered): q = 0 (r = -1: U rows
 // 0..N-1), q = 1 (r = 0: f rows 0..N-2 and U row N, the latter through a
@@ -803,31 +691,6 @@ template <int N>
 cudaError_t pad0_bwd_tma(double2* f, double2* g, double2* U, double2* V, long ncols, long batch, long bstride,
                          long ustride, cudaStream_t s) {
   using C = K78Cfg<N>;
-  if constexpr (N == 512 && IDC_K7_WARP) {   // warp-per-column K7 (swizzled stage and output tile)
-    constexpr int W = 8, BR = 256, R2 = 1024;
-    const double2* twN = pass_table(N, 16);
-    const double2* tw3N = zeta_table(3 * N);
-    if (!twN || !tw3N) return cudaErrorMemoryAllocation;
-    CUtensorMap mf, mg;
-    if (!encode_pencil_map(&mf, f, ncols, 2 * N - 1, batch, bstride, W, BR, true) ||
-        !encode_pencil_map(&mg, g ? g : f, ncols, 2 * N - 1, batch, bstride, W, BR, true))
-      return cudaErrorNotSupported;
-    Tiles tl = make_tiles<W>(ncols, batch, g ? 2 : 1, bstride, ustride);
-    K7StoreMaps sm;
-    double2* gg = g ? g : f;
-    double2* VV = g ? V : U;
-    const long lo = ((long)N - 1) * ncols;
-    if (!encode_pencil_map(&sm.flo, f, ncols, N - 1, batch, bstride, W, BR, true) ||
-        !encode_pencil_map(&sm.fhi, f + lo, ncols, N, batch, bstride, W, BR, true) ||
-        !encode_pencil_map(&sm.glo, gg, ncols, N - 1, batch, bstride, W, BR, true) ||
-        !encode_pencil_map(&sm.ghi, gg + lo, ncols, N, batch, bstride, W, BR, true) ||
-        !encode_pencil_map(&sm.u, U, ncols, N, batch, ustride, W, BR, true) ||
-        !encode_pencil_map(&sm.v, VV, ncols, N, batch, ustride, W, BR, true))
-      return cudaErrorNotSupported;
-    void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw3N, &sm};
-    const size_t smem = 1024 + ((size_t)R2 * W + (size_t)W * xbuf_elems<N, 16>()) * 16 + 16;
-    return launch_t(k_pad0_bwd_warp<N>, 256, smem, tl.ntiles, s, args, {"K7", N, ncols * batch * (g ? 2 : 1)});
-  }
   constexpr int R2 = ((2 * N - 1 + C::BR - 1) / C::BR) * C::BR;
   const double2* twN = pass_table(N, C::E);
   const double2* tw3N = zeta_table(3 * N);
