@@ -70,7 +70,7 @@ def test_plan_properties():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("P,shape", [(1, (8, 8, 8)), (2, (8, 4, 16)), (4, (16, 16, 8)), (8, (16, 8, 4)),
-                                     (8, (64, 32, 32))])
+                                     (8, (64, 32, 32)), (8, (64, 64, 64))])
 def test_emulated_ranks_gpu(P, shape):
     import torch
     from paper_1008_1366_b200 import idconv
@@ -127,7 +127,7 @@ def _herm_slabs(f, P):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("P,shape", [(1, (4, 4, 4)), (2, (4, 2, 8)), (4, (4, 4, 4)), (8, (4, 8, 4)),
-                                     (8, (32, 16, 16))])
+                                     (8, (32, 16, 16)), (8, (64, 64, 64)), (4, (64, 64, 32))])
 def test_hermitian_emulated_ranks_gpu(P, shape):
     import torch
     from paper_1008_1366_b200 import idconv
