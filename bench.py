@@ -372,7 +372,7 @@ def kernel_table(p, prof, steps, pk, traffic, step_ms):
             t_b = b_u / (pk["hbm_gbs"] * 1e9)
             t_f = f_u / (pk["fp64_tflops"] * 1e12)
             d["bound"] = "hbm" if t_b >= t_f else "alu"
-            tpu = traffic.get(f"{r['tag']}:{r['n']}")
+            tpu = traffic.get(f"{p.get('name', '')}:{r['tag']}:{r['n']}") or traffic.get(f"{r['tag']}:{r['n']}")
             d["traffic_per_launch"] = tpu * d["units_per_launch"] if tpu else None
         rows.append(d)
     rows.sort(key=lambda d: -d["ms_per_call"])
@@ -406,7 +406,7 @@ def dominant_roofline(kt, pk):
 def measure(idc, torch, tdist, name, args, rank, ws, dev, comm=None, want_e2e=False):
     """Time one config: W warm-up calls, K timed calls (restore + L2 flush
     before each, outside the events), kernel profile over the timed calls."""
-    p = CONFIGS[name]
+    p = dict(CONFIGS[name], name=name)
     dist3d = comm is not None and p["kind"] in ("cconv3d", "hconv3d")
     if dist3d:
         pristine = make_dist_inputs(idc, torch, p, rank, ws, dev)

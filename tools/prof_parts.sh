@@ -18,4 +18,10 @@ prof c5a_k2 cconv_rows2 python tools/prof_nd.py cconv3d 512,512,512 --reps 1
 prof c5a_k5 pad_bwd_tma python tools/prof_nd.py cconv3d 512,512,512 --reps 1
 prof c5b_k3 hconv_rows3 python tools/prof_nd.py hconv3d 1023,1023,512 --reps 1
 prof c5b_k7 pad0_bwd_tma python tools/prof_nd.py hconv3d 1023,1023,512 --reps 1
+# keep only text: ncu summaries and raw metric CSVs (the reports exceed the copy-back limit)
+for r in gpurun_out/r02p_*.ncu-rep; do
+  python tools/ncu_summary.py "$r" > "${r%.ncu-rep}.txt" 2>&1
+  ncu -i "$r" --page raw --csv > "${r%.ncu-rep}.raw.csv" 2>/dev/null
+  rm -f "$r"
+done
 echo done

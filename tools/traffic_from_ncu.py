@@ -2,7 +2,7 @@
 `ncu --set full` capture, merged into profiles/traffic.json (read by
 bench.py for the roofline "traffic" field: bytes per unit x units per launch).
 
-usage: python tools/traffic_from_ncu.py <report.ncu-rep> <tag:n> <units in that launch> [note]"""
+usage: python tools/traffic_from_ncu.py <report.ncu-rep | raw.csv> <tag:n> <units in that launch> [note]"""
 import csv
 import io
 import json
@@ -13,7 +13,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 rep, key, units = sys.argv[1], sys.argv[2], float(sys.argv[3])
 note = sys.argv[4] if len(sys.argv) > 4 else ""
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if rep.endswith(".csv"):                       # `ncu -i ... --page raw --csv` output saved on the GPU box
+    raw = open(rep).read()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h, u, v = rows[0], rows[1], rows[2]
 scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
