@@ -7,7 +7,8 @@ rows = list(csv.reader(open(sys.argv[1])))
 hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
 h = rows[hi]
 ik, im, iu, iv = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Unit"), h.index("Metric Value")
-scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
+         "ns": 1e-9, "us": 1e-6, "ms": 1e-3}
 tot = defaultdict(float)
 per = defaultdict(lambda: defaultdict(float))
 for r in rows[hi + 1:]:
