@@ -31,7 +31,7 @@ namespace {
 
 template <int M>
 struct Cfg3 {
-  static constexpr int E = M <= 512 ? 8 : 16;          // 8 at m = 512 (measured 8% faster there)
+  static constexpr int E = M <= IDC_ROWS3_E8_MAX ? 8 : 16;   // 8 at m = 512 (measured 8% faster there)
   static constexpr int T = M / E;
   static constexpr int G = T >= 256 ? 1 : 256 / T;     // row groups per CTA
   static constexpr int THREADS = G * T;

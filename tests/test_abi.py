@@ -121,3 +121,22 @@ def test_launch_count_counts_hot_path_kernels():
     n1 = idconv.launch_count()
     idconv.cconv2d(a, b)                                     # K5, K2 (both x-streams), K6
     assert idconv.launch_count() - n1 == 3
+
+
+@pytest.mark.gpu
+def test_profiler_reports_kernel_classes_and_units():
+    """idc_profile_begin/end: one record per kernel class with launches, units
+    (rows / pencil columns) and a positive device time."""
+    import torch
+    a = torch.zeros((2, 64, 32), dtype=torch.complex128, device="cuda")
+    b = torch.zeros_like(a)
+    idconv.profile_begin()
+    idconv.cconv2d(a, b)                                     # K5 (64 cols x 2 items x 2 inputs), K2, K6
+    recs = {r["tag"]: r for r in idconv.profile_end()}
+    assert set(recs) == {"K5", "K2", "K6"} or set(recs) == {"K5s", "K2", "K6s"}, recs
+    k5 = recs.get("K5") or recs["K5s"]
+    assert k5["n"] == 64 and k5["units"] == 32 * 2 * 2 and k5["launches"] == 1
+    assert recs["K2"]["n"] == 32 and recs["K2"]["units"] == 2 * 2 * 64
+    assert all(r["ms"] > 0 for r in recs.values())
+    again = {r["tag"]: r for r in idconv.profile_end()}              # a second end returns the same window
+    assert again == recs

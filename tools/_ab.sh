@@ -1,1 +1,2 @@
-timeout 900 python -m pytest tests/test_parity_nd.py tests/test_guard_regions.py -m gpu -x -q -k "hconv" > gpurun_out/pt_k7w.log 2>&1 && bash tools/ab_all.sh > gpurun_out/ab_k7w.log 2>&1
+IDCONV_LIB=tools/var_k3e16.so timeout 600 python -m pytest tests/test_parity_1d.py -m gpu -x -q -k "hconv or tconv" > gpurun_out/pt_k3e16.log 2>&1
+bash tools/ab_all.sh > gpurun_out/ab_k3e16.log 2>&1
