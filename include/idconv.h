@@ -207,10 +207,13 @@ IDC_API idc_status idc_dist_force_exchange(int on);
  * paper is single-process).  f, g hold this rank's x-slab
  * [rank*mx/P, (rank+1)*mx/P) of the global mx x my x mz arrays (each rank's
  * slab contiguous, row-major) -- result in place, same layout.  Requires P a
- * power of two dividing mx and 2*my.  Internally: fftpadBackward along the
- * locally complete y axis, ncclAlltoAll of the y-residue streams, the 2D
- * (x, z) implicit convolution (Function cconv2) of every owned
- * y-residue, ncclAlltoAll back, fftpadForward along y.  All on `stream`. */
+ * power of two dividing mx and my.  Internally: fftpadBackward along the
+ * locally complete y axis writing its two residue streams straight into the
+ * rank-major send blocks (rank d receives rows [d my/P, (d+1) my/P) of each
+ * stream), ncclAlltoAll, the 2D (x, z) implicit convolution (Function
+ * cconv2) of every owned y-residue, ncclAlltoAll back,
+ * fftpadForward along y reading the returned blocks.  All on `stream`.  One
+ * rank runs idc_cconv3d on the slab (nothing to exchange). */
 IDC_API idc_status idc_cconv3d_dist(void* comm, idc_c128* f, idc_c128* g, size_t mx, size_t my, size_t mz,
                             void* work, size_t work_bytes, idc_stream stream);
 
@@ -219,8 +222,9 @@ IDC_API idc_status idc_cconv3d_dist(void* comm, idc_c128* f, idc_c128* g, size_t
  * are padded to 2mx x-planes (the extra last plane is never read and its
  * output is unspecified); rank r holds planes [r*2mx/P, (r+1)*2mx/P) --
  * result in place, same layout.  Requires P a power of two dividing 2mx and
- * 3my, and mx, my, mz >= 2.  Internally: fft0padBackward along the locally
- * complete centered y axis (3my y-residues), ncclAlltoAll, Function conv2
+ * my, and mx, my, mz >= 2.  Internally: fft0padBackward along the locally
+ * complete centered y axis (three streams of my residues, dealt out by rows
+ * as for cconv3d), ncclAlltoAll, Function conv2
  * on the (x, z) plane of every owned y-residue, ncclAlltoAll
  * back, fft0padForward along y.  Workspace: idc_dist_workspace_bytes(
  * IDC_HCONV3D, ...).  Errors as idc_cconv3d_dist. */
@@ -228,8 +232,9 @@ IDC_API idc_status idc_hconv3d_dist(void* comm, idc_c128* f, idc_c128* g, size_t
                             void* work, size_t work_bytes, idc_stream stream);
 
 /* Host-side plan of the decomposition (no GPU needed): out[0..5] =
- * {local x planes nx, y-residues per rank nres, elements per peer block,
- * first local plane x0, first owned residue q0, elements per y-stream S}. */
+ * {local x planes nx, y-residues per rank nres (= streams * my/P),
+ * elements per peer block, first local plane x0, first owned row l0 of each
+ * y stream (rank * my/P), elements of the local slab S}. */
 IDC_API idc_status idc_dist_plan(size_t mx, size_t my, size_t mz, int nranks, int rank, long long* out);
 /* Same for k = IDC_CCONV3D or IDC_HCONV3D (idc_dist_plan == IDC_CCONV3D). */
 IDC_API idc_status idc_dist_plan_kind(idc_kind k, size_t mx, size_t my, size_t mz, int nranks, int rank,

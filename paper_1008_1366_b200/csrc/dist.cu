@@ -5,30 +5,36 @@
 // rank r holds planes [r*nx, (r+1)*nx), nx = mx/P, full y and z.
 //
 //   A. y is locally complete: fftpadBackward along y (K5) on every local
-//      x-plane -> even y-stream in place, odd y-stream in Uy (same for g).
-//      The 2*my y-residues (q < my: even stream row q; q >= my: odd stream
-//      row q-my) are dealt out in contiguous ranges of nres = 2my/P; the
-//      send buffer is packed rank-major: send[p][x_local][q'][z].
+//      x-plane gives S = 2 residue streams (even, odd) of my rows each.  The
+//      rows of every stream are dealt out in blocks of L = my/P: rank d owns
+//      rows [d L, (d+1) L) of each stream, nres = S L residues.  K5 stores
+//      the streams straight into the send buffer in rank-major order,
+//      send[d][x_local][s L + l - d L][z] (4D TMA maps; DistLayout in
+//      nd_internal.cuh) -- no pack copy, no y-stream work arrays.
 //   X. ncclAlltoAll (one per input): rank p receives recv[r][x_local][q'][z]
 //      = [x = r*nx + x_local][q'][z] -- the full x range of its residues.
 //   B. for every owned y-residue, the 2D (x, z) convolution: K5 along x over
 //      all (q', z) columns, K2 on all z-rows of both x-streams, K6 along x
 //      (Function cconv2, applied to the (x, z) plane).
 //   X. ncclAlltoAll back (the result blocks are contiguous per destination).
-//   C. unpack into the y-streams, fftpadForward along y (K6): f <- result.
+//   C. fftpadForward along y (K6) reading both streams from the returned
+//      blocks directly (no unpack copy): f <- result.
 //
 // Communication volume per rank: 6 nx my mz complex words (4 out, 2 back).
 //
 // Hermitian (idc_hconv3d_dist): the global (2mx-1) x (2my-1) x mz array is
 // padded to 2mx x-planes (the last plane is never read; its output is
 // unspecified) and split into nx = 2mx/P planes per rank.  y is centered:
-// A. fft0padBackward along y (K7) -> 3my y-residues per plane (q < 2my-1:
-//    row q of f; q >= 2my-1: row q-(2my-1) of Uy), dealt out nres = 3my/P
-//    per rank; X. all-to-all; B. for every owned y-residue the (x, z) conv2
-//    (Function conv2: K7 along x over the 2mx-1 valid planes, K3
-//    on the z-rows of the three x-streams, K8 along x); X. back; C. K8 along
-//    y.  Doing y before x is valid because the centered x and y transforms
-//    are separable and commute; only z (the Hermitian axis) must come last.
+// A. fft0padBackward along y (K7) -> S = 3 streams (r = -1, 0, 1) of my rows
+//    per plane, dealt out as above (nres = 3 L); X. all-to-all; B. for every
+//    owned y-residue the (x, z) conv2 (Function conv2: K7 along x
+//    over the 2mx-1 valid planes, K3 on the z-rows of the three x-streams, K8
+//    along x); X. back; C. K8 along y from the returned blocks.  Doing y
+//    before x is valid because the centered x and y transforms are separable
+//    and commute; only z (the Hermitian axis) must come last.
+// y lengths outside the TMA pencils (my < 64 or > 4096) run the in-place y
+// passes and copy the streams to / from the blocked layout (copy_streams).
+// One rank: the single-GPU composition (nothing to exchange).
 // The same phases run in a single-process emulation of P ranks on one GPU
 // (idc_cconv3d_dist_emulated) with device copies standing in for the
 // all-to-all; tests use it to exercise the P > 1 path without P GPUs.
@@ -39,6 +45,7 @@
 #include <vector>
 
 #include "../../include/idconv.h"
+#include "config.cuh"
 #include "kernels.cuh"
 #include "nd.cuh"
 #include "nd_internal.cuh"
@@ -58,6 +65,9 @@ struct Plan {
   long mx, my, mz, nx, nres, blk, S;
   long ny, nu;               // y rows of a plane in f (my or 2my-1), in Uy (my or my+1)
   long nxg;                  // global x planes seen by the x pass (mx or 2mx-1)
+  long L;                    // rows of each y stream per destination rank (my / P)
+  int streams;               // y residue streams (2 complex, 3 centered)
+  bool direct;               // TMA y pencils write / read the blocked layout directly
 };
 
 bool pow2(size_t v) { return v >= 1 && (v & (v - 1)) == 0; }
@@ -67,25 +77,30 @@ bool make_plan(bool herm, size_t mx, size_t my, size_t mz, int P, Plan* pl) {
   if (mx > 8192 || my > 8192 || mz > 8192) return false;
   if (herm && (mx < 2 || my < 2 || mz < 2)) return false;
   const size_t planes = herm ? 2 * mx : mx;      // Hermitian: 2mx-1 planes padded to 2mx
-  const size_t yres = herm ? 3 * my : 2 * my;    // y-residue rows per plane
-  if (planes % (size_t)P != 0 || yres % (size_t)P != 0) return false;
+  if (planes % (size_t)P != 0 || my % (size_t)P != 0) return false;
   pl->P = P;
   pl->herm = herm;
   pl->mx = (long)mx;
   pl->my = (long)my;
   pl->mz = (long)mz;
+  pl->streams = herm ? 3 : 2;
+  pl->L = (long)(my / P);
   pl->nx = (long)(planes / P);
-  pl->nres = (long)(yres / P);
+  pl->nres = pl->streams * pl->L;
   pl->blk = pl->nx * pl->nres * pl->mz;
   pl->ny = herm ? 2 * (long)my - 1 : (long)my;
   pl->nu = herm ? (long)my + 1 : (long)my;
   pl->nxg = herm ? 2 * (long)mx - 1 : (long)mx;
   pl->S = pl->nx * pl->ny * pl->mz;              // elements of the local slab
+  pl->direct = IDC_PENCIL_TMA && my >= 64 && my <= 4096;
   return true;
 }
 
-// per-rank workspace: Uy, Vy (nx*nu*mz each), sendF, sendG, recvF, recvG (P*blk each)
-size_t rank_work_elems(const Plan& p) { return 2 * (size_t)p.nx * p.nu * p.mz + 4 * (size_t)p.P * p.blk; }
+// per-rank workspace: Uy, Vy (nx*nu*mz each; only for the copying fallback),
+// sendF, sendG, recvF, recvG (P*blk each)
+size_t rank_work_elems(const Plan& p) {
+  return (p.direct ? 0 : 2 * (size_t)p.nx * p.nu * p.mz) + 4 * (size_t)p.P * p.blk;
+}
 
 struct RankBufs {
   double2 *f, *g, *Uy, *Vy, *sendF, *sendG, *recvF, *recvG;
@@ -95,9 +110,10 @@ RankBufs carve(const Plan& p, double2* f, double2* g, double2* work) {
   RankBufs b;
   b.f = f;
   b.g = g;
-  b.Uy = work;
-  b.Vy = b.Uy + (size_t)p.nx * p.nu * p.mz;
-  b.sendF = b.Vy + (size_t)p.nx * p.nu * p.mz;
+  const size_t u = p.direct ? 0 : (size_t)p.nx * p.nu * p.mz;
+  b.Uy = p.direct ? nullptr : work;
+  b.Vy = p.direct ? nullptr : work + u;
+  b.sendF = work + 2 * u;
   b.sendG = b.sendF + (size_t)p.P * p.blk;
   b.recvF = b.sendG + (size_t)p.P * p.blk;
   b.recvG = b.recvF + (size_t)p.P * p.blk;
@@ -110,39 +126,76 @@ RankBufs carve(const Plan& p, double2* f, double2* g, double2* work) {
     if (e_ != cudaSuccess) return e_; \
   } while (0)
 
-// copy the residue range [qbase, qbase+nres) of the local y-streams (rows of
-// the x-planes: residue q < ny is row q of the in-place stream, q >= ny row
-// q-ny of the extra stream Uy) to/from a [nx][nres][mz] block.
-// dir = 0: streams -> block, 1: block -> streams.
-cudaError_t move_residues(const Plan& p, double2* src_even, double2* src_odd, double2* blk, long qbase, int dir,
-                          cudaStream_t s) {
-  long q = qbase, end = qbase + p.nres;
-  while (q < end) {
-    const bool even = q < p.ny;
-    const long l0 = even ? q : q - p.ny;
-    const long cnt = std::min(end, even ? p.ny : p.ny + p.nu) - q;
-    double2* sp = (even ? src_even : src_odd) + l0 * p.mz;
-    double2* bp = blk + (q - qbase) * p.mz;
-    const size_t width = (size_t)cnt * p.mz * sizeof(double2);
-    const size_t spitch = (size_t)(even ? p.ny : p.nu) * p.mz * sizeof(double2);
-    const size_t bpitch = (size_t)p.nres * p.mz * sizeof(double2);
-    if (dir == 0) TRYC(cudaMemcpy2DAsync(bp, bpitch, sp, spitch, width, p.nx, cudaMemcpyDeviceToDevice, s));
-    else TRYC(cudaMemcpy2DAsync(sp, spitch, bp, bpitch, width, p.nx, cudaMemcpyDeviceToDevice, s));
-    q += cnt;
+// Copying fallback (y lengths outside the TMA pencils): stream st row l of
+// the in-place y passes (rows of f, or of Uy) <-> the blocked layout.
+// Row l of stream st: complex st = 0 -> f row l, st = 1 -> Uy row l;
+// centered st = 0 (r = -1) -> Uy row l, st = 1 (r = 0) -> f row l (l < my-1)
+// or Uy row my (l = my-1), st = 2 (r = +1) -> f row my-1+l.
+// dir = 0: streams -> blocks, 1: blocks -> streams.
+cudaError_t copy_stream_rows(const Plan& p, double2* fs, double2* us, double2* blocks, int st, long l0, long cnt,
+                             int dir, cudaStream_t s) {
+  bool in_u;
+  long row;
+  if (!p.herm) {
+    in_u = st == 1;
+    row = l0;
+  } else if (st == 0) {
+    in_u = true;
+    row = l0;
+  } else if (st == 1) {
+    in_u = l0 == p.my - 1;
+    row = in_u ? p.my : l0;
+  } else {
+    in_u = false;
+    row = p.my - 1 + l0;
   }
+  double2* sp = (in_u ? us : fs) + row * p.mz;
+  const long d = l0 / p.L;
+  double2* bp = blocks + d * p.blk + (st * p.L + l0 % p.L) * p.mz;
+  const size_t width = (size_t)cnt * p.mz * sizeof(double2);
+  const size_t spitch = (size_t)(in_u ? p.nu : p.ny) * p.mz * sizeof(double2);
+  const size_t bpitch = (size_t)p.nres * p.mz * sizeof(double2);
+  if (dir == 0) return cudaMemcpy2DAsync(bp, bpitch, sp, spitch, width, p.nx, cudaMemcpyDeviceToDevice, s);
+  return cudaMemcpy2DAsync(sp, spitch, bp, bpitch, width, p.nx, cudaMemcpyDeviceToDevice, s);
+}
+
+cudaError_t copy_streams(const Plan& p, double2* fs, double2* us, double2* blocks, int dir, cudaStream_t s) {
+  for (int st = 0; st < p.streams; ++st)
+    for (long d = 0; d < p.P; ++d) {
+      long cnt = p.L;
+      if (p.herm && st == 1 && d == p.P - 1) {   // the r = 0 stream's last row lives in Uy row my
+        TRYC(copy_stream_rows(p, fs, us, blocks, st, p.my - 1, 1, dir, s));
+        --cnt;
+      }
+      if (cnt > 0) TRYC(copy_stream_rows(p, fs, us, blocks, st, d * p.L, cnt, dir, s));
+    }
   return cudaSuccess;
 }
 
-// phase A: y-pass + rank-major pack
+idc::DistLayout layout(const Plan& p, double2* a, double2* b) {
+  idc::DistLayout dl;
+  dl.base[0] = a;
+  dl.base[1] = b;
+  dl.L = p.L;
+  dl.nblocks = p.P;
+  dl.xstride = p.nres * p.mz;
+  dl.blk = p.blk;
+  dl.S = p.streams;
+  return dl;
+}
+
+// phase A: y-pass into the rank-major send blocks
 cudaError_t phase_a(const Plan& p, const RankBufs& b, cudaStream_t s) {
   const long ps = p.ny * p.mz, us = p.nu * p.mz;
+  if (p.direct) {
+    const idc::DistLayout dl = layout(p, b.sendF, b.sendG);
+    if (p.herm) return launch_pad0_bwd(b.f, b.g, nullptr, nullptr, (int)p.my, p.mz, p.nx, ps, us, s, &dl);
+    return launch_pad_bwd(b.f, b.g, nullptr, nullptr, (int)p.my, p.mz, p.nx, ps, us, s, double2{1.0, 0.0}, &dl);
+  }
   if (p.herm) TRYC(launch_pad0_bwd(b.f, b.g, b.Uy, b.Vy, (int)p.my, p.mz, p.nx, ps, us, s));
   else TRYC(launch_pad_bwd(b.f, b.g, b.Uy, b.Vy, (int)p.my, p.mz, p.nx, ps, us, s));
-  for (int d = 0; d < p.P; ++d) {
-    TRYC(move_residues(p, b.f, b.Uy, b.sendF + (size_t)d * p.blk, (long)d * p.nres, 0, s));
-    TRYC(move_residues(p, b.g, b.Vy, b.sendG + (size_t)d * p.blk, (long)d * p.nres, 0, s));
-  }
-  return cudaSuccess;
+  TRYC(copy_streams(p, b.f, b.Uy, b.sendF, 0, s));
+  return copy_streams(p, b.g, b.Vy, b.sendG, 0, s);
 }
 
 // phase B: 2D (x, z) convolution of the owned residues; recvF <- result.
@@ -163,11 +216,15 @@ cudaError_t phase_b(const Plan& p, const RankBufs& b, double2* roww, cudaStream_
   return launch_pad_fwd(b.recvF, b.sendF, (int)p.mx, cols, 1, 0, 0, s);
 }
 
-// phase C: unpack the returned blocks (in sendF) into the y-streams, y-forward.
+// phase C: y-forward from the returned blocks (in sendF): f <- result.
 cudaError_t phase_c(const Plan& p, const RankBufs& b, cudaStream_t s) {
-  for (int src = 0; src < p.P; ++src)
-    TRYC(move_residues(p, b.f, b.Uy, b.sendF + (size_t)src * p.blk, (long)src * p.nres, 1, s));
   const long ps = p.ny * p.mz, us = p.nu * p.mz;
+  if (p.direct) {
+    const idc::DistLayout dl = layout(p, b.sendF, nullptr);
+    if (p.herm) return launch_pad0_fwd(b.f, nullptr, (int)p.my, p.mz, p.nx, ps, us, s, &dl);
+    return launch_pad_fwd(b.f, nullptr, (int)p.my, p.mz, p.nx, ps, us, s, double2{1.0, 0.0}, &dl);
+  }
+  TRYC(copy_streams(p, b.f, b.Uy, b.sendF, 1, s));
   if (p.herm) return launch_pad0_fwd(b.f, b.Uy, (int)p.my, p.mz, p.nx, ps, us, s);
   return launch_pad_fwd(b.f, b.Uy, (int)p.my, p.mz, p.nx, ps, us, s);
 }
@@ -234,7 +291,8 @@ size_t idc_dist_workspace_bytes(idc_kind k, size_t mx, size_t my, size_t mz, int
 }
 
 // Host-side plan of the decomposition (pure logic, no GPU): fills
-// out[0..5] = {nx, nres, blk, local planes x0, first residue q0, S}.
+// out[0..5] = {nx, nres, blk, first local plane x0, first owned row l0 of
+// every y stream (rank * my / P), S}.
 idc_status idc_dist_plan_kind(idc_kind k, size_t mx, size_t my, size_t mz, int nranks, int rank, long long* out) {
   Plan p;
   if (!out || rank < 0 || rank >= nranks || (k != IDC_CCONV3D && k != IDC_HCONV3D) ||
@@ -244,7 +302,7 @@ idc_status idc_dist_plan_kind(idc_kind k, size_t mx, size_t my, size_t mz, int n
   out[1] = p.nres;
   out[2] = p.blk;
   out[3] = (long long)rank * p.nx;
-  out[4] = (long long)rank * p.nres;
+  out[4] = (long long)rank * p.L;
   out[5] = p.S;
   return IDC_OK;
 }

@@ -335,27 +335,33 @@ cudaError_t pad0_fwd_n(double2* f, const double2* U, long ncols, long batch, lon
       default: break;                                               \
     }
 
+// dl (distributed blocked stream layout, dist.cu): the TMA pencils only; the
+// other sizes return cudaErrorNotSupported and dist.cu packs instead
 cudaError_t launch_pad_bwd(double2* f, double2* g, double2* U, double2* V, int m, long ncols, long batch,
-                           long bstride, long ustride, cudaStream_t s, double2 odd_phase) {
-  IDC_TDISPATCH(m, return pad_bwd_tma<NN>(f, g, U, V, ncols, batch, bstride, ustride, s, odd_phase));
+                           long bstride, long ustride, cudaStream_t s, double2 odd_phase, const DistLayout* dl) {
+  IDC_TDISPATCH(m, return pad_bwd_tma<NN>(f, g, U, V, ncols, batch, bstride, ustride, s, odd_phase, dl));
+  if (dl) return cudaErrorNotSupported;
   IDC_PDISPATCH(m, return pad_bwd_n<NN>(f, g, U, V, ncols, batch, bstride, ustride, s, odd_phase));
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_pad_fwd(double2* f, const double2* U, int m, long ncols, long batch, long bstride, long ustride,
-                           cudaStream_t s, double2 odd_phase) {
-  IDC_TDISPATCH(m, return pad_fwd_tma<NN>(f, U, ncols, batch, bstride, ustride, s, odd_phase));
+                           cudaStream_t s, double2 odd_phase, const DistLayout* dl) {
+  IDC_TDISPATCH(m, return pad_fwd_tma<NN>(f, U, ncols, batch, bstride, ustride, s, odd_phase, dl));
+  if (dl) return cudaErrorNotSupported;
   IDC_PDISPATCH(m, return pad_fwd_n<NN>(f, U, ncols, batch, bstride, ustride, s, odd_phase));
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_pad0_bwd(double2* f, double2* g, double2* U, double2* V, int m, long ncols, long batch,
-                            long bstride, long ustride, cudaStream_t s) {
-  IDC_TDISPATCH(m, return pad0_bwd_tma<NN>(f, g, U, V, ncols, batch, bstride, ustride, s));
+                            long bstride, long ustride, cudaStream_t s, const DistLayout* dl) {
+  IDC_TDISPATCH(m, return pad0_bwd_tma<NN>(f, g, U, V, ncols, batch, bstride, ustride, s, dl));
+  if (dl) return cudaErrorNotSupported;
   IDC_PDISPATCH(m, return pad0_bwd_n<NN>(f, g, U, V, ncols, batch, bstride, ustride, s));
   return cudaErrorInvalidValue;
 }
 cudaError_t launch_pad0_fwd(double2* f, const double2* U, int m, long ncols, long batch, long bstride, long ustride,
-                            cudaStream_t s) {
-  IDC_TDISPATCH(m, return pad0_fwd_tma<NN>(f, U, ncols, batch, bstride, ustride, s));
+                            cudaStream_t s, const DistLayout* dl) {
+  IDC_TDISPATCH(m, return pad0_fwd_tma<NN>(f, U, ncols, batch, bstride, ustride, s, dl));
+  if (dl) return cudaErrorNotSupported;
   IDC_PDISPATCH(m, return pad0_fwd_n<NN>(f, U, ncols, batch, bstride, ustride, s));
   return cudaErrorInvalidValue;
 }

@@ -13,6 +13,7 @@
 #include "config.cuh"
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstring>
 
 #include "fft_dev.cuh"
@@ -126,6 +127,37 @@ __device__ __forceinline__ void tile_store(const double2 (&v)[E], int t, int c, 
   }
 }
 
+// Distributed y passes (dist.cu): the residue streams live in the blocked
+// rank-major layout of the all-to-all buffers -- stream s row l of local
+// plane x at base + (l / L) blk + x (S L ncols) + (s L + l % L) ncols -- so the
+// backward pencils store into the send buffer and the forward pencils load
+// from the returned blocks directly (no pack / unpack copies).  One 4D map per
+// (input, stream), boxes of BRd <= L rows.
+struct DistIO {
+  CUtensorMap st[2][3];   // [input][stream]
+  int L, BRd;
+};
+
+template <int N, int E, int W>
+__device__ __forceinline__ void tile_store_dist(const double2 (&v)[E], int t, int c, double2* xb, const CUtensorMap* map,
+                                                long col0, long item, int L, int BRd) {
+  constexpr int T = N / E;
+#pragma unroll
+  for (int i = 0; i < E; ++i) xb[(t + T * i) * W + c] = v[i];
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int r0 = 0; r0 < N; r0 += BRd) tma_store_4d(map, (int)(2 * col0), r0 % L, (int)item, r0 / L, xb + (long)r0 * W);
+    bulk_commit();
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void load_rows_dist(const CUtensorMap* map, double2* stage, long col0, int nrows, long item,
+                                               int L, int BRd, uint64_t* bar) {
+  for (int b = 0; b < nrows; b += BRd) tma_load_4d(stage + (long)b * W, map, (int)(2 * col0), b % L, (int)item, b / L, bar);
+}
+
 }  // namespace
 
 // K5 / K6: tiles of at most IDC_K56_TMA_STORE_MAXW columns (16-32-byte row segments,
@@ -144,16 +176,17 @@ constexpr bool k5_double_xb() {
 }
 
 // ------------------------------------------------------------------- K5 --
-template <int N>
+template <int N, bool DIST = false>
 __global__ void __launch_bounds__(K56Cfg<N>::THREADS, IDC_PENCIL_MINB)
 k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mg, double2* __restrict__ f,
               double2* __restrict__ g, double2* __restrict__ U, double2* __restrict__ V, Tiles tl,
               const double2* __restrict__ twN, const double2* __restrict__ tw2N, double2 ophase,
-              const __grid_constant__ CUtensorMap mU, const __grid_constant__ CUtensorMap mV) {
+              const __grid_constant__ CUtensorMap mU, const __grid_constant__ CUtensorMap mV,
+              const __grid_constant__ DistIO dio) {
   using C = K56Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
-  constexpr bool TS = W <= IDC_K56_TMA_STORE_MAXW;   // outputs by TMA stores
-  constexpr bool DB = k5_double_xb<N>();              // second exchange buffer for the even stream
+  constexpr bool TS = DIST || W <= IDC_K56_TMA_STORE_MAXW;   // outputs by TMA stores
+  constexpr bool DB = !DIST && k5_double_xb<N>();            // second exchange buffer for the even stream
   extern __shared__ __align__(128) double2 smem[];
   double2* stage = smem;                       // N x W
   double2* xb = stage + N * W;
@@ -210,12 +243,14 @@ k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
         // store's barrier
         tile_store<N, E, W, BR>(v, t, c, xb, in == 0 ? &mU : &mV, col0, item, true);
       } else {
-        tile_store<N, E, W, BR>(v, t, c, xb, in == 0 ? &mU : &mV, col0, item);
+        if constexpr (DIST) tile_store_dist<N, E, W>(v, t, c, xb, &dio.st[in][1], col0, item, dio.L, dio.BRd);
+        else tile_store<N, E, W, BR>(v, t, c, xb, in == 0 ? &mU : &mV, col0, item);
         if (threadIdx.x == 0) bulk_wait_read();
         __syncthreads();
       }
-      fft<N, E, +1>(x0, t, xb1, twN, CtaSync{}, xs);   // even stream, in place
-      tile_store<N, E, W, BR>(x0, t, c, xb1, in == 0 ? &mf : &mg, col0, item);
+      fft<N, E, +1>(x0, t, xb1, twN, CtaSync{}, xs);   // even stream (in place, or to the send blocks)
+      if constexpr (DIST) tile_store_dist<N, E, W>(x0, t, c, xb1, &dio.st[in][0], col0, item, dio.L, dio.BRd);
+      else tile_store<N, E, W, BR>(x0, t, c, xb1, in == 0 ? &mf : &mg, col0, item);
     } else {
       const long rs = (long)T * tl.ncols;   // pointer step between a thread's rows
       if (ok) {
@@ -235,13 +270,24 @@ k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
 }
 
 // ------------------------------------------------------------------- K6 --
-template <int N>
+template <int N, bool DIST = false>
 __global__ void __launch_bounds__(K56Cfg<N>::THREADS, IDC_PENCIL_MINB)
 k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mu, double2* __restrict__ f,
-              Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw2N, double2 ophase) {
+              Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw2N, double2 ophase,
+              const __grid_constant__ DistIO dio) {
   using C = K56Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   constexpr bool TS = W <= IDC_K56_TMA_STORE_MAXW;   // output by TMA stores
+  // stream loads: the even stream from f / the odd one from U, or (DIST) both
+  // from the returned blocks
+  auto load_u = [&](double2* dst, long col0, long item, uint64_t* bar) {
+    if constexpr (DIST) load_rows_dist<W>(&dio.st[0][1], dst, col0, N, item, dio.L, dio.BRd, bar);
+    else load_rows<W, BR>(&mu, dst, col0, 0, N, item, bar);
+  };
+  auto load_f = [&](double2* dst, long col0, long item, uint64_t* bar) {
+    if constexpr (DIST) load_rows_dist<W>(&dio.st[0][0], dst, col0, N, item, dio.L, dio.BRd, bar);
+    else load_rows<W, BR>(&mf, dst, col0, 0, N, item, bar);
+  };
   extern __shared__ __align__(128) double2 smem[];
   double2* sf = smem;
   double2* su = sf + N * W;
@@ -261,9 +307,9 @@ k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
     int in; long item, col0;
     tile_coords(tl, tau, W, in, item, col0);
     mbar_arrive_expect_tx(&bars[1], BYTES);
-    load_rows<W, BR>(&mu, su, col0, 0, N, item, &bars[1]);
+    load_u(su, col0, item, &bars[1]);
     mbar_arrive_expect_tx(&bars[0], BYTES);
-    load_rows<W, BR>(&mf, sf, col0, 0, N, item, &bars[0]);
+    load_f(sf, col0, item, &bars[0]);
   }
   const double inv = 1.0 / (2.0 * N);
   uint32_t phase = 0;
@@ -284,7 +330,7 @@ k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
     __syncthreads();
     if (threadIdx.x == 0 && nx < tl.ntiles) {
       mbar_arrive_expect_tx(&bars[1], BYTES);
-      load_rows<W, BR>(&mu, su, c2, 0, N, item2, &bars[1]);
+      load_u(su, c2, item2, &bars[1]);
     }
     fft<N, E, -1>(v, t, xb, twN, CtaSync{}, xs);
     for_roots<2 * E, 1, -1, E>(cconj(ldtw(&tw2N[t])), [&](int i, double2 w) { s[i] = cmul(cmul(v[i], w), ophase); });  // c zeta_{2m}^{-k} U_k
@@ -295,7 +341,7 @@ k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
     __syncthreads();
     if (threadIdx.x == 0 && nx < tl.ntiles) {
       mbar_arrive_expect_tx(&bars[0], BYTES);
-      load_rows<W, BR>(&mf, sf, c2, 0, N, item2, &bars[0]);
+      load_f(sf, c2, item2, &bars[0]);
     }
     fft<N, E, -1>(v, t, xb, twN, CtaSync{}, xs);
     if constexpr (TS) {
@@ -328,12 +374,13 @@ struct K7StoreMaps {
   CUtensorMap flo, fhi, glo, ghi, u, v;
 };
 
-template <int N>
+template <int N, bool DIST = false>
 __global__ void __launch_bounds__(K78Cfg<N>::THREADS, IDC_PENCIL0_MINB)
 k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mg,
                double2* __restrict__ f, double2* __restrict__ g, double2* __restrict__ U, double2* __restrict__ V,
                Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw3N,
-               const __grid_constant__ K7StoreMaps sm) {
+               const __grid_constant__ K7StoreMaps sm, const __grid_constant__ DistIO dio) {
+  static_assert(!DIST || IDC_K7_TMA_STORE, "distributed K7 stores through TMA");
   using C = K78Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   constexpr int R2 = ((2 * N - 1 + BR - 1) / BR) * BR;              // staged rows
@@ -435,6 +482,16 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
       fft<N, E, +1>(v, t, xb, twN, CtaSync{}, xs);  // ends with a barrier after its last exchange
 #pragma unroll
       for (int i = 0; i < E; ++i) xb[(t + T * i) * W + c] = v[i];
+      if constexpr (DIST) {                         // stream r = (r+1)-th map of the send blocks, m rows
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          for (int b = 0; b < N; b += dio.BRd)
+            tma_store_4d(&dio.st[in][r + 1], (int)(2 * col0), b % dio.L, (int)item, b / dio.L, xb + (long)b * W);
+          bulk_commit();
+        }
+        continue;
+      }
       if (r == 0 && t == T - 1 && ok) u[(long)N * S] = v[E - 1];   // l = m-1 -> U row m
       fence_proxy_async_smem();
       __syncthreads();
@@ -470,12 +527,14 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
 // Streams staged one at a time (double buffered): q = 0 (r = -1: U rows
 // 0..N-1), q = 1 (r = 0: f rows 0..N-2 and U row N, the latter through a
 // one-row box into a separate tail slot), q = 2 (r = +1: f rows N-1..2N-2).
-template <int N>
+template <int N, bool DIST = false>
 __global__ void __launch_bounds__(K78Cfg<N>::THREADS, IDC_PENCIL_MINB)
 k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mu,
                const __grid_constant__ CUtensorMap mu1, double2* __restrict__ f, Tiles tl,
                const double2* __restrict__ twN, const double2* __restrict__ tw3N,
-               const __grid_constant__ CUtensorMap mflo, const __grid_constant__ CUtensorMap mfhi) {
+               const __grid_constant__ CUtensorMap mflo, const __grid_constant__ CUtensorMap mfhi,
+               const __grid_constant__ DistIO dio) {
+  static_assert(!DIST || IDC_K8_TMA_STORE == 2, "distributed K8 stores through TMA");
   using C = K78Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   extern __shared__ __align__(128) double2 smem[];
@@ -496,6 +555,11 @@ k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
   auto issue = [&](long tau, int q, int b) {
     int in; long item, col0;
     tile_coords(tl, tau, W, in, item, col0);
+    if constexpr (DIST) {                   // stream r = q - 1: m uniform rows of the returned blocks
+      mbar_arrive_expect_tx(&bars[b], (uint32_t)N * W * 16);
+      load_rows_dist<W>(&dio.st[0][q], st[b], col0, N, item, dio.L, dio.BRd, &bars[b]);
+      return;
+    }
     if (q == 0) {
       mbar_arrive_expect_tx(&bars[b], (uint32_t)N * W * 16);
       load_rows<W, BR>(&mu, st[b], col0, 0, N, item, &bars[b]);
@@ -535,7 +599,7 @@ k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         const int l = t + T * i;
-        v[i] = (q == 1 && l == N - 1) ? tail[b][c] : st[b][l * W + c];
+        v[i] = (!DIST && q == 1 && l == N - 1) ? tail[b][c] : st[b][l * W + c];
       }
 #if IDC_K8_TMA_STORE
       if (q == 0 && threadIdx.x == 0) bulk_wait_read();   // last tile's output stores have read xb
@@ -637,6 +701,19 @@ cudaError_t launch_t(K kernel, int threads, size_t smem, long ntiles, cudaStream
   return launch_kernel((const void*)kernel, dim3((unsigned)grid), dim3(threads), args, smem, s, tag);
 }
 
+// DistIO maps of a host DistLayout (nd_internal.cuh), one per (input, stream)
+bool make_dist_io(DistIO* io, const DistLayout& dl, long ncols, long nx, int W, int BR, int inputs) {
+  memset(io, 0, sizeof(*io));
+  io->L = (int)dl.L;
+  io->BRd = (int)std::min<long>(BR, dl.L);
+  for (int in = 0; in < inputs; ++in)
+    for (int st = 0; st < dl.S; ++st)
+      if (!encode_blocked_map(&io->st[in][st], dl.base[in] + (long)st * dl.L * ncols, ncols, dl.L, nx, dl.nblocks,
+                              dl.xstride, dl.blk, W, io->BRd))
+        return false;
+  return true;
+}
+
 template <int W>
 Tiles make_tiles(long ncols, long batch, int inputs, long bstride, long ustride) {
   Tiles tl;
@@ -654,7 +731,7 @@ Tiles make_tiles(long ncols, long batch, int inputs, long bstride, long ustride)
 
 template <int N>
 cudaError_t pad_bwd_tma(double2* f, double2* g, double2* U, double2* V, long ncols, long batch, long bstride,
-                        long ustride, cudaStream_t s, double2 ophase) {
+                        long ustride, cudaStream_t s, double2 ophase, const DistLayout* dl) {
   using C = K56Cfg<N>;
   const double2* twN = pass_table(N, C::E);
   const double2* tw2N = zeta_table(2 * N);
@@ -664,32 +741,54 @@ cudaError_t pad_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nco
   if (!encode_pencil_map(&mg, g ? g : f, ncols, N, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
   Tiles tl = make_tiles<C::W>(ncols, batch, g ? 2 : 1, bstride, ustride);
   CUtensorMap mU, mV;
-  if (!encode_pencil_map(&mU, U, ncols, N, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
-  if (!encode_pencil_map(&mV, g ? V : U, ncols, N, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
-  void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw2N, &ophase, &mU, &mV};
+  DistIO dio;
+  if (dl) {                                    // streams into the send blocks; U, V unused
+    if (!make_dist_io(&dio, *dl, ncols, batch, C::W, C::BR, g ? 2 : 1)) return cudaErrorNotSupported;
+    mU = mf;
+    mV = mf;
+  } else {
+    memset(&dio, 0, sizeof(dio));
+    if (!encode_pencil_map(&mU, U, ncols, N, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
+    if (!encode_pencil_map(&mV, g ? V : U, ncols, N, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
+  }
+  void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw2N, &ophase, &mU, &mV, &dio};
+  const LaunchTag tag{"K5", N, ncols * batch * (g ? 2 : 1)};
+  if (dl) {
+    const size_t smem = ((size_t)N * C::W + (size_t)C::XB) * 16 + 16;
+    return launch_t(k_pad_bwd_tma<N, true>, C::THREADS, smem, tl.ntiles, s, args, tag);
+  }
   const size_t smem = ((size_t)N * C::W + (k5_double_xb<N>() ? 2 : 1) * (size_t)C::XB) * 16 + 16;
-  return launch_t(k_pad_bwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args, {"K5", N, ncols * batch * (g ? 2 : 1)});
+  return launch_t(k_pad_bwd_tma<N, false>, C::THREADS, smem, tl.ntiles, s, args, tag);
 }
 
 template <int N>
 cudaError_t pad_fwd_tma(double2* f, const double2* U, long ncols, long batch, long bstride, long ustride,
-                        cudaStream_t s, double2 ophase) {
+                        cudaStream_t s, double2 ophase, const DistLayout* dl) {
   using C = K56Cfg<N>;
   const double2* twN = pass_table(N, C::E);
   const double2* tw2N = zeta_table(2 * N);
   if (!twN || !tw2N) return cudaErrorMemoryAllocation;
   CUtensorMap mf, mu;
   if (!encode_pencil_map(&mf, f, ncols, N, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
-  if (!encode_pencil_map(&mu, U, ncols, N, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
+  DistIO dio;
+  if (dl) {                                    // both streams from the returned blocks; U unused
+    if (!make_dist_io(&dio, *dl, ncols, batch, C::W, C::BR, 1)) return cudaErrorNotSupported;
+    mu = mf;
+  } else {
+    memset(&dio, 0, sizeof(dio));
+    if (!encode_pencil_map(&mu, U, ncols, N, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
+  }
   Tiles tl = make_tiles<C::W>(ncols, batch, 1, bstride, ustride);
-  void* args[] = {&mf, &mu, &f, &tl, &twN, &tw2N, &ophase};
+  void* args[] = {&mf, &mu, &f, &tl, &twN, &tw2N, &ophase, &dio};
   const size_t smem = (2 * (size_t)N * C::W + C::XB) * 16 + 32;
-  return launch_t(k_pad_fwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args, {"K6", N, ncols * batch});
+  const LaunchTag tag{"K6", N, ncols * batch};
+  if (dl) return launch_t(k_pad_fwd_tma<N, true>, C::THREADS, smem, tl.ntiles, s, args, tag);
+  return launch_t(k_pad_fwd_tma<N, false>, C::THREADS, smem, tl.ntiles, s, args, tag);
 }
 
 template <int N>
 cudaError_t pad0_bwd_tma(double2* f, double2* g, double2* U, double2* V, long ncols, long batch, long bstride,
-                         long ustride, cudaStream_t s) {
+                         long ustride, cudaStream_t s, const DistLayout* dl) {
   using C = K78Cfg<N>;
   constexpr int R2 = ((2 * N - 1 + C::BR - 1) / C::BR) * C::BR;
   const double2* twN = pass_table(N, C::E);
@@ -700,8 +799,13 @@ cudaError_t pad0_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nc
   if (!encode_pencil_map(&mg, g ? g : f, ncols, 2 * N - 1, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
   Tiles tl = make_tiles<C::W>(ncols, batch, g ? 2 : 1, bstride, ustride);
   K7StoreMaps sm;
+  memset(&sm, 0, sizeof(sm));
+  DistIO dio;
+  memset(&dio, 0, sizeof(dio));
+  if (dl) {                                    // the three streams into the send blocks
+    if (!make_dist_io(&dio, *dl, ncols, batch, C::W, C::BR, g ? 2 : 1)) return cudaErrorNotSupported;
+  } else {
 #if IDC_K7_TMA_STORE
-  {
     double2* gg = g ? g : f;
     double2* VV = g ? V : U;
     const long lo = ((long)N - 1) * ncols;
@@ -712,43 +816,55 @@ cudaError_t pad0_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nc
         !encode_pencil_map(&sm.u, U, ncols, N, batch, ustride, C::W, C::BR) ||
         !encode_pencil_map(&sm.v, VV, ncols, N, batch, ustride, C::W, C::BR))
       return cudaErrorNotSupported;
-  }
-#else
-  memset(&sm, 0, sizeof(sm));
 #endif
-  void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw3N, &sm};
+  }
+  void* args[] = {&mf, &mg, &f, &g, &U, &V, &tl, &twN, &tw3N, &sm, &dio};
   const size_t smem = ((size_t)R2 * C::W + C::XB) * 16 + 16;
-  return launch_t(k_pad0_bwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args, {"K7", N, ncols * batch * (g ? 2 : 1)});
+  const LaunchTag tag{"K7", N, ncols * batch * (g ? 2 : 1)};
+  if (dl) return launch_t(k_pad0_bwd_tma<N, true>, C::THREADS, smem, tl.ntiles, s, args, tag);
+  return launch_t(k_pad0_bwd_tma<N, false>, C::THREADS, smem, tl.ntiles, s, args, tag);
 }
 
 template <int N>
 cudaError_t pad0_fwd_tma(double2* f, const double2* U, long ncols, long batch, long bstride, long ustride,
-                         cudaStream_t s) {
+                         cudaStream_t s, const DistLayout* dl) {
   using C = K78Cfg<N>;
   const double2* twN = pass_table(N, C::E);
   const double2* tw3N = zeta_table(3 * N);
   if (!twN || !tw3N) return cudaErrorMemoryAllocation;
   CUtensorMap mf, mu, mu1;
   if (!encode_pencil_map(&mf, f, ncols, 2 * N - 1, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
-  if (!encode_pencil_map(&mu, U, ncols, N + 1, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
-  if (!encode_pencil_map(&mu1, U, ncols, N + 1, batch, ustride, C::W, 1)) return cudaErrorNotSupported;
+  DistIO dio;
+  memset(&dio, 0, sizeof(dio));
+  if (dl) {                                    // the three streams from the returned blocks; U unused
+    if (!make_dist_io(&dio, *dl, ncols, batch, C::W, C::BR, 1)) return cudaErrorNotSupported;
+    mu = mf;
+    mu1 = mf;
+  } else {
+    if (!encode_pencil_map(&mu, U, ncols, N + 1, batch, ustride, C::W, C::BR)) return cudaErrorNotSupported;
+    if (!encode_pencil_map(&mu1, U, ncols, N + 1, batch, ustride, C::W, 1)) return cudaErrorNotSupported;
+  }
   Tiles tl = make_tiles<C::W>(ncols, batch, 1, bstride, ustride);
   CUtensorMap mflo, mfhi;
   if (!encode_pencil_map(&mflo, f, ncols, N - 1, batch, bstride, C::W, C::BR)) return cudaErrorNotSupported;
   if (!encode_pencil_map(&mfhi, f + ((long)N - 1) * ncols, ncols, N, batch, bstride, C::W, C::BR))
     return cudaErrorNotSupported;
-  void* args[] = {&mf, &mu, &mu1, &f, &tl, &twN, &tw3N, &mflo, &mfhi};
+  void* args[] = {&mf, &mu, &mu1, &f, &tl, &twN, &tw3N, &mflo, &mfhi, &dio};
   const size_t smem = (2 * (size_t)N * C::W + 32 + C::XB) * 16 + 32;
-  return launch_t(k_pad0_fwd_tma<N>, C::THREADS, smem, tl.ntiles, s, args, {"K8", N, ncols * batch});
+  const LaunchTag tag{"K8", N, ncols * batch};
+  if (dl) return launch_t(k_pad0_fwd_tma<N, true>, C::THREADS, smem, tl.ntiles, s, args, tag);
+  return launch_t(k_pad0_fwd_tma<N, false>, C::THREADS, smem, tl.ntiles, s, args, tag);
 }
 
 #define IDC_INST_T(N)                                                                                           \
   template cudaError_t pad_bwd_tma<N>(double2*, double2*, double2*, double2*, long, long, long, long, cudaStream_t, \
-                                      double2);                                                                    \
-  template cudaError_t pad_fwd_tma<N>(double2*, const double2*, long, long, long, long, cudaStream_t, double2);     \
+                                      double2, const DistLayout*);                                                 \
+  template cudaError_t pad_fwd_tma<N>(double2*, const double2*, long, long, long, long, cudaStream_t, double2,      \
+                                      const DistLayout*);                                                          \
   template cudaError_t pad0_bwd_tma<N>(double2*, double2*, double2*, double2*, long, long, long, long,             \
-                                       cudaStream_t);                                                            \
-  template cudaError_t pad0_fwd_tma<N>(double2*, const double2*, long, long, long, long, cudaStream_t);
+                                       cudaStream_t, const DistLayout*);                                         \
+  template cudaError_t pad0_fwd_tma<N>(double2*, const double2*, long, long, long, long, cudaStream_t,             \
+                                       const DistLayout*);
 IDC_INST_T(64)
 IDC_INST_T(128)
 IDC_INST_T(256)

@@ -16,4 +16,11 @@ namespace idc {
 bool encode_pencil_map(CUtensorMap* map, const void* base, long ncols, long rows, long batch, long bstride, int W,
                        int BR, bool swizzle128 = false);
 
+// One stream of the distributed blocked layout (dist.cu): row l (0..rows-1)
+// of local plane x lives at base + (l / L) * blk + x * xstride + (l % L) * ncols
+// (elements), i.e. a 4D tensor (2 ncols doubles, L, nx, rows / L) tiled by
+// boxes of W columns x BR rows (BR <= L).
+bool encode_blocked_map(CUtensorMap* map, const void* base, long ncols, long L, long nx, long nblocks, long xstride,
+                        long blk, int W, int BR);
+
 }  // namespace idc

@@ -476,7 +476,7 @@ def dist_plan(mx: int, my: int, mz: int, nranks: int, rank: int, kind: int = Non
     out = (ctypes.c_longlong * 6)()
     k = CCONV3D if kind is None else kind
     _check(lib().idc_dist_plan_kind(k, mx, my, mz, nranks, rank, out), "idc_dist_plan_kind")
-    return dict(nx=out[0], nres=out[1], blk=out[2], x0=out[3], q0=out[4], S=out[5])
+    return dict(nx=out[0], nres=out[1], blk=out[2], x0=out[3], l0=out[4], S=out[5])
 
 
 class Comm:

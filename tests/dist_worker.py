@@ -1,7 +1,8 @@
 """Worker of the gloo tests of the distributed cconv3d / hconv3d decompositions.
 
 Each rank follows the library's own host-side plan (idc_dist_plan, pure C
-logic) for which x-planes it owns and which y-residues it receives, moves the
+logic) for which x-planes it owns and which y-residues it receives (rows
+[rank L, (rank+1) L) of every y stream, L = my / P), moves the
 residue blocks with a real collective (torch.distributed all_to_all_single
 over gloo), and evaluates the per-rank arithmetic with the oracle's implicit
 equations (numpy; the GPU kernels are covered by the emulated-rank GPU test).
@@ -37,9 +38,17 @@ def run(rank, world, port, shape, outdir):
         e, o = implicit.fftpad_backward(np.swapaxes(a, 1, 2))      # along y
         return np.concatenate([np.swapaxes(e, 1, 2), np.swapaxes(o, 1, 2)], axis=1)  # residues q = 0..2my-1
 
-    def pack(streams):
-        blocks = [streams[:, p * nres:(p + 1) * nres, :] for p in range(world)]
-        return torch.from_numpy(np.ascontiguousarray(np.stack(blocks)))   # [p][x][q'][z]
+    L = my // world                                               # rows of each stream per rank
+
+    def pack(streams, S=2):
+        """rank p receives rows [p L, (p+1) L) of each of the S streams (q = s my + l)"""
+        blocks = [np.concatenate([streams[:, s * my + p * L: s * my + (p + 1) * L, :] for s in range(S)], axis=1)
+                  for p in range(world)]
+        return torch.from_numpy(np.ascontiguousarray(np.stack(blocks)))   # [p][x][s L + l'][z]
+
+    def unpack(back, S=2):
+        return np.concatenate([np.concatenate([back[p][:, s * L:(s + 1) * L, :] for p in range(world)], axis=1)
+                               for s in range(S)], axis=1)               # [x][s my + l][z]
 
     sf, sg = pack(ypass(fl)), pack(ypass(gl))
     rf, rg = torch.empty_like(sf), torch.empty_like(sg)
@@ -53,8 +62,8 @@ def run(rank, world, port, shape, outdir):
     send_back = torch.from_numpy(np.ascontiguousarray(out.reshape(world, nx, nres, mz)))
     back = torch.empty_like(send_back)
     dist.all_to_all_single(back.view(torch.float64), send_back.view(torch.float64))
-    # phase C: unpack residues of every source rank, fftpadForward along y
-    streams = np.concatenate([back.numpy()[p] for p in range(world)], axis=1)   # [x][2my][z]
+    # phase C: the streams from every source rank's block, fftpadForward along y
+    streams = unpack(back.numpy())                                            # [x][2my][z]
     e, o = streams[:, :my, :], streams[:, my:, :]
     res = np.swapaxes(implicit.fftpad_forward(np.swapaxes(e, 1, 2), np.swapaxes(o, 1, 2)), 1, 2)
     np.save(os.path.join(outdir, f"rank{rank}.npy"), res)
@@ -87,9 +96,16 @@ def run_herm(rank, world, port, shape, outdir):
         S = implicit.fft0pad_backward(np.moveaxis(a, 1, -1))          # r -> (nx, mz, my)
         return np.concatenate([np.moveaxis(S[r], -1, 1) for r in (-1, 0, 1)], axis=1)  # q = (r+1) my + l
 
-    def pack(streams):
-        blocks = [streams[:, p * nres:(p + 1) * nres, :] for p in range(world)]
+    L = my // world
+
+    def pack(streams, S=3):
+        blocks = [np.concatenate([streams[:, s * my + p * L: s * my + (p + 1) * L, :] for s in range(S)], axis=1)
+                  for p in range(world)]
         return torch.from_numpy(np.ascontiguousarray(np.stack(blocks)))
+
+    def unpack(back, S=3):
+        return np.concatenate([np.concatenate([back[p][:, s * L:(s + 1) * L, :] for p in range(world)], axis=1)
+                               for s in range(S)], axis=1)
 
     sf, sg = pack(ypass(fl)), pack(ypass(gl))
     rf, rg = torch.empty_like(sf), torch.empty_like(sg)
@@ -103,7 +119,7 @@ def run_herm(rank, world, port, shape, outdir):
     back = torch.empty_like(send_back)
     dist.all_to_all_single(back.view(torch.float64), send_back.view(torch.float64))
     # phase C: fft0padForward along y
-    streams = np.concatenate([back.numpy()[p] for p in range(world)], axis=1)   # [x][3my][z]
+    streams = unpack(back.numpy())                                            # [x][3my][z]
     S = {r: np.moveaxis(streams[:, (r + 1) * my:(r + 2) * my, :], 1, -1) for r in (-1, 0, 1)}
     res = np.moveaxis(implicit.fft0pad_forward(S, my), -1, 1)
     np.save(os.path.join(outdir, f"rank{rank}.npy"), res)
