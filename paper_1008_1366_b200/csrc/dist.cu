@@ -66,7 +66,9 @@ struct Plan {
   long ny, nu;               // y rows of a plane in f (my or 2my-1), in Uy (my or my+1)
   long nxg;                  // global x planes seen by the x pass (mx or 2mx-1)
   long L;                    // rows of each y stream per destination rank (my / P)
-  int streams;               // y residue streams (2 complex, 3 centered)
+  long ce;                   // elements of one stream's part of a peer block (nx * L * mz)
+  long nux;                  // planes of the x pass's extra stream (mx + 1 centered, mx complex)
+  int streams;               // y residue streams (2 complex, 3 centered) = all-to-all chunks
   bool direct;               // TMA y pencils write / read the blocked layout directly
 };
 
@@ -87,7 +89,9 @@ bool make_plan(bool herm, size_t mx, size_t my, size_t mz, int P, Plan* pl) {
   pl->L = (long)(my / P);
   pl->nx = (long)(planes / P);
   pl->nres = pl->streams * pl->L;
-  pl->blk = pl->nx * pl->nres * pl->mz;
+  pl->ce = pl->nx * pl->L * pl->mz;
+  pl->blk = pl->streams * pl->ce;
+  pl->nux = herm ? (long)mx + 1 : (long)mx;
   pl->ny = herm ? 2 * (long)my - 1 : (long)my;
   pl->nu = herm ? (long)my + 1 : (long)my;
   pl->nxg = herm ? 2 * (long)mx - 1 : (long)mx;
@@ -96,14 +100,19 @@ bool make_plan(bool herm, size_t mx, size_t my, size_t mz, int P, Plan* pl) {
   return true;
 }
 
-// per-rank workspace: Uy, Vy (nx*nu*mz each; only for the copying fallback),
-// sendF, sendG, recvF, recvG (P*blk each)
+// per-rank workspace: sendF, sendG, recvF, recvG (P*blk each), the phase-B
+// x-pass scratch Ux, Vx of one chunk (nux*L*mz each), and Uy, Vy (nx*nu*mz
+// each) only for the copying fallback.
+// Send blocks are chunk-major per peer: send[d][s][x_local][l'][z]; the
+// receive buffers are chunk-major overall: recv[s][src][x_local][l'][z], so
+// chunk (stream) s of every source is one contiguous [x][L][mz] array.
+size_t chunk_scratch(const Plan& p) { return (size_t)p.nux * p.L * p.mz; }
 size_t rank_work_elems(const Plan& p) {
-  return (p.direct ? 0 : 2 * (size_t)p.nx * p.nu * p.mz) + 4 * (size_t)p.P * p.blk;
+  return (p.direct ? 0 : 2 * (size_t)p.nx * p.nu * p.mz) + 4 * (size_t)p.P * p.blk + 2 * chunk_scratch(p);
 }
 
 struct RankBufs {
-  double2 *f, *g, *Uy, *Vy, *sendF, *sendG, *recvF, *recvG;
+  double2 *f, *g, *Uy, *Vy, *sendF, *sendG, *recvF, *recvG, *Ux, *Vx;
 };
 
 RankBufs carve(const Plan& p, double2* f, double2* g, double2* work) {
@@ -117,6 +126,8 @@ RankBufs carve(const Plan& p, double2* f, double2* g, double2* work) {
   b.sendG = b.sendF + (size_t)p.P * p.blk;
   b.recvF = b.sendG + (size_t)p.P * p.blk;
   b.recvG = b.recvF + (size_t)p.P * p.blk;
+  b.Ux = b.recvG + (size_t)p.P * p.blk;
+  b.Vx = b.Ux + chunk_scratch(p);
   return b;
 }
 
@@ -151,10 +162,10 @@ cudaError_t copy_stream_rows(const Plan& p, double2* fs, double2* us, double2* b
   }
   double2* sp = (in_u ? us : fs) + row * p.mz;
   const long d = l0 / p.L;
-  double2* bp = blocks + d * p.blk + (st * p.L + l0 % p.L) * p.mz;
+  double2* bp = blocks + d * p.blk + st * p.ce + (l0 % p.L) * p.mz;
   const size_t width = (size_t)cnt * p.mz * sizeof(double2);
   const size_t spitch = (size_t)(in_u ? p.nu : p.ny) * p.mz * sizeof(double2);
-  const size_t bpitch = (size_t)p.nres * p.mz * sizeof(double2);
+  const size_t bpitch = (size_t)p.L * p.mz * sizeof(double2);
   if (dir == 0) return cudaMemcpy2DAsync(bp, bpitch, sp, spitch, width, p.nx, cudaMemcpyDeviceToDevice, s);
   return cudaMemcpy2DAsync(sp, spitch, bp, bpitch, width, p.nx, cudaMemcpyDeviceToDevice, s);
 }
@@ -178,8 +189,9 @@ idc::DistLayout layout(const Plan& p, double2* a, double2* b) {
   dl.base[1] = b;
   dl.L = p.L;
   dl.nblocks = p.P;
-  dl.xstride = p.nres * p.mz;
+  dl.xstride = p.L * p.mz;
   dl.blk = p.blk;
+  dl.soff = p.ce;
   dl.S = p.streams;
   return dl;
 }
@@ -198,22 +210,20 @@ cudaError_t phase_a(const Plan& p, const RankBufs& b, cudaStream_t s) {
   return copy_streams(p, b.g, b.Vy, b.sendG, 0, s);
 }
 
-// phase B: 2D (x, z) convolution of the owned residues; recvF <- result.
-// The received block [x][q'][z] is an (x) x (nres*mz) array for the x pass
-// and (x*nres) rows of mz for the z rows.  The send buffers are free now and
-// serve as the x-pass work arrays (Hermitian: mx+1 planes <= 2mx = P*nx).
-cudaError_t phase_b(const Plan& p, const RankBufs& b, double2* roww, cudaStream_t s) {
-  const long cols = p.nres * p.mz;
+// phase B, one chunk (y-residue stream) of the received data: the 2D (x, z)
+// convolution of its L residues; the chunk [x][L][mz] of recvF <- result.
+cudaError_t phase_b(const Plan& p, const RankBufs& b, int c, double2* roww, cudaStream_t s) {
+  double2* Rf = b.recvF + (size_t)c * p.P * p.ce;
+  double2* Rg = b.recvG + (size_t)c * p.P * p.ce;
+  const long cols = p.L * p.mz;
   if (p.herm) {
-    TRYC(launch_pad0_bwd(b.recvF, b.recvG, b.sendF, b.sendG, (int)p.mx, cols, 1, 0, 0, s));
-    TRYC(idc::launch_hconv_rows_sets(b.recvF, b.recvG, p.nxg * p.nres, b.sendF, b.sendG, (p.mx + 1) * p.nres,
-                                     (int)p.mz, roww, s));
-    return launch_pad0_fwd(b.recvF, b.sendF, (int)p.mx, cols, 1, 0, 0, s);
+    TRYC(launch_pad0_bwd(Rf, Rg, b.Ux, b.Vx, (int)p.mx, cols, 1, 0, 0, s));
+    TRYC(idc::launch_hconv_rows_sets(Rf, Rg, p.nxg * p.L, b.Ux, b.Vx, (p.mx + 1) * p.L, (int)p.mz, roww, s));
+    return launch_pad0_fwd(Rf, b.Ux, (int)p.mx, cols, 1, 0, 0, s);
   }
-  TRYC(launch_pad_bwd(b.recvF, b.recvG, b.sendF, b.sendG, (int)p.mx, cols, 1, 0, 0, s));
-  TRYC(idc::launch_cconv_rows_sets(b.recvF, b.recvG, p.mx * p.nres, b.sendF, b.sendG, p.mx * p.nres, (int)p.mz,
-                                   roww, s));
-  return launch_pad_fwd(b.recvF, b.sendF, (int)p.mx, cols, 1, 0, 0, s);
+  TRYC(launch_pad_bwd(Rf, Rg, b.Ux, b.Vx, (int)p.mx, cols, 1, 0, 0, s));
+  TRYC(idc::launch_cconv_rows_sets(Rf, Rg, p.mx * p.L, b.Ux, b.Vx, p.mx * p.L, (int)p.mz, roww, s));
+  return launch_pad_fwd(Rf, b.Ux, (int)p.mx, cols, 1, 0, 0, s);
 }
 
 // phase C: y-forward from the returned blocks (in sendF): f <- result.
@@ -233,10 +243,60 @@ size_t row_work_bytes(const Plan& p) {
   return p.herm ? idc::hconv_rows_work_bytes((int)p.mz) : idc::cconv_rows_work_bytes((int)p.mz);
 }
 
+// Communicator + the exchange stream: the chunked all-to-alls run on `cs`
+// while phase B runs on the caller's stream, ordered by events.
+constexpr int kMaxChunks = 3;
 struct Comm {
   ncclComm_t nc;
   int nranks, rank;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t a = nullptr, fwd[kMaxChunks] = {}, b[kMaxChunks] = {}, back = nullptr;
+  bool ready() {
+    if (cs) return true;
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return false;
+    bool ok = cudaEventCreateWithFlags(&a, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&back, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; i < kMaxChunks; ++i)
+      ok = ok && cudaEventCreateWithFlags(&fwd[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&b[i], cudaEventDisableTiming) == cudaSuccess;
+    return ok;
+  }
+  void release() {
+    if (!cs) return;
+    cudaStreamDestroy(cs);
+    cudaEventDestroy(a);
+    cudaEventDestroy(back);
+    for (int i = 0; i < kMaxChunks; ++i) {
+      cudaEventDestroy(fwd[i]);
+      cudaEventDestroy(b[i]);
+    }
+    cs = nullptr;
+  }
 };
+
+// one chunk (y-residue stream c) of the exchange with every peer:
+// forward: send[d][c] -> peer d's recv[c][me]; back: recv[c][d] -> peer d's send[me][c]
+ncclResult_t exchange_chunk(const Plan& p, const RankBufs& b, int c, bool fwd, Comm* cm) {
+  const size_t n = (size_t)p.ce * 2;   // doubles
+  ncclResult_t r = ncclGroupStart();
+  for (int d = 0; d < p.P && r == ncclSuccess; ++d) {
+    double2* blk_d_f = b.sendF + (size_t)d * p.blk + (size_t)c * p.ce;
+    double2* rcv_d_f = b.recvF + ((size_t)c * p.P + d) * p.ce;
+    if (fwd) {
+      double2* blk_d_g = b.sendG + (size_t)d * p.blk + (size_t)c * p.ce;
+      double2* rcv_d_g = b.recvG + ((size_t)c * p.P + d) * p.ce;
+      r = ncclSend(blk_d_f, n, ncclDouble, d, cm->nc, cm->cs);
+      if (r == ncclSuccess) r = ncclRecv(rcv_d_f, n, ncclDouble, d, cm->nc, cm->cs);
+      if (r == ncclSuccess) r = ncclSend(blk_d_g, n, ncclDouble, d, cm->nc, cm->cs);
+      if (r == ncclSuccess) r = ncclRecv(rcv_d_g, n, ncclDouble, d, cm->nc, cm->cs);
+    } else {
+      r = ncclSend(rcv_d_f, n, ncclDouble, d, cm->nc, cm->cs);
+      if (r == ncclSuccess) r = ncclRecv(blk_d_f, n, ncclDouble, d, cm->nc, cm->cs);
+    }
+  }
+  const ncclResult_t e = ncclGroupEnd();
+  return r != ncclSuccess ? r : e;
+}
 
 // test hook (idc_dist_force_exchange): run the y-first exchange phases and
 // the NCCL all-to-alls even for a one-rank communicator
@@ -276,6 +336,7 @@ idc_status idc_comm_init(void** comm, int nranks, int rank, const void* nccl_uni
 idc_status idc_comm_destroy(void* comm) {
   if (!comm) return IDC_OK;
   Comm* c = static_cast<Comm*>(comm);
+  c->release();
   ncclResult_t r = ncclCommDestroy(c->nc);
   delete c;
   return r == ncclSuccess ? IDC_OK : IDC_ERR_NCCL;
@@ -338,15 +399,26 @@ static idc_status run_dist(bool herm, void* comm, idc_c128* f, idc_c128* g, size
     return e == cudaSuccess ? IDC_OK : IDC_ERR_CUDA;
   }
   RankBufs b = carve(p, reinterpret_cast<double2*>(f), reinterpret_cast<double2*>(g), reinterpret_cast<double2*>(work));
-  double2* roww = b.recvG + (size_t)p.P * p.blk;
-  if (phase_a(p, b, s) != cudaSuccess) return IDC_ERR_CUDA;
-  const size_t cnt = (size_t)p.blk * 2;  // doubles per peer block
-  if (ncclGroupStart() != ncclSuccess) return IDC_ERR_NCCL;
-  if (ncclAlltoAll(b.sendF, b.recvF, cnt, ncclDouble, c->nc, s) != ncclSuccess) return IDC_ERR_NCCL;
-  if (ncclAlltoAll(b.sendG, b.recvG, cnt, ncclDouble, c->nc, s) != ncclSuccess) return IDC_ERR_NCCL;
-  if (ncclGroupEnd() != ncclSuccess) return IDC_ERR_NCCL;
-  if (phase_b(p, b, roww, s) != cudaSuccess) return IDC_ERR_CUDA;
-  if (ncclAlltoAll(b.recvF, b.sendF, cnt, ncclDouble, c->nc, s) != ncclSuccess) return IDC_ERR_NCCL;
+  double2* roww = b.Vx + chunk_scratch(p);
+  if (!c->ready()) return IDC_ERR_CUDA;
+  // A on s; the forward exchange of every chunk on cs; phase B of chunk k on
+  // s as soon as its exchange is in (overlapping the exchange of chunk k+1)
+  // and its way back on cs; C on s after the last chunk is back
+  if (phase_a(p, b, s) != cudaSuccess || cudaEventRecord(c->a, s) != cudaSuccess ||
+      cudaStreamWaitEvent(c->cs, c->a, 0) != cudaSuccess)
+    return IDC_ERR_CUDA;
+  for (int k = 0; k < p.streams; ++k) {
+    if (exchange_chunk(p, b, k, true, c) != ncclSuccess) return IDC_ERR_NCCL;
+    if (cudaEventRecord(c->fwd[k], c->cs) != cudaSuccess) return IDC_ERR_CUDA;
+  }
+  for (int k = 0; k < p.streams; ++k) {
+    if (cudaStreamWaitEvent(s, c->fwd[k], 0) != cudaSuccess || phase_b(p, b, k, roww, s) != cudaSuccess ||
+        cudaEventRecord(c->b[k], s) != cudaSuccess || cudaStreamWaitEvent(c->cs, c->b[k], 0) != cudaSuccess)
+      return IDC_ERR_CUDA;
+    if (exchange_chunk(p, b, k, false, c) != ncclSuccess) return IDC_ERR_NCCL;
+  }
+  if (cudaEventRecord(c->back, c->cs) != cudaSuccess || cudaStreamWaitEvent(s, c->back, 0) != cudaSuccess)
+    return IDC_ERR_CUDA;
   if (phase_c(p, b, s) != cudaSuccess) return IDC_ERR_CUDA;
   return IDC_OK;
 }
@@ -381,28 +453,34 @@ static idc_status run_emulated(bool herm, int nranks, idc_c128** f_slabs, idc_c1
   for (int r = 0; r < nranks; ++r)
     B[r] = carve(p, reinterpret_cast<double2*>(f_slabs[r]), reinterpret_cast<double2*>(g_slabs[r]),
                  reinterpret_cast<double2*>(static_cast<char*>(work) + per * r));
-  const size_t bytes = (size_t)p.blk * sizeof(double2);
-  auto alltoall = [&](bool fwd) -> cudaError_t {
+  const size_t bytes = (size_t)p.ce * sizeof(double2);
+  // the chunked exchange of run_dist as device copies between the virtual ranks
+  auto exchange = [&](int k, bool fwd) -> cudaError_t {
     for (int dst = 0; dst < nranks; ++dst)
       for (int src = 0; src < nranks; ++src) {
+        double2* sblk = B[src].sendF + (size_t)dst * p.blk + (size_t)k * p.ce;
         if (fwd) {
-          TRYC(cudaMemcpyAsync(B[dst].recvF + (size_t)src * p.blk, B[src].sendF + (size_t)dst * p.blk, bytes,
+          TRYC(cudaMemcpyAsync(B[dst].recvF + ((size_t)k * p.P + src) * p.ce, sblk, bytes,
                                cudaMemcpyDeviceToDevice, s));
-          TRYC(cudaMemcpyAsync(B[dst].recvG + (size_t)src * p.blk, B[src].sendG + (size_t)dst * p.blk, bytes,
+          TRYC(cudaMemcpyAsync(B[dst].recvG + ((size_t)k * p.P + src) * p.ce,
+                               B[src].sendG + (size_t)dst * p.blk + (size_t)k * p.ce, bytes,
                                cudaMemcpyDeviceToDevice, s));
         } else {
-          TRYC(cudaMemcpyAsync(B[dst].sendF + (size_t)src * p.blk, B[src].recvF + (size_t)dst * p.blk, bytes,
-                               cudaMemcpyDeviceToDevice, s));
+          TRYC(cudaMemcpyAsync(B[dst].sendF + (size_t)src * p.blk + (size_t)k * p.ce,
+                               B[src].recvF + ((size_t)k * p.P + dst) * p.ce, bytes, cudaMemcpyDeviceToDevice, s));
         }
       }
     return cudaSuccess;
   };
   for (int r = 0; r < nranks; ++r)
     if (phase_a(p, B[r], s) != cudaSuccess) return IDC_ERR_CUDA;
-  if (alltoall(true) != cudaSuccess) return IDC_ERR_CUDA;
-  for (int r = 0; r < nranks; ++r)
-    if (phase_b(p, B[r], B[r].recvG + (size_t)p.P * p.blk, s) != cudaSuccess) return IDC_ERR_CUDA;
-  if (alltoall(false) != cudaSuccess) return IDC_ERR_CUDA;
+  for (int k = 0; k < p.streams; ++k)
+    if (exchange(k, true) != cudaSuccess) return IDC_ERR_CUDA;
+  for (int k = 0; k < p.streams; ++k) {
+    for (int r = 0; r < nranks; ++r)
+      if (phase_b(p, B[r], k, B[r].Vx + chunk_scratch(p), s) != cudaSuccess) return IDC_ERR_CUDA;
+    if (exchange(k, false) != cudaSuccess) return IDC_ERR_CUDA;
+  }
   for (int r = 0; r < nranks; ++r)
     if (phase_c(p, B[r], s) != cudaSuccess) return IDC_ERR_CUDA;
   return IDC_OK;

@@ -6,12 +6,12 @@ namespace idc {
 
 // Blocked rank-major stream layout of the distributed 3D y passes (dist.cu):
 // stream st (0..S-1) row l of local plane x at
-//   base[input] + (l / L) * blk + x * xstride + (st * L + l % L) * ncols.
+//   base[input] + (l / L) * blk + st * soff + x * xstride + (l % L) * ncols.
 // Passed to the launchers below, the backward pencils write their streams
 // there (instead of in place / U) and the forward pencils read them from there.
 struct DistLayout {
   double2* base[2];
-  long L, nblocks, xstride, blk;
+  long L, nblocks, xstride, blk, soff;
   int S;
 };
 

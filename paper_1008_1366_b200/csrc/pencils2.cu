@@ -129,7 +129,7 @@ __device__ __forceinline__ void tile_store(const double2 (&v)[E], int t, int c, 
 
 // Distributed y passes (dist.cu): the residue streams live in the blocked
 // rank-major layout of the all-to-all buffers -- stream s row l of local
-// plane x at base + (l / L) blk + x (S L ncols) + (s L + l % L) ncols -- so the
+// plane x at base + (l / L) blk + s soff + x xstride + (l % L) ncols -- so the
 // backward pencils store into the send buffer and the forward pencils load
 // from the returned blocks directly (no pack / unpack copies).  One 4D map per
 // (input, stream), boxes of BRd <= L rows.
@@ -708,7 +708,7 @@ bool make_dist_io(DistIO* io, const DistLayout& dl, long ncols, long nx, int W, 
   io->BRd = (int)std::min<long>(BR, dl.L);
   for (int in = 0; in < inputs; ++in)
     for (int st = 0; st < dl.S; ++st)
-      if (!encode_blocked_map(&io->st[in][st], dl.base[in] + (long)st * dl.L * ncols, ncols, dl.L, nx, dl.nblocks,
+      if (!encode_blocked_map(&io->st[in][st], dl.base[in] + (long)st * dl.soff, ncols, dl.L, nx, dl.nblocks,
                               dl.xstride, dl.blk, W, io->BRd))
         return false;
   return true;
