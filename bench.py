@@ -10,14 +10,18 @@ single-GPU configuration of BASELINE.json.  One step = one idc_hconv3d call
 (every row of SURVEY 8(a): the x-pencil fft0pad backward, the per-x-residue
 slab 2D convolutions -- y pencils, z rows -- and the forward passes), inputs
 resident in HBM.  Every other config (C1 cconv1d, C2a hconv1d, C2b tconv1d,
-C3a / C3b cconv2d, C4 hconv2d, C5a cconv3d) is measured the same way and
-reported in ``parts``, each with its own roofline and CPU-oracle baseline.
+C3a / C3b cconv2d, C4 hconv2d, C5a cconv3d) and the two §8(f) NEXT calls at
+the C4 size (c4adv: the 2D Euler advective term, c4t: the 2D ternary
+tconv2d) are measured the same way and reported in ``parts``, each with its
+own roofline, kernel table, host-buffer e2e and CPU-oracle baseline.
 
 Timing: W warm-up calls, then K timed calls, each bracketed by CUDA events on
 the launch stream; before every call (outside the events) the inputs are
 restored from pristine device copies (the call is in place) and a 256 MB
 buffer is written (L2 flush).  The library's per-kernel-class event profiler
-(idc_profile_begin/end) runs during the timed calls and gives each kernel's
+(idc_profile_begin/end) runs over a second pass of the same K calls right
+after the timed loop (its per-launch events serialise the launches and would
+add ~15% to a 0.1 ms call if they ran inside it) and gives each kernel's
 device time, from which the dominant kernel's achieved algorithmic bytes or
 flops per launch are computed (``roofline``).
 
@@ -54,7 +58,7 @@ import synthgen  # noqa: E402  (seeded inputs; no method arithmetic)
 METRIC = "dealiased convolutions/sec (fp64) and achieved HBM GB/s vs B200 peak"
 W = 16  # bytes per complex128 word
 HEADLINE = "c5b"
-DEFAULT_PARTS = "c1,c2a,c2b,c3a,c3b,c4,c5a"
+DEFAULT_PARTS = "c1,c2a,c2b,c3a,c3b,c4,c5a,c4adv,c4t"
 
 
 def peaks():
@@ -405,7 +409,7 @@ def dominant_roofline(kt, pk):
 
 def measure(idc, torch, tdist, name, args, rank, ws, dev, comm=None, want_e2e=False):
     """Time one config: W warm-up calls, K timed calls (restore + L2 flush
-    before each, outside the events), kernel profile over the timed calls."""
+    before each, outside the events), kernel profile over a second pass of K calls."""
     p = dict(CONFIGS[name], name=name)
     dist3d = comm is not None and p["kind"] in ("cconv3d", "hconv3d")
     if dist3d:
@@ -440,7 +444,6 @@ def measure(idc, torch, tdist, name, args, rank, ws, dev, comm=None, want_e2e=Fa
     time.sleep(0.2)
     torch.cuda.synchronize()
     n0 = idc.launch_count()
-    idc.profile_begin()
     t_wall0 = time.perf_counter()
     for k in range(args.steps):
         restore()
@@ -449,11 +452,22 @@ def measure(idc, torch, tdist, name, args, rank, ws, dev, comm=None, want_e2e=Fa
         evs[k][1].record(stream)
     torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall0
-    prof = idc.profile_end()
     launches = idc.launch_count() - n0
+    samples = [e0.elapsed_time(e1) for e0, e1 in evs]
+    # kernel pass: the same K calls again with the library's event profiler
+    # bracketing every launch (kept out of the timed loop: its events
+    # serialise the launches and add ~15% to a 0.1 ms call, profiles/r02/ab/)
+    idc.profile_begin()
+    for k in range(args.steps):
+        restore()
+        evs[k][0].record(stream)
+        run(work)
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    prof = idc.profile_end()
+    prof_step_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / args.steps
     time.sleep(0.2)
     clk.__exit__()
-    samples = [e0.elapsed_time(e1) for e0, e1 in evs]
     tot = torch.tensor([sum(samples)], dtype=torch.float64, device=dev)
     if ws > 1:
         tdist.all_reduce(tot, op=tdist.ReduceOp.MAX)
@@ -465,13 +479,16 @@ def measure(idc, torch, tdist, name, args, rank, ws, dev, comm=None, want_e2e=Fa
     ngpu_peak = ws
     t_b = b * convs / (pk["hbm_gbs"] * 1e9 * ngpu_peak)
     t_f = fl * convs / (pk["fp64_tflops"] * 1e12 * ngpu_peak)
-    kt = kernel_table(p, prof, args.steps, pk, load_traffic(), sec * 1e3)
+    kt = kernel_table(p, prof, args.steps, pk, load_traffic(), prof_step_ms)
     out = dict(config=name, workload=p["desc"], kind=p["kind"], m=p["m"], batch=p["batch"],
                scaling="strong" if dist3d else "weak", ms_per_call=sec * 1e3, call_stats=timing_stats(samples),
                conv_per_s=convs / sec, hbm_gbs_alg=b * convs / sec / 1e9, fp64_tflops_alg=fl * convs / sec / 1e12,
                t_roof_ms=max(t_b, t_f) * 1e3, roofline_frac=max(t_b, t_f) / sec,
                bound="hbm" if t_b >= t_f else "alu", gpu_launches=launches, kernels=kt,
-               roofline=dominant_roofline(kt, pk), clocks=clk.summary(), wall_s_timed_loop=t_wall)
+               roofline=dominant_roofline(kt, pk), clocks=clk.summary(), wall_s_timed_loop=t_wall,
+               kernel_pass={"ms_per_call": prof_step_ms, "steps": args.steps,
+                            "how": "K more calls right after the timed loop, same restore + L2 flush, with "
+                                   "idc_profile_begin/end events around every launch on its stream"})
     del work, flush
     if want_e2e and not dist3d:
         out["e2e"] = run_e2e(args, idc, torch, p, pristine, dev, ws, tdist)
@@ -529,7 +546,7 @@ def run_ours(args):
     parts = []
     for name in parts_names:
         parts.append(measure(idc, torch, tdist, name, args, rank, ws, dev, comm=comm,
-                             want_e2e=(not args.no_e2e and ws == 1 and CONFIGS[name]["kind"].endswith("1d"))))
+                             want_e2e=(not args.no_e2e and ws == 1)))
     head = measure(idc, torch, tdist, args.workload, args, rank, ws, dev, comm=comm, want_e2e=not args.no_e2e)
     if comm is not None:
         comm.close()
@@ -577,6 +594,8 @@ def _oracle_inputs(p):
         return [f[0], g[0]]
     if kind == "hconv2d":
         return list(synthgen.hconv2d_inputs(*p["m"]))
+    if kind == "advection2d":                  # the vorticity w (one array)
+        return [synthgen.hconv2d_inputs(*p["m"], roles=(0,))[0]]
     if kind == "cconv3d":
         return list(synthgen.cconv3d_inputs(*p["m"]))
     if kind == "hconv3d":
@@ -597,7 +616,7 @@ class OracleSampler:
         self.name = name
         self.rs = np.random.default_rng(1008)
         kind = self.p["kind"]
-        if kind.endswith("1d"):
+        if kind.endswith("1d") or kind == "tconv2d":
             self.arrs = None
         else:
             self.arrs = _oracle_inputs(self.p)
@@ -623,10 +642,17 @@ class OracleSampler:
                 if time.perf_counter() > t_end:
                     break
             return done, secs, f"{done} whole rows of {p['batch']} ({kind}, m={p['m']})"
-        f, g = self.arrs
+        if kind == "tconv2d":
+            return self._sample_tconv2d(budget_s)
+        f, g = (self.arrs + [None])[:2]
         npts = 0
         while True:
-            if kind == "cconv2d":
+            if kind == "advection2d":
+                idx = self.rs.choice(f.size, 2, replace=False)
+                t0 = time.perf_counter()
+                from oracle import application
+                application.euler_sum_at(f, idx)
+            elif kind == "cconv2d":
                 idx = self.rs.choice(f.size, 4, replace=False)
                 t0 = time.perf_counter()
                 d.cconv_nd_at(f, g, idx)
@@ -655,10 +681,45 @@ class OracleSampler:
                              f"EXTRAPOLATED to {outputs_per_conv(p)} outputs per convolution")
 
 
+    def _sample_tconv2d(self, budget_s):
+        """One output of the 2D ternary sum costs ~(2m)^4 products (2.8e14 at
+        m = 2048), so not one output of the real size fits the budget: the
+        oracle (ternary2d.direct, two stages of direct 2D convolution) runs
+        whole at mx = my = ms and the time is scaled by the operation count of
+        the two stages, ((2m-1)^2 (2m-1)^2 + (4m-3)^2 (2m-1)^2), to the
+        config's m.  EXTRAPOLATED, and labelled so."""
+        from oracle import ternary2d
+        mx, my = self.p["m"]
+        ms = 16
+
+        def cost(a, b):
+            return (2 * a - 1) ** 2 * (2 * b - 1) ** 2 + (4 * a - 3) * (4 * b - 3) * (2 * a - 1) * (2 * b - 1)
+
+        f, g, h = synthgen.hconv2d_inputs(ms, ms, roles=(0, 1, 2))
+        arrs = [np.concatenate([np.zeros((1, ms), np.complex128), a]) for a in (f, g, h)]
+        t_end = time.perf_counter() + budget_s
+        secs, done = 0.0, 0
+        while True:
+            t0 = time.perf_counter()
+            ternary2d.direct(*arrs)
+            secs += time.perf_counter() - t0
+            done += 1
+            if time.perf_counter() > t_end:
+                break
+        scale = cost(mx, my) / cost(ms, ms)
+        convs = done / scale
+        return convs, secs, (f"{done} whole tconv2d at mx = my = {ms} (ternary2d.direct, scipy direct 2D "
+                             f"convolution, {secs / done * 1e3:.2f} ms each); EXTRAPOLATED to mx = {mx}, my = {my} "
+                             f"by the two stages' product count (x{scale:.3g})")
+
+
 def cpu_baseline(name, budget):
     threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
     s = OracleSampler(name)
     convs, secs, desc = s.sample(budget)
+    if CONFIGS[name]["kind"] in ("advection2d", "tconv2d"):    # numpy / scipy sums, one thread
+        return {"value": convs / secs, "unit": "conv/s", "cores": 1, "kind": "oracle",
+                "sample": desc + " -- oracle/__init__.py (numpy / scipy sums)"}
     return {"value": convs / secs, "unit": "conv/s", "cores": threads, "kind": "oracle",
             "sample": desc + " -- oracle/direct.c (TwoProd + Neumaier / Dot2 compensated, OpenMP)"}
 

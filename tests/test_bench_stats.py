@@ -59,3 +59,17 @@ def test_outputs_per_conv():
     assert bench.outputs_per_conv(bench.CONFIGS["c5b"]) == 1023 * 1023 * 512
     assert bench.outputs_per_conv(bench.CONFIGS["c1"]) == 1024
     assert bench.outputs_per_conv(bench.CONFIGS["c3b"]) == 256 * 256
+
+
+def test_cpu_baseline_every_default_part():
+    """Every config of the default run (except the two 3D ones, whose inputs
+    are several GB) gets a CPU-oracle baseline: the sampler knows its kind."""
+    names = [n for n in bench.DEFAULT_PARTS.split(",") if n not in ("c5a", "c5b")]
+    assert "c4adv" in names and "c4t" in names
+    for n in names:
+        cb = bench.cpu_baseline(n, 0.01)
+        assert cb["value"] > 0 and cb["unit"] == "conv/s" and cb["kind"] == "oracle", (n, cb)
+        if n in ("c4adv", "c4t", "c3a", "c4"):
+            assert "EXTRAPOLATED" in cb["sample"], (n, cb["sample"])
+    for k in ("c5a", "c5b"):
+        assert bench.CONFIGS[k]["kind"] in ("cconv3d", "hconv3d")
