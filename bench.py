@@ -567,7 +567,7 @@ def run_ours(args):
             "call_roofline": {"bound": head["bound"], "frac": head["roofline_frac"], "t_roof_ms": head["t_roof_ms"],
                               "hbm_gbs_alg": head["hbm_gbs_alg"], "fp64_tflops_alg": head["fp64_tflops_alg"]},
             "e2e": head.get("e2e"), "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
-            "call_stats": head["call_stats"], "kernels": head["kernels"],
+            "call_stats": head["call_stats"], "kernels": head["kernels"], "kernel_pass": head["kernel_pass"],
             "wall_s_timed_loop": head["wall_s_timed_loop"], "parts": parts,
         }
         if ws > 1:
