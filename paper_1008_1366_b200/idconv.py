@@ -146,6 +146,12 @@ def _workspace(nbytes: int, device, work, stream=None):
     return w, w.numel()
 
 
+def free_workspaces():
+    """Drop the cached per-stream workspaces (call after the streams' work is
+    complete, e.g. after torch.cuda.synchronize())."""
+    _work_cache.clear()
+
+
 def _stream_ptr(stream, device):
     s = stream if stream is not None else torch.cuda.current_stream(device)
     return ctypes.c_void_p(s.cuda_stream)
@@ -177,7 +183,7 @@ def _need_cuda(arrs):
 HOST_CHUNK_BYTES = int(float(os.environ.get("IDC_HOST_CHUNK_MB", "64")) * (1 << 20))
 
 
-def _run_host_1d(arrs, kind, m, batch, stream):
+def _run_host_1d(arrs, kind, m, batch, stream, out=None):
     """Host tensors of a 1D kind: idc_conv1d_host streams chunks of rows through
     the device (copies of chunk c+1 overlap the kernel of chunk c and the copy
     back of chunk c-1; pinned host memory makes the copies asynchronous)."""
@@ -189,20 +195,32 @@ def _run_host_1d(arrs, kind, m, batch, stream):
     w, wb = _workspace(nb + 256, device, None, stream)
     base = (w.data_ptr() + 255) // 256 * 256
     ins = (ctypes.c_void_p * len(arrs))(*[a.data_ptr() for a in arrs])
-    _check(lib().idc_conv1d_host(kind, ins, ctypes.c_void_p(arrs[0].data_ptr()), m, batch, chunk,
+    dst = arrs[0] if out is None else out
+    _check(lib().idc_conv1d_host(kind, ins, ctypes.c_void_p(dst.data_ptr()), m, batch, chunk,
                                  ctypes.c_void_p(base), nb, _stream_ptr(stream, device)), "idc_conv1d_host")
     if stream is None:                      # host results are complete on return
         torch.cuda.current_stream(device).synchronize()
-    return arrs[0]
+    return dst
 
 
-def _run(arrs, kind, sizes, batch, call, work, stream):
-    """Marshal (possibly host) tensors through one C-ABI call."""
+def _run(arrs, kind, sizes, batch, call, work, stream, out=None):
+    """Marshal (possibly host) tensors through one C-ABI call.  The result
+    goes to f, or to `out` (same shape and device as f) with f left as it
+    was; on the device path g (and h) are scratch either way."""
     on_dev = _prep(arrs)
+    if out is not None:
+        if out.dtype != torch.complex128 or not out.is_contiguous() or out.shape != arrs[0].shape:
+            raise ValueError("out must be a contiguous complex128 tensor of f's shape")
+        if out.device != arrs[0].device:
+            raise ValueError("out must be on f's device")
     if not on_dev and kind in (CCONV1D, HCONV1D, TCONV1D):
-        return _run_host_1d(arrs, kind, sizes[0], batch, stream)
+        return _run_host_1d(arrs, kind, sizes[0], batch, stream, out)
     if on_dev:
         device = arrs[0].device
+        if out is not None:                 # the call runs in place on out
+            with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream(device)):
+                out.copy_(arrs[0])
+            arrs = [out] + list(arrs[1:])
         w, wb = _workspace(workspace_bytes(kind, *sizes, batch=batch), device, work, stream)
         ptrs = [ctypes.c_void_p(a.data_ptr()) for a in arrs]
         _check(call(ptrs, ctypes.c_void_p(w.data_ptr()) if w is not None else None, wb, _stream_ptr(stream, device)),
@@ -219,54 +237,55 @@ def _run(arrs, kind, sizes, batch, call, work, stream):
         ptrs = [ctypes.c_void_p(a.data_ptr()) for a in dev_arrs]
         _check(call(ptrs, ctypes.c_void_p(w.data_ptr()) if w is not None else None, wb, ctypes.c_void_p(s.cuda_stream)),
                "idconv")
-        arrs[0].copy_(dev_arrs[0], non_blocking=True)
+        dst = arrs[0] if out is None else out
+        dst.copy_(dev_arrs[0], non_blocking=True)
         del dev_arrs
     if stream is None:                      # host results are complete on return
         s.synchronize()
-    return arrs[0]
+    return dst
 
 
 # ------------------------------------------------------------------- 1D --
 
-def cconv1d(f, g, work=None, stream=None):
+def cconv1d(f, g, work=None, stream=None, out=None):
     """Function cconv on f, g of shape (..., m); f <- result."""
     m = f.shape[-1]
     B = f.numel() // m
     L = lib()
     return _run([f, g], CCONV1D, (m, 1, 1), B,
-                lambda p, w, wb, s: L.idc_cconv1d(p[0], p[1], m, B, w, wb, s), work, stream)
+                lambda p, w, wb, s: L.idc_cconv1d(p[0], p[1], m, B, w, wb, s), work, stream, out)
 
 
-def hconv1d(f, g, work=None, stream=None):
+def hconv1d(f, g, work=None, stream=None, out=None):
     """Centered Hermitian convolution (Function conv); f <- result."""
     m = f.shape[-1]
     B = f.numel() // m
     L = lib()
     return _run([f, g], HCONV1D, (m, 1, 1), B,
-                lambda p, w, wb, s: L.idc_hconv1d(p[0], p[1], m, B, w, wb, s), work, stream)
+                lambda p, w, wb, s: L.idc_hconv1d(p[0], p[1], m, B, w, wb, s), work, stream, out)
 
 
-def tconv1d(f, g, h, work=None, stream=None):
+def tconv1d(f, g, h, work=None, stream=None, out=None):
     """Centered Hermitian ternary convolution (Function tconv)."""
     m = f.shape[-1]
     B = f.numel() // m
     L = lib()
     return _run([f, g, h], TCONV1D, (m, 1, 1), B,
-                lambda p, w, wb, s: L.idc_tconv1d(p[0], p[1], p[2], m, B, w, wb, s), work, stream)
+                lambda p, w, wb, s: L.idc_tconv1d(p[0], p[1], p[2], m, B, w, wb, s), work, stream, out)
 
 
 # ------------------------------------------------------------------- 2D --
 
-def cconv2d(f, g, work=None, stream=None):
+def cconv2d(f, g, work=None, stream=None, out=None):
     """Function cconv2 on (..., mx, my); f <- result."""
     mx, my = f.shape[-2], f.shape[-1]
     B = f.numel() // (mx * my)
     L = lib()
     return _run([f, g], CCONV2D, (mx, my, 1), B,
-                lambda p, w, wb, s: L.idc_cconv2d(p[0], p[1], mx, my, B, w, wb, s), work, stream)
+                lambda p, w, wb, s: L.idc_cconv2d(p[0], p[1], mx, my, B, w, wb, s), work, stream, out)
 
 
-def tconv2d(f, g, h, work=None, stream=None):
+def tconv2d(f, g, h, work=None, stream=None, out=None):
     """Function tconv2 on (2mx, my) arrays (row 0 = kx -mx, read as
     zero); f rows 1..2mx-1 <- the centered Hermitian ternary convolution."""
     nx, my = f.shape[-2], f.shape[-1]
@@ -275,10 +294,10 @@ def tconv2d(f, g, h, work=None, stream=None):
     mx = nx // 2
     L = lib()
     return _run([f, g, h], TCONV2D, (mx, my, 1), 1,
-                lambda p, w, wb, s: L.idc_tconv2d(p[0], p[1], p[2], mx, my, w, wb, s), work, stream)
+                lambda p, w, wb, s: L.idc_tconv2d(p[0], p[1], p[2], mx, my, w, wb, s), work, stream, out)
 
 
-def hconv2d(f, g, work=None, stream=None):
+def hconv2d(f, g, work=None, stream=None, out=None):
     """Function conv2 on (2mx-1, my); f <- result."""
     nx, my = f.shape[-2], f.shape[-1]
     if nx % 2 == 0 or f.dim() != 2:
@@ -286,22 +305,22 @@ def hconv2d(f, g, work=None, stream=None):
     mx = (nx + 1) // 2
     L = lib()
     return _run([f, g], HCONV2D, (mx, my, 1), 1,
-                lambda p, w, wb, s: L.idc_hconv2d(p[0], p[1], mx, my, w, wb, s), work, stream)
+                lambda p, w, wb, s: L.idc_hconv2d(p[0], p[1], mx, my, w, wb, s), work, stream, out)
 
 
 # ------------------------------------------------------------------- 3D --
 
-def cconv3d(f, g, work=None, stream=None):
+def cconv3d(f, g, work=None, stream=None, out=None):
     """Function cconv3 on (mx, my, mz); f <- result."""
     if f.dim() != 3:
         raise ValueError(f"cconv3d takes one (mx, my, mz) array pair, got shape {tuple(f.shape)}")
     mx, my, mz = f.shape
     L = lib()
     return _run([f, g], CCONV3D, (mx, my, mz), 1,
-                lambda p, w, wb, s: L.idc_cconv3d(p[0], p[1], mx, my, mz, w, wb, s), work, stream)
+                lambda p, w, wb, s: L.idc_cconv3d(p[0], p[1], mx, my, mz, w, wb, s), work, stream, out)
 
 
-def hconv3d(f, g, work=None, stream=None):
+def hconv3d(f, g, work=None, stream=None, out=None):
     """Centered Hermitian 3D (AMB-9) on (2mx-1, 2my-1, mz)."""
     nx, ny, mz = f.shape[-3:]
     if nx % 2 == 0 or ny % 2 == 0 or f.dim() != 3:
@@ -309,7 +328,7 @@ def hconv3d(f, g, work=None, stream=None):
     mx, my = (nx + 1) // 2, (ny + 1) // 2
     L = lib()
     return _run([f, g], HCONV3D, (mx, my, mz), 1,
-                lambda p, w, wb, s: L.idc_hconv3d(p[0], p[1], mx, my, mz, w, wb, s), work, stream)
+                lambda p, w, wb, s: L.idc_hconv3d(p[0], p[1], mx, my, mz, w, wb, s), work, stream, out)
 
 
 # --------------------------------------------------------- synthetic data --
