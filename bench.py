@@ -828,7 +828,7 @@ def main(argv=None):
     ap.add_argument("--parts", default=DEFAULT_PARTS, help="comma-separated configs measured besides the headline")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle CPU work (headline)")
     ap.add_argument("--cpu-budget-part", type=float, default=3.0, help="seconds of oracle CPU work per part")
-    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dry-run", action="store_true", help="spawn/rendezvous check only (no GPU)")
