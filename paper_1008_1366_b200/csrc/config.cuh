@@ -33,6 +33,8 @@
 // | IDC_K7_TMA_STORE        | 1       | K7 residue tiles leave through the exchange buffer by TMA stores        |
 // | IDC_K7_KEEP_RAW         | 1       | K7 reads U_k, U_{k-m} once into registers; next tile loaded at once     |
 // | IDC_K8_TMA_STORE        | 2       | K8: both output halves by TMA stores (1: U_k only, 0: per thread)      |
+// | IDC_PENCIL_WAIT_IN_FFT  | 1       | K7/K8 wait for the previous TMA store's read of xb after the first     |
+// |                         |         | radix pass of the next FFT (0: before the FFT)                          |
 #pragma once
 
 #ifndef IDC_V2_MAX_M
@@ -118,4 +120,7 @@
 #endif
 #ifndef IDC_K8_TMA_STORE
 #define IDC_K8_TMA_STORE 2
+#endif
+#ifndef IDC_PENCIL_WAIT_IN_FFT
+#define IDC_PENCIL_WAIT_IN_FFT 1
 #endif

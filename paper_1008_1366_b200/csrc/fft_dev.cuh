@@ -395,18 +395,28 @@ __device__ __forceinline__ void pass_exchange(double2 (&v)[E], int t, double2* _
   sync();
 }
 
-template <int N, int E, int NS, int SIGN, class Sync, class XS>
+struct NoPre {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// `pre` runs once, after the first pass's arithmetic and before the first
+// write to xb: a caller whose earlier TMA store still reads xb waits there,
+// so the wait overlaps the first radix pass instead of preceding the FFT.
+template <int N, int E, int NS, int SIGN, class Sync, class XS, class Pre = NoPre>
 __device__ __forceinline__ void fft_passes(double2 (&v)[E], int t, double2* __restrict__ xb,
                                            const double2* __restrict__ tw, Sync sync, XS xs,
-                                           const PassTw<N, E, pass_radix(N, E, NS), NS>& pt) {
+                                           const PassTw<N, E, pass_radix(N, E, NS), NS>& pt, Pre pre = Pre{}) {
   if constexpr (NS < N) {
     constexpr int R = pass_radix(N, E, NS);
     pass_compute<N, E, R, NS, SIGN>(v, pt);
+    if constexpr (NS == 1) pre();
     if constexpr (NS * R < N) {
       const auto next = load_pass_tw<N, E, pass_radix(N, E, NS * R), NS * R>(t, tw);   // ahead of the exchange
       pass_exchange<N, E, R, NS>(v, t, xb, sync, xs);
       fft_passes<N, E, NS * R, SIGN>(v, t, xb, tw, sync, xs, next);
     }
+  } else {
+    pre();
   }
 }
 
@@ -417,9 +427,9 @@ struct IdentitySlot {
 // Unnormalised N-point FFT of the group's vector, sign SIGN (+1 = backward,
 // P:185-186; -1 = forward).  All threads of the group (and, with a CTA-wide
 // barrier, of the CTA) must call it together.
-template <int N, int E, int SIGN, class Sync, class XS = IdentitySlot>
+template <int N, int E, int SIGN, class Sync, class XS = IdentitySlot, class Pre = NoPre>
 __device__ __forceinline__ void fft(double2 (&v)[E], int t, double2* __restrict__ xb,
-                                    const double2* __restrict__ tw, Sync sync, XS xs = XS{}) {
+                                    const double2* __restrict__ tw, Sync sync, XS xs = XS{}, Pre pre = Pre{}) {
   static_assert(N % E == 0 && (E & (E - 1)) == 0 && (N & (N - 1)) == 0, "power-of-two sizes");
   // Launder the thread index so that the (thread-invariant) exchange and
   // twiddle addresses are recomputed per transform instead of being hoisted
@@ -427,7 +437,7 @@ __device__ __forceinline__ void fft(double2 (&v)[E], int t, double2* __restrict_
   int tl;
   asm volatile("mov.b32 %0, %1;" : "=r"(tl) : "r"(t));
   count_fft(ilog2(N), tl, 1);
-  fft_passes<N, E, 1, SIGN>(v, tl, xb, tw, sync, xs, PassTw<N, E, pass_radix(N, E, 1), 1>{});
+  fft_passes<N, E, 1, SIGN>(v, tl, xb, tw, sync, xs, PassTw<N, E, pass_radix(N, E, 1), 1>{}, pre);
 }
 
 // Two independent N-point FFTs (same sign) in lockstep: each pass computes

@@ -477,9 +477,18 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
         }
       }
 #if IDC_K7_TMA_STORE
-      if (threadIdx.x == 0) bulk_wait_read();       // the previous residue's stores have read xb
-      __syncthreads();
-      fft<N, E, +1>(v, t, xb, twN, CtaSync{}, xs);  // ends with a barrier after its last exchange
+      // the previous residue's stores must have read xb before the first
+      // exchange writes it: waited for after the first radix pass
+      auto drained = [] {
+        if (threadIdx.x == 0) bulk_wait_read();
+        __syncthreads();
+      };
+      if constexpr (IDC_PENCIL_WAIT_IN_FFT) {
+        fft<N, E, +1>(v, t, xb, twN, CtaSync{}, xs, drained);   // ends with a barrier after its last exchange
+      } else {
+        drained();
+        fft<N, E, +1>(v, t, xb, twN, CtaSync{}, xs);
+      }
 #pragma unroll
       for (int i = 0; i < E; ++i) xb[(t + T * i) * W + c] = v[i];
       if constexpr (DIST) {                         // stream r = (r+1)-th map of the send blocks, m rows
@@ -602,7 +611,7 @@ k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
         v[i] = (!DIST && q == 1 && l == N - 1) ? tail[b][c] : st[b][l * W + c];
       }
 #if IDC_K8_TMA_STORE
-      if (q == 0 && threadIdx.x == 0) bulk_wait_read();   // last tile's output stores have read xb
+      if (!IDC_PENCIL_WAIT_IN_FFT && q == 0 && threadIdx.x == 0) bulk_wait_read();   // last tile's stores have read xb
 #endif
       __syncthreads();
       if (threadIdx.x == 0) {  // refill this buffer with the stream two steps ahead
@@ -611,7 +620,16 @@ k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
         else if (tau + gridDim.x < tl.ntiles) issue(tau + gridDim.x, q2 - 3, b);
       }
       b ^= 1;
-      fft<N, E, -1>(v, t, xb, twN, CtaSync{}, xs);
+      if (IDC_K8_TMA_STORE && IDC_PENCIL_WAIT_IN_FFT && q == 0) {
+        // the last tile's output stores must have read xb before the first
+        // exchange writes it: waited for after the first radix pass
+        fft<N, E, -1>(v, t, xb, twN, CtaSync{}, xs, [] {
+          if (threadIdx.x == 0) bulk_wait_read();
+          __syncthreads();
+        });
+      } else {
+        fft<N, E, -1>(v, t, xb, twN, CtaSync{}, xs);
+      }
       // 3m U_k = sum_r zeta_{3m}^{-rk} S_r(k); 3m U_{k-m} = sum_r zeta_{3m}^{-rk} zeta_3^{r} S_r(k)
       const double2 z3 = make_double2(r == 0 ? 1.0 : -0.5, r == 0 ? 0.0 : (r > 0 ? s3 : -s3));  // zeta_3^{r}
       auto acc = [&](int i, double2 zr) {                                 // zr = zeta_{3m}^{-rk}
