@@ -480,12 +480,20 @@ def measure(idc, torch, tdist, name, args, rank, ws, dev, comm=None, want_e2e=Fa
     t_b = b * convs / (pk["hbm_gbs"] * 1e9 * ngpu_peak)
     t_f = fl * convs / (pk["fp64_tflops"] * 1e12 * ngpu_peak)
     kt = kernel_table(p, prof, args.steps, pk, load_traffic(), prof_step_ms)
+    # SURVEY 8(d) d.3 "measured" HBM GB/s: ncu DRAM bytes per unit of every
+    # kernel class (profiles/traffic.json, one --set full capture each) x the
+    # units of one call, over the call time
+    dram_call = None
+    if kt and all(k.get("traffic_per_launch") for k in kt):
+        dram_call = sum(k["traffic_per_launch"] * k["launches_per_call"] for k in kt)
     out = dict(config=name, workload=p["desc"], kind=p["kind"], m=p["m"], batch=p["batch"],
                scaling="strong" if dist3d else "weak", ms_per_call=sec * 1e3, call_stats=timing_stats(samples),
                conv_per_s=convs / sec, hbm_gbs_alg=b * convs / sec / 1e9, fp64_tflops_alg=fl * convs / sec / 1e12,
                t_roof_ms=max(t_b, t_f) * 1e3, roofline_frac=max(t_b, t_f) / sec,
                bound="hbm" if t_b >= t_f else "alu", gpu_launches=launches, kernels=kt,
                roofline=dominant_roofline(kt, pk), clocks=clk.summary(), wall_s_timed_loop=t_wall,
+               dram_bytes_per_call_ncu=dram_call,
+               hbm_gbs_measured=(dram_call * ws / sec / 1e9) if dram_call else None,   # all ranks
                kernel_pass={"ms_per_call": prof_step_ms, "steps": args.steps,
                             "how": "K more calls right after the timed loop, same restore + L2 flush, with "
                                    "idc_profile_begin/end events around every launch on its stream"})
@@ -597,7 +605,9 @@ def run_ours(args):
                        "seed": synthgen.SEED},
             "roofline": head["roofline"],
             "call_roofline": {"bound": head["bound"], "frac": head["roofline_frac"], "t_roof_ms": head["t_roof_ms"],
-                              "hbm_gbs_alg": head["hbm_gbs_alg"], "fp64_tflops_alg": head["fp64_tflops_alg"]},
+                              "hbm_gbs_alg": head["hbm_gbs_alg"], "fp64_tflops_alg": head["fp64_tflops_alg"],
+                              "dram_bytes_per_call_ncu": head["dram_bytes_per_call_ncu"],
+                              "hbm_gbs_measured": head["hbm_gbs_measured"]},
             "e2e": head.get("e2e"), "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
             "call_stats": head["call_stats"], "kernels": head["kernels"], "kernel_pass": head["kernel_pass"],
             "wall_s_timed_loop": head["wall_s_timed_loop"], "parts": parts,

@@ -50,6 +50,20 @@ def test_library_is_sm100a_only():
     assert "sm_90" not in out and "sm_80" not in out
 
 
+def test_sass_no_tensor_core_ops_and_tma_present():
+    """the path is not a dense contraction, so no
+    tensor-core instruction (HMMA / DMMA / IMMA / UTC*MMA) may appear in the
+    library; the pencil and row kernels move tiles with TMA (UTMALDG /
+    UTMASTG tensor copies, UBLKCP bulk copies)."""
+    import collections
+    import re
+    sass = os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {idconv.LIB_PATH} 2>&1").read()
+    ops = collections.Counter(re.findall(r"\b(HMMA|DMMA|IMMA|UTCHMMA|UTCQMMA|UTCIMMA|UTCMMA|UTMALDG|UTMASTG|UBLKCP)\b", sass))
+    assert sum(ops[k] for k in ("HMMA", "DMMA", "IMMA", "UTCHMMA", "UTCQMMA", "UTCIMMA", "UTCMMA")) == 0, ops
+    assert ops["UTMALDG"] > 0 and ops["UTMASTG"] > 0 and ops["UBLKCP"] > 0, ops
+    assert len(re.findall(r"\bDFMA\b", sass)) > 1000
+
+
 def _fake(addr):
     return ctypes.c_void_p(addr)
 
