@@ -466,6 +466,18 @@ def measure(idc, torch, tdist, name, args, rank, ws, dev, comm=None, want_e2e=Fa
     torch.cuda.synchronize()
     prof = idc.profile_end()
     prof_step_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / args.steps
+    # the distributed path's NCCL exchanges (spans on the communicator's
+    # stream, "A2A"): reported beside the kernels, not among them
+    a2a = [r for r in prof if r["tag"] == "A2A"]
+    prof = [r for r in prof if r["tag"] != "A2A"]
+    a2a_rec = None
+    if a2a:
+        ms_a = sum(r["ms"] for r in a2a) / args.steps
+        by = sum(r["units"] for r in a2a) / args.steps
+        a2a_rec = {"ms_per_call": ms_a, "exchanges_per_call": sum(r["launches"] for r in a2a) / args.steps,
+                   "bytes_sent_per_call": by, "gbs_per_rank": by / (ms_a / 1e3) / 1e9 if ms_a > 0 else None,
+                   "how": "CUDA events around each grouped ncclSend/ncclRecv chunk on the communicator's stream "
+                          "(overlapping phase B), this rank"}
     time.sleep(0.2)
     clk.__exit__()
     tot = torch.tensor([sum(samples)], dtype=torch.float64, device=dev)
@@ -492,7 +504,7 @@ def measure(idc, torch, tdist, name, args, rank, ws, dev, comm=None, want_e2e=Fa
                t_roof_ms=max(t_b, t_f) * 1e3, roofline_frac=max(t_b, t_f) / sec,
                bound="hbm" if t_b >= t_f else "alu", gpu_launches=launches, kernels=kt,
                roofline=dominant_roofline(kt, pk), clocks=clk.summary(), wall_s_timed_loop=t_wall,
-               dram_bytes_per_call_ncu=dram_call,
+               dram_bytes_per_call_ncu=dram_call, all_to_all=a2a_rec,
                hbm_gbs_measured=(dram_call * ws / sec / 1e9) if dram_call else None,   # all ranks
                kernel_pass={"ms_per_call": prof_step_ms, "steps": args.steps,
                             "how": "K more calls right after the timed loop, same restore + L2 flush, with "
@@ -610,6 +622,7 @@ def run_ours(args):
                               "hbm_gbs_measured": head["hbm_gbs_measured"]},
             "e2e": head.get("e2e"), "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
             "call_stats": head["call_stats"], "kernels": head["kernels"], "kernel_pass": head["kernel_pass"],
+            "all_to_all": head["all_to_all"],
             "wall_s_timed_loop": head["wall_s_timed_loop"], "parts": parts,
         }
         if ws > 1:

@@ -47,6 +47,7 @@
 #include "../../include/idconv.h"
 #include "config.cuh"
 #include "kernels.cuh"
+#include "launch.cuh"
 #include "nd.cuh"
 #include "nd_internal.cuh"
 
@@ -278,6 +279,9 @@ struct Comm {
 // forward: send[d][c] -> peer d's recv[c][me]; back: recv[c][d] -> peer d's send[me][c]
 ncclResult_t exchange_chunk(const Plan& p, const RankBufs& b, int c, bool fwd, Comm* cm) {
   const size_t n = (size_t)p.ce * 2;   // doubles
+  // profiled as "A2A" (n = ranks, units = bytes this rank sends)
+  Span sp = span_begin(cm->cs);
+  const LaunchTag tag{"A2A", p.P, (long)((fwd ? 2 : 1) * (size_t)p.P * n * sizeof(double))};
   ncclResult_t r = ncclGroupStart();
   for (int d = 0; d < p.P && r == ncclSuccess; ++d) {
     double2* blk_d_f = b.sendF + (size_t)d * p.blk + (size_t)c * p.ce;
@@ -295,6 +299,7 @@ ncclResult_t exchange_chunk(const Plan& p, const RankBufs& b, int c, bool fwd, C
     }
   }
   const ncclResult_t e = ncclGroupEnd();
+  span_end(sp, cm->cs, tag);
   return r != ncclSuccess ? r : e;
 }
 

@@ -69,6 +69,24 @@ cudaError_t launch_kernel(const void* fn, dim3 grid, dim3 block, void** args, si
   return e;
 }
 
+Span span_begin(cudaStream_t s) {
+  Span sp;
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_on) return sp;
+  sp.a = get_event();
+  cudaEventRecord(sp.a, s);
+  return sp;
+}
+
+void span_end(Span& sp, cudaStream_t s, const LaunchTag& tag) {
+  if (!sp.a) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaEvent_t b = get_event();
+  cudaEventRecord(b, s);
+  g_recs.push_back(Rec{tag.tag, tag.n, tag.units, sp.a, b});
+  sp.a = nullptr;
+}
+
 }  // namespace idc
 
 extern "C" {

@@ -22,4 +22,14 @@ struct LaunchTag {
 cudaError_t launch_kernel(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s,
                           const LaunchTag& tag);
 
+// A profiled span of stream work that is not one of our kernel launches (the
+// distributed path's NCCL exchanges): with the profiler on, span_begin
+// records an event on s and span_end a second one, filed under `tag` (units =
+// bytes sent by this rank); with it off both are no-ops.
+struct Span {
+  cudaEvent_t a = nullptr;
+};
+Span span_begin(cudaStream_t s);
+void span_end(Span& sp, cudaStream_t s, const LaunchTag& tag);
+
 }  // namespace idc
