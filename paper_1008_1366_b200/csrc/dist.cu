@@ -280,8 +280,8 @@ struct Comm {
 ncclResult_t exchange_chunk(const Plan& p, const RankBufs& b, int c, bool fwd, Comm* cm) {
   const size_t n = (size_t)p.ce * 2;   // doubles
   // profiled as "A2A" (n = ranks, units = bytes this rank sends)
-  Span sp = span_begin(cm->cs);
-  const LaunchTag tag{"A2A", p.P, (long)((fwd ? 2 : 1) * (size_t)p.P * n * sizeof(double))};
+  idc::Span sp = idc::span_begin(cm->cs);
+  const idc::LaunchTag tag{"A2A", p.P, (long)((fwd ? 2 : 1) * (size_t)p.P * n * sizeof(double))};
   ncclResult_t r = ncclGroupStart();
   for (int d = 0; d < p.P && r == ncclSuccess; ++d) {
     double2* blk_d_f = b.sendF + (size_t)d * p.blk + (size_t)c * p.ce;
@@ -299,7 +299,7 @@ ncclResult_t exchange_chunk(const Plan& p, const RankBufs& b, int c, bool fwd, C
     }
   }
   const ncclResult_t e = ncclGroupEnd();
-  span_end(sp, cm->cs, tag);
+  idc::span_end(sp, cm->cs, tag);
   return r != ncclSuccess ? r : e;
 }
 

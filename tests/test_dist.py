@@ -169,3 +169,37 @@ def test_hermitian_nccl_single_rank_gpu(exchange):
     finally:
         idconv.lib().idc_dist_force_exchange(0)
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_exchange_spans_profiled_gpu():
+    """The profiler files the NCCL exchanges of the forced P = 1 exchange path
+    as "A2A" spans: 3 chunks there and 3 back for hconv3d (one per y stream),
+    bytes = what this rank sends."""
+    import torch
+    import torch.distributed as dist
+    from paper_1008_1366_b200 import idconv
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = "29741"
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = idconv.Comm()
+        idconv.lib().idc_dist_force_exchange(1)
+        shape = (8, 64, 16)
+        f, g = synthgen.hconv3d_inputs(*shape)
+        F, G = [torch.from_numpy(a).cuda() for a in _herm_slabs(f, 1)], [torch.from_numpy(a).cuda() for a in _herm_slabs(g, 1)]
+        idconv.profile_begin()
+        idconv.hconv3d_dist(comm, F[0], G[0], *shape)
+        prof = idconv.profile_end()
+        torch.cuda.synchronize()
+        a2a = [r for r in prof if r["tag"] == "A2A"]
+        assert len(a2a) == 1 and a2a[0]["n"] == 1 and a2a[0]["launches"] == 6, prof
+        plan = idconv.dist_plan(*shape, 1, 0, kind=idconv.HCONV3D)
+        words = plan["nx"] * plan["nres"] * shape[2]            # one rank's residues x its planes x mz
+        assert a2a[0]["units"] == 16 * words * 3, (a2a, plan)   # both inputs there, one array back
+        assert any(r["tag"] in ("K7", "K7s") for r in prof)
+        assert rel_l2(F[0].cpu().numpy()[:-1], direct.hconv3d(f, g)) < 1e-14
+        comm.close()
+    finally:
+        idconv.lib().idc_dist_force_exchange(0)
+        dist.destroy_process_group()
