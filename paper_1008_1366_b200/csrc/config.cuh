@@ -7,6 +7,7 @@
 //
 // | knob                    | default | what it selects                                                        |
 // |-------------------------|---------|------------------------------------------------------------------------|
+// | IDC_FOLD_TW             | 1       | Stockham pass twiddles folded into FMA-form DIT butterflies (fft_dev.cuh) |
 // | IDC_V2_MAX_M            | 4096    | rows up to this m run the rows2.cu kernels (K2/K3/K4 register-resident) |
 // | IDC_V3_MIN_M            | 512     | hconv / tconv rows from this m run the TMA-staged rows3.cu K3/K4        |
 // | IDC_ROWS_E              | 16      | rows2.cu elements per thread for m >= 1024                             |
@@ -36,6 +37,10 @@
 // | IDC_PENCIL_WAIT_IN_FFT  | 1       | K7/K8 wait for the previous TMA store's read of xb after the first     |
 // |                         |         | radix pass of the next FFT (0: before the FFT)                          |
 #pragma once
+
+#ifndef IDC_FOLD_TW
+#define IDC_FOLD_TW 1
+#endif
 
 #ifndef IDC_V2_MAX_M
 #define IDC_V2_MAX_M 4096

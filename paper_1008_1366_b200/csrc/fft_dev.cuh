@@ -26,6 +26,8 @@
 // no arithmetic.
 #pragma once
 #include <cuda_runtime.h>
+
+#include "config.cuh"
 #include <type_traits>
 #include <utility>
 
@@ -303,13 +305,18 @@ __host__ __device__ constexpr int xbuf_elems() { return N <= E ? 0 : N + N / E; 
 // butterfly -- measured 6-12% slower: more L1 wavefronts)
 __host__ __device__ constexpr int pass_q(int R) { return R >= 16 ? 4 : (R >= 4 ? 2 : 1); }
 __host__ __device__ constexpr int pass_radix(int N, int E, int NS) { return (NS * E <= N) ? E : N / NS; }
+// Table rows per pass of radix R: folded (IDC_FOLD_TW, below) w^{2^l}, l < log2 R;
+// otherwise w^c (c < Q) and w^{Qa} (a < R/Q).
+__host__ __device__ constexpr int pass_rows(int R) {
+  return IDC_FOLD_TW ? ilog2(R) : (pass_q(R) - 1 + R / pass_q(R) - 1);
+}
 template <int N, int E>
 __host__ __device__ constexpr int pass_tab_offset(int ns_target) {
   int off = 0;
   for (int NS = 1; NS < N;) {
     const int R = pass_radix(N, E, NS);
     if (NS == ns_target) return off;
-    if (NS > 1) off += (pass_q(R) - 1 + R / pass_q(R) - 1) * NS;
+    if (NS > 1) off += pass_rows(R) * NS;
     NS *= R;
   }
   return off;
@@ -322,25 +329,90 @@ __host__ __device__ constexpr int pass_tab_offset(int ns_target) {
 // so the load latency is hidden behind the barriers.
 template <int N, int E, int R, int NS>
 struct PassTw {
-  static constexpr int B = E / R, Q = pass_q(R);
+  static constexpr int B = E / R, Q = pass_q(R), LR = ilog2(R) > 0 ? ilog2(R) : 1;
+#if IDC_FOLD_TW
+  double2 p[B][LR];      // w^{2^l}
+#else
   double2 lo[B][Q], hi[B][R / Q];
+#endif
 };
 template <int N, int E, int R, int NS>
 __device__ __forceinline__ PassTw<N, E, R, NS> load_pass_tw(int t, const double2* __restrict__ tw) {
   PassTw<N, E, R, NS> p;
   if constexpr (NS > 1) {
-    constexpr int T = N / E, B = E / R, Q = pass_q(R);
+    constexpr int T = N / E, B = E / R;
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const int jm = (t + T * b) & (NS - 1);
       const double2* tp = tw + pass_tab_offset<N, E>(NS) + jm;
+#if IDC_FOLD_TW
+#pragma unroll
+      for (int l = 0; l < ilog2(R); ++l) p.p[b][l] = ldtw_pass(&tp[l * NS]);
+#else
+      constexpr int Q = pass_q(R);
 #pragma unroll
       for (int c = 1; c < Q; ++c) p.lo[b][c] = ldtw_pass(&tp[(c - 1) * NS]);
 #pragma unroll
       for (int a = 1; a < R / Q; ++a) p.hi[b][a] = ldtw_pass(&tp[(Q - 2 + a) * NS]);
+#endif
     }
   }
   return p;
+}
+
+// ------------------------------------- twiddled DFT_R with folded twiddles --
+// X_k = sum_r x_r w^r omega_R^{rk} (omega_R = exp(SIGN 2 pi i / R)) as an
+// in-register radix-2 decimation in time whose butterflies absorb the pass
+// twiddle: with E_k, O_k the same problem over the even / odd r with base
+// w^2, X_k = E_k + (w omega_R^k) O_k and X_{k+R/2} = E_k - (w omega_R^k) O_k.
+// Level L (sub-DFTs of size L) has base u_L = w^{R/L}; its butterflies
+// a +- t b (t = u_L omega_L^k) cost 6 fp64 instructions in FMA form
+// (y0 = a + t b by two FMAs per component, y1 = 2a - y0 by one), against 8
+// for a separate complex multiply and two complex adds.  Per 16 points of a
+// radix-16 pass: 32 butterflies (192) + 14 for the t_k = u omega^k, against
+// 24 twiddle multiplies (96) + 168 in DFT16 with the table scheme below.
+// wp[l] = w^{2^l} from the pass table (direction +1; conjugated for SIGN < 0).
+__device__ __forceinline__ void bfly_fma(double2& a, double2& b, double2 t) {
+  const double2 y0 = make_double2(fma(t.x, b.x, fma(-t.y, b.y, a.x)), fma(t.x, b.y, fma(t.y, b.x, a.y)));
+  b = make_double2(fma(2.0, a.x, -y0.x), fma(2.0, a.y, -y0.y));
+  a = y0;
+}
+template <int R, int L, int SIGN>
+__device__ __forceinline__ void dit_level(double2 (&y)[R], double2 u) {
+  // t_k = u omega_L^k for k < L/2, t_{k + L/4} = (SIGN i) t_k; one t live at a time
+  static_for<(L >= 4 ? L / 4 : 1)>([&](auto K) {
+    constexpr int k = decltype(K)::value;
+    const double2 t = twc<k, L, SIGN>(u);
+    static_for<R / L>([&](auto Gi) {
+      constexpr int g = decltype(Gi)::value;
+      bfly_fma(y[g * L + k], y[g * L + k + L / 2], t);
+    });
+    if constexpr (L >= 4) {
+      const double2 ti = twc<1, 4, SIGN>(t);
+      static_for<R / L>([&](auto Gi) {
+        constexpr int g = decltype(Gi)::value;
+        bfly_fma(y[g * L + k + L / 4], y[g * L + k + L / 4 + L / 2], ti);
+      });
+    }
+  });
+}
+template <int R, int SIGN, int L = 2>
+__device__ __forceinline__ void dit_levels(double2 (&y)[R], const double2* wp) {
+  if constexpr (L <= R) {
+    double2 u = wp[ilog2(R / L)];                   // w^{R/L}
+    if constexpr (SIGN < 0) u.y = -u.y;
+    dit_level<R, L, SIGN>(y, u);
+    dit_levels<R, SIGN, 2 * L>(y, wp);
+  }
+}
+template <int R, int SIGN>
+__device__ __forceinline__ void dft_tw(double2 (&x)[R], const double2* wp) {
+  double2 y[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) y[k] = x[brev(k, ilog2(R))];
+  dit_levels<R, SIGN>(y, wp);
+#pragma unroll
+  for (int k = 0; k < R; ++k) x[k] = y[k];
 }
 
 // One Stockham radix-R pass with preloaded twiddles; data stays in registers.
@@ -352,6 +424,13 @@ __device__ __forceinline__ void pass_compute(double2 (&v)[E], const PassTw<N, E,
     double2 x[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r] = v[b + r * B];
+#if IDC_FOLD_TW
+    if constexpr (NS > 1) {
+      dft_tw<R, SIGN>(x, pt.p[b]);
+    } else {
+      dft<R, SIGN>(x);
+    }
+#else
     if constexpr (NS > 1) {
       // x[Qa + c] * w^c * w^{Qa}: two multiplies per element instead of
       // forming every w^r = w^{Qa} w^c first (same multiply count, but no
@@ -365,6 +444,7 @@ __device__ __forceinline__ void pass_compute(double2 (&v)[E], const PassTw<N, E,
       }
     }
     dft<R, SIGN>(x);
+#endif
 #pragma unroll
     for (int r = 0; r < R; ++r) v[b + r * B] = x[r];
   }

@@ -106,8 +106,13 @@ const double2* pass_table(int N, int E) {
           h.push_back(make_double2(c, s));
         }
       };
+#if IDC_FOLD_TW
+      (void)Q;
+      for (int l = 0; (1 << l) < R; ++l) put(1L << l);
+#else
       for (int c = 1; c < Q; ++c) put(c);
       for (int a = 1; a < R / Q; ++a) put((long)Q * a);
+#endif
     }
     NS *= R;
   }
