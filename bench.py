@@ -537,7 +537,9 @@ def run_e2e(args, idc, torch, p, pristine, dev, ws, tdist):
     outs = [torch.empty(host[0].shape, dtype=host[0].dtype, pin_memory=True) for _ in range(2)]
     streams = [torch.cuda.Stream(dev) for _ in range(ns)]
     bi = sum(a.numel() * 16 for a in ins)
-    steps = max(2, args.e2e_steps) if bi > 2e9 else max(16, args.e2e_steps)   # small calls: more steps
+    # small calls: more steps (>= 16, and >= ~2 GB of host -> device copies, so
+    # that one host-side hiccup does not decide a region of a few milliseconds)
+    steps = max(2, args.e2e_steps) if bi > 2e9 else max(16, args.e2e_steps, min(256, -(-int(2e9) // max(bi, 1))))
     bo = host[0].numel() * 16
 
     def step(k):

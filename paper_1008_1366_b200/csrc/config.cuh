@@ -8,6 +8,7 @@
 // | knob                    | default | what it selects                                                        |
 // |-------------------------|---------|------------------------------------------------------------------------|
 // | IDC_FOLD_TW             | 1       | Stockham pass twiddles folded into FMA-form DIT butterflies (fft_dev.cuh) |
+// | IDC_ROWS_TW_COH_MIN_E   | 16      | row kernels with E >= this reload pass twiddles per pass (coherent loads) |
 // | IDC_V2_MAX_M            | 4096    | rows up to this m run the rows2.cu kernels (K2/K3/K4 register-resident) |
 // | IDC_V3_MIN_M            | 512     | hconv / tconv rows from this m run the TMA-staged rows3.cu K3/K4        |
 // | IDC_ROWS_E              | 16      | rows2.cu elements per thread for m >= 1024                             |
@@ -40,6 +41,9 @@
 
 #ifndef IDC_FOLD_TW
 #define IDC_FOLD_TW 1
+#endif
+#ifndef IDC_ROWS_TW_COH_MIN_E
+#define IDC_ROWS_TW_COH_MIN_E 16
 #endif
 
 #ifndef IDC_V2_MAX_M

@@ -9,6 +9,7 @@
 // P:1079-1083) live in registers / shared memory ("stash"), never in HBM,
 // except for m = 8192 where the stash spills to the caller's workspace
 // (L2-resident).
+#define IDC_ROW_UNIT 1   // row kernels: coherent pass-twiddle loads at E >= 16 (fft_dev.cuh)
 #include "config.cuh"
 #include <atomic>
 

@@ -86,14 +86,32 @@ __device__ __forceinline__ double2 ldtw(const double2* p) {
   asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
 }
-// Stockham pass twiddles: read-only path (few per pass; ptxas keeps them in
-// registers across the row loop) unless a unit defines IDC_PASS_TW_COHERENT
-// (reloaded per pass from L1: fewer registers, more L1 traffic).
-#ifdef IDC_PASS_TW_COHERENT
-__device__ __forceinline__ double2 ldtw_pass(const double2* p) { return ldtw(p); }
-#else
-__device__ __forceinline__ double2 ldtw_pass(const double2* p) { return __ldg(p); }
+// Stockham pass twiddles: read-only path (ptxas may keep them in registers
+// across the row loop) or coherent loads (reloaded per pass from L1: fewer
+// registers, more L1 traffic).  Coherent in the row kernels with E >= 16
+// (IDC_ROWS_TW_COH_MIN_E; units defining IDC_ROW_UNIT): there the hoisted
+// twiddles pushed the 255-register kernels into local-memory spills (K2<1024>
+// 264 -> 16 bytes of stack, K4<4096> 232 -> 8; cconv1d 1024 0.740 -> 0.716 ms,
+// tconv1d 4096 0.868 -> 0.844 ms), while at E = 8 and in the pencil kernels
+// the reloads cost more than they save (hconv1d 512 0.592 -> 0.616 ms,
+// hconv3d 56.1 -> 57.5 ms; profiles/r02/ab/pass_tw_coherent.log).
+// IDC_PASS_TW_COHERENT makes every unit coherent (experiments).
+#ifndef IDC_ROW_UNIT
+#define IDC_ROW_UNIT 0
 #endif
+template <int E>
+__host__ __device__ constexpr bool pass_tw_coherent() {
+#ifdef IDC_PASS_TW_COHERENT
+  return true;
+#else
+  return IDC_ROW_UNIT && E >= IDC_ROWS_TW_COH_MIN_E;
+#endif
+}
+template <int E>
+__device__ __forceinline__ double2 ldtw_pass(const double2* p) {
+  if constexpr (pass_tw_coherent<E>()) return ldtw(p);
+  else return __ldg(p);
+}
 // Data load that the compiler may not merge with an earlier load of the same
 // address (the residue loops re-read the row; keeping the first read live
 // across transforms would cost 4 registers per element).  L1-cached.
@@ -347,13 +365,13 @@ __device__ __forceinline__ PassTw<N, E, R, NS> load_pass_tw(int t, const double2
       const double2* tp = tw + pass_tab_offset<N, E>(NS) + jm;
 #if IDC_FOLD_TW
 #pragma unroll
-      for (int l = 0; l < ilog2(R); ++l) p.p[b][l] = ldtw_pass(&tp[l * NS]);
+      for (int l = 0; l < ilog2(R); ++l) p.p[b][l] = ldtw_pass<E>(&tp[l * NS]);
 #else
       constexpr int Q = pass_q(R);
 #pragma unroll
-      for (int c = 1; c < Q; ++c) p.lo[b][c] = ldtw_pass(&tp[(c - 1) * NS]);
+      for (int c = 1; c < Q; ++c) p.lo[b][c] = ldtw_pass<E>(&tp[(c - 1) * NS]);
 #pragma unroll
-      for (int a = 1; a < R / Q; ++a) p.hi[b][a] = ldtw_pass(&tp[(Q - 2 + a) * NS]);
+      for (int a = 1; a < R / Q; ++a) p.hi[b][a] = ldtw_pass<E>(&tp[(Q - 2 + a) * NS]);
 #endif
     }
   }

@@ -9,6 +9,7 @@
 //     accumulator of tconv) stay in registers; shared memory holds only the
 //     Stockham exchange buffer (plus, for tconv, the f*g stream products), so
 //     the row's inputs stay L1-resident for the mirrored (U_{m-k}) loads.
+#define IDC_ROW_UNIT 1   // row kernels: coherent pass-twiddle loads at E >= 16 (fft_dev.cuh)
 #include "config.cuh"
 #include "fft_dev.cuh"
 #include "launch.cuh"

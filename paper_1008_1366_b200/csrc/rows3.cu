@@ -15,6 +15,7 @@
 //     hconv; the f*g stream products of tconv) lives in registers; tconv
 //     parks the first residue pair's partial sum in the (already staged)
 //     global f row and finishes it with the second pair.
+#define IDC_ROW_UNIT 1   // row kernels: coherent pass-twiddle loads at E >= 16 (fft_dev.cuh)
 #include "config.cuh"
 #include "fft_dev.cuh"
 #include "launch.cuh"

@@ -16,6 +16,7 @@
 //
 // Layout: pair i's rows start at f + i * istride (g likewise); row j of pair
 // i is f + i * istride + j * m.  The result goes to pair 0's rows (f).
+#define IDC_ROW_UNIT 1   // row kernels: coherent pass-twiddle loads at E >= 16 (fft_dev.cuh)
 #include "fft_dev.cuh"
 #include "launch.cuh"
 #include "kernels.cuh"
