@@ -11,6 +11,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <vector>
 #include <cstdlib>
 
 constexpr int NST = 3;                 // stages of 64 KB
@@ -144,7 +145,16 @@ int main(int argc, char** argv) {
   const int smem = NST * STAGE + 64;
   cudaFuncSetAttribute(k_load, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   printf("%d rows, row pitch %ld columns (%ld bytes)\n", rows, cols, cols * 16);
-  for (int W : {4, 8, 16}) {
+  std::vector<int> widths = {4, 8, 16};
+  if (argc > 4) {                         // comma-separated widths, e.g. "1,2,4"
+    widths.clear();
+    for (const char* p = argv[4]; *p;) {
+      widths.push_back(atoi(p));
+      while (*p && *p != ',') ++p;
+      if (*p == ',') ++p;
+    }
+  }
+  for (int W : widths) {
     CUtensorMap map;
     const int BR = STAGE / (W * 16) < 256 ? STAGE / (W * 16) : 256;
     cuuint64_t dims[2] = {(cuuint64_t)(2 * cols), (cuuint64_t)rows};
