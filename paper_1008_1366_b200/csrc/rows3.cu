@@ -107,7 +107,9 @@ k_hconv_rows3(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
     double2 v[E], Q[E];
     double p0[E];
     // ONE: all three residue streams from one read of the staged pair, the
-    // r = -1 stream kept in registers (E <= 8: room below 255 registers);
+    // r = -1 stream kept in registers (at E = 16 spill-free since the E = 16
+    // rows reload pass twiddles per pass: hconv1d 4096 0.437 -> 0.419 ms,
+    // hconv2d 4095 x 2048 0.600 -> 0.584 ms, profiles/r02/ab/k3_one_split_e16.log);
     // halves the split's shared-memory wavefronts and frees the stage for
     // the next row's bulk copy before the first transform
     constexpr bool ONE = E <= IDC_K3_ONE_SPLIT_MAXE;
