@@ -356,7 +356,7 @@ struct PassTw {
 };
 template <int N, int E, int R, int NS>
 __device__ __forceinline__ PassTw<N, E, R, NS> load_pass_tw(int t, const double2* __restrict__ tw) {
-  PassTw<N, E, R, NS> p;
+  PassTw<N, E, R, NS> p{};
   if constexpr (NS > 1) {
     constexpr int T = N / E, B = E / R;
 #pragma unroll
@@ -583,6 +583,63 @@ __device__ __forceinline__ void fft2(double2 (&v)[E], double2 (&w)[E], int t, do
   asm volatile("mov.b32 %0, %1;" : "=r"(tl) : "r"(t));
   count_fft(ilog2(N), tl, 2);
   fft2_passes<N, E, 1, SIGN>(v, w, tl, xb, xb2, tw, sync, xs, PassTw<N, E, pass_radix(N, E, 1), 1>{});
+}
+
+// Two independent N-point FFTs with their exchanges staggered by half a pass
+// (IDC_FFT2_STAGGER): while one vector's pass output goes through shared
+// memory, the other vector's butterflies run, so the shared-memory pipe and
+// the fp64 pipe work at the same time (tools/pipe_overlap.cu: on B200 a mix
+// of independent DFMA and STS/LDS.128 streams takes max(F, S), not F + S).
+// Per pass with an exchange after it (v computed, w ready):
+//   store v -> xb ; compute w ; barrier ; load v ; store w -> xb2 ;
+//   compute v (next pass) ; barrier ; load w
+// -- the same two barriers per pass as fft2, both buffers as in fft2.
+template <int N, int E, int R, int NS, class XS>
+__device__ __forceinline__ void pass_store(const double2 (&v)[E], int t, double2* __restrict__ xb, XS xs) {
+  constexpr int T = N / E, B = E / R;
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const int j = t + T * b;
+    const int base = (j / NS) * NS * R + (j & (NS - 1));
+#pragma unroll
+    for (int r = 0; r < R; ++r) xb[xs(xpad<NS, R>(base + r * NS))] = v[b + r * B];
+  }
+}
+template <int N, int E, int R, int NS, class XS>
+__device__ __forceinline__ void pass_load(double2 (&v)[E], int t, const double2* __restrict__ xb, XS xs) {
+  constexpr int T = N / E;
+#pragma unroll
+  for (int i = 0; i < E; ++i) v[i] = xb[xs(xpad<NS, R>(t + T * i))];
+}
+template <int N, int E, int NS, int SIGN, int SIGN2, class Sync, class XS>
+__device__ __forceinline__ void fft2s_step(double2 (&v)[E], double2 (&w)[E], int t, double2* __restrict__ xb,
+                                           double2* __restrict__ xb2, const double2* __restrict__ tw, Sync sync,
+                                           XS xs) {
+  constexpr int R = pass_radix(N, E, NS), NR = NS * R;
+  if constexpr (NR < N) {
+    pass_store<N, E, R, NS>(v, t, xb, xs);
+    pass_compute<N, E, R, NS, SIGN2>(w, t, tw);
+    sync();
+    pass_load<N, E, R, NS>(v, t, xb, xs);
+    pass_store<N, E, R, NS>(w, t, xb2, xs);
+    pass_compute<N, E, pass_radix(N, E, NR), NR, SIGN>(v, t, tw);
+    sync();
+    pass_load<N, E, R, NS>(w, t, xb2, xs);
+    fft2s_step<N, E, NR, SIGN, SIGN2>(v, w, t, xb, xb2, tw, sync, xs);
+  } else {
+    pass_compute<N, E, R, NS, SIGN2>(w, t, tw);
+  }
+}
+// v transformed with sign SIGN, w with SIGN2 (default the same)
+template <int N, int E, int SIGN, int SIGN2 = SIGN, class Sync, class XS = IdentitySlot>
+__device__ __forceinline__ void fft2s(double2 (&v)[E], double2 (&w)[E], int t, double2* __restrict__ xb,
+                                      double2* __restrict__ xb2, const double2* __restrict__ tw, Sync sync,
+                                      XS xs = XS{}) {
+  int tl;
+  asm volatile("mov.b32 %0, %1;" : "=r"(tl) : "r"(t));
+  count_fft(ilog2(N), tl, 2);
+  pass_compute<N, E, pass_radix(N, E, 1), 1, SIGN>(v, tl, tw);
+  fft2s_step<N, E, 1, SIGN, SIGN2>(v, w, tl, xb, xb2, tw, sync, xs);
 }
 
 // CTA barrier as volatile asm: it keeps its order relative to the volatile

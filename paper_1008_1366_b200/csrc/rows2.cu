@@ -17,6 +17,15 @@
 #include "tables.cuh"
 #include "tma.cuh"
 
+#ifndef IDC_FFT2_STAGGER
+#define IDC_FFT2_STAGGER 1
+#endif
+#if IDC_FFT2_STAGGER
+#define IDC_FFT2 fft2s
+#else
+#define IDC_FFT2 fft2
+#endif
+
 namespace idc {
 
 namespace {
@@ -162,19 +171,19 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
         z[i] = cmul(b, w);
       });
       refill();
-      fft2<M, E, +1>(x, y, t, xb, xb2, twM, sync);                        // r = 0
+      IDC_FFT2<M, E, +1>(x, y, t, xb, xb2, twM, sync);                        // r = 0
 #pragma unroll
       for (int i = 0; i < E; ++i) x[i] = cmul(x[i], y[i]);
-      fft2<M, E, +1>(y1, z, t, xb, xb2, twM, sync);
+      IDC_FFT2<M, E, +1>(y1, z, t, xb, xb2, twM, sync);
 #pragma unroll
       for (int i = 0; i < E; ++i) y[i] = cmul(y1[i], z[i]);
-      fft2<M, E, -1>(x, y, t, xb, xb2, twM, sync);                        // forward
+      IDC_FFT2<M, E, -1>(x, y, t, xb, xb2, twM, sync);                        // forward
     } else if constexpr (FFT2) {
 #pragma unroll
       for (int i = 0; i < E; ++i) x[i] = ldrow<ST>(&fr[t + T * i]);
 #pragma unroll
       for (int i = 0; i < E; ++i) y[i] = ldrow<ST>(&gr[t + T * i]);
-      fft2<M, E, +1>(x, y, t, xb, xb2, twM, sync);                        // r = 0
+      IDC_FFT2<M, E, +1>(x, y, t, xb, xb2, twM, sync);                        // r = 0
 #pragma unroll
       for (int i = 0; i < E; ++i) x[i] = cmul(x[i], y[i]);
       // r = 1: zeta_{2m}^k-shifted streams
@@ -182,10 +191,10 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
       for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { y[i] = cmul(ldrow<ST>(&fr[t + T * i]), w); });
       for_roots<2 * E, 1, +1, E>(zt, [&](int i, double2 w) { z[i] = cmul(ldrow<ST>(&gr[t + T * i]), w); });
       refill();
-      fft2<M, E, +1>(y, z, t, xb, xb2, twM, sync);
+      IDC_FFT2<M, E, +1>(y, z, t, xb, xb2, twM, sync);
 #pragma unroll
       for (int i = 0; i < E; ++i) y[i] = cmul(y[i], z[i]);
-      fft2<M, E, -1>(x, y, t, xb, xb2, twM, sync);                        // forward
+      IDC_FFT2<M, E, -1>(x, y, t, xb, xb2, twM, sync);                        // forward
     } else if constexpr (PARK) {
       // r = 0 stream all the way back first, parked in this thread's own
       // shared-memory slots while the r = 1 stream is transformed: two

@@ -37,7 +37,10 @@ struct Cfg3 {
   static constexpr int G = T >= 256 ? 1 : 256 / T;     // row groups per CTA
   static constexpr int THREADS = G * T;
   static constexpr int XB = xbuf_elems<M, E>() > M ? xbuf_elems<M, E>() : M;
-  static constexpr int PER = 2 * M + XB;              // staged f, g + exchange buffer (double2)
+  // K3 pairs independent transforms with staggered exchanges (fft2s) where a
+  // second exchange buffer fits: m <= IDC_K3_STAGGER_MAX_M
+  static constexpr bool STAG = M <= IDC_K3_STAGGER_MAX_M;
+  static constexpr int PER = 2 * M + (STAG ? 2 : 1) * XB;   // staged f, g + exchange buffer(s) (double2)
   static constexpr size_t SMEM = (size_t)G * PER * 16 + (size_t)G * 16;  // + one mbarrier per group
   static constexpr bool NAMED = G > 1;
   static constexpr int MINB = M <= 512 ? IDC_ROWS3_MINB_SMALL : 1;   // CTAs per SM (register cap)
@@ -143,6 +146,17 @@ k_hconv_rows3(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
         tma_load_1d(Gs, row_ptr(g, rs.g1, rs.n0, row + stride, M), M * 16u, bar);
       }
     }
+    if constexpr (C::STAG && ONE) {
+      // five transforms as two staggered pairs and one single: (v, Q)
+      // backward; (Q forward, r = -1 stream backward); P_{-1} forward
+      double2* xb2 = xb + C::XB;
+      fft2s<M, E, +1>(v, Q, t, xb, xb2, twM, sync);             // two c2r pairs, residues 0 and 1
+#pragma unroll
+      for (int i = 0; i < E; ++i) Q[i] = make_double2(v[i].x * v[i].y, Q[i].x * Q[i].y);
+      fft2s<M, E, -1, +1>(Q, Vm, t, xb, xb2, twM, sync);         // Q = fft(p_0 + i p_1); r = -1 pair
+#pragma unroll
+      for (int i = 0; i < E; ++i) v[i] = make_double2(Vm[i].x * Vm[i].y, 0.0);
+    } else {
     fft<M, E, +1>(v, t, xb, twM, sync);                         // two c2r in one complex FFT
 #pragma unroll
     for (int i = 0; i < E; ++i) p0[i] = v[i].x * v[i].y;
@@ -170,6 +184,7 @@ k_hconv_rows3(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
     fft<M, E, +1>(v, t, xb, twM, sync);
 #pragma unroll
     for (int i = 0; i < E; ++i) v[i] = make_double2(v[i].x * v[i].y, 0.0);
+    }
     fft<M, E, -1>(v, t, xb, twM, sync);                         // P_{-1}
     // P_0, P_1 from Q via Q_{m-k}; 3m h_k = P_0 + zeta^{k} P_{-1} + zeta^{-k} P_1 (Eq. fft0forwardB)
 #pragma unroll
