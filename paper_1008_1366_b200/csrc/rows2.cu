@@ -49,6 +49,20 @@ struct Cfg2 {
   static constexpr int MINB = (65536 / (THREADS * IDC_ROWS_REGS)) < 1 ? 1 : 65536 / (THREADS * IDC_ROWS_REGS);
 };
 
+// K2 shared-memory layout per row group, used by the kernel and its launcher:
+// staged f, g rows (m <= IDC_ROWS2_TMA_MAX), one exchange buffer per vector
+// transformed at once (two for the pairs at E = 8; pairs at E = 16 measured
+// slower: cconv1d 1024 0.704 -> 0.784 ms, profiles/r02/ab/k2_pairs_e16.log),
+// and the parked r = 0 result (single transforms from IDC_K2_PARK_MIN up).
+template <int M, int E>
+struct K2Layout {
+  static constexpr bool FFT2 = E <= 8;
+  static constexpr bool ST = M <= IDC_ROWS2_TMA_MAX;
+  static constexpr bool PARK = !FFT2 && M >= IDC_K2_PARK_MIN;
+  static constexpr int XB = xbuf_elems<M, E>() > M ? xbuf_elems<M, E>() : M;
+  static constexpr int PER = (ST ? 2 * M : 0) + (FFT2 ? 2 : 1) * XB + (PARK ? M : 0);
+};
+
 template <bool NAMED>
 struct RowSync;
 template <>
@@ -94,12 +108,12 @@ k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
   constexpr int T = C::T;
   extern __shared__ __align__(16) double2 smem[];
   const int grp = threadIdx.x / T, t = threadIdx.x - grp * T;
-  constexpr bool FFT2 = E <= 8;
+  constexpr bool FFT2 = K2Layout<M, E>::FFT2;   // transforms in (staggered) pairs, two exchange buffers
   // ST: per group the staged f and g rows, then the exchange buffer(s); the
   // groups' mbarriers after all groups.  Otherwise exchange buffers only.
   constexpr bool ST = M <= IDC_ROWS2_TMA_MAX;
-  constexpr bool PARK = !FFT2 && M >= IDC_K2_PARK_MIN;   // r = 0 result parked in shared memory
-  constexpr int PER = (ST ? 2 * M : 0) + (FFT2 ? 2 : 1) * C::XB + (PARK ? M : 0);
+  constexpr bool PARK = K2Layout<M, E>::PARK;   // r = 0 result parked in shared memory
+  constexpr int PER = K2Layout<M, E>::PER;
   double2* Fs = smem + grp * PER;
   double2* Gs = Fs + M;
   double2* xb = ST ? Gs + M : Fs;
@@ -462,8 +476,7 @@ cudaError_t cconv_rows2(double2* f, double2* g, long nrows, cudaStream_t s, RowS
   if (!twM || !tw2M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &nrows, &twM, &tw2M, &rs};
   // staged f, g rows (m <= IDC_ROWS2_TMA_MAX) + exchange buffer(s) + mbarriers
-  constexpr size_t per = (M <= IDC_ROWS2_TMA_MAX ? 2 * M : 0) + (E <= 8 ? 2 : 1) * C::XB +
-                         (E > 8 && M >= IDC_K2_PARK_MIN ? M : 0);
+  constexpr size_t per = K2Layout<M, E>::PER;
   static_assert((size_t)G * per * 16 + (size_t)G * 8 <= 227 * 1024, "K2 configuration exceeds shared memory");
   return launch2(k_cconv_rows2<M, E, G>, C::THREADS, (size_t)G * per * 16 + (size_t)G * 8, nrows, G, s, args, "K2", M);
 }
