@@ -30,6 +30,7 @@
 // | IDC_PENCIL0_MINB        | =above  | K7 CTAs per SM                                                          |
 // | IDC_K56_NARROW_MIN/MAX  | 256/1024| K5/K6 with 128-thread CTAs (half-width tiles) for m in this range      |
 // | IDC_K56_TMA_STORE_MAXW  | 2       | K5/K6 store tiles of at most this many columns by TMA tensor stores     |
+// | IDC_K5_PAIR             | 1       | K5 with per-thread stores: odd/even streams as a staggered pair (fft2s) |
 // | IDC_K5_DOUBLE_XB        | 1       | K5 second exchange buffer (odd stream's store drains during the even)  |
 // | IDC_K78_WIDE_MIN/MAX    | 256/4096| K7/K8 with E = 16 and 256-thread CTAs for m in this range               |
 // | IDC_K78_NARROW_MASK     | m=1024,256 | K7/K8 with 128-thread CTAs for the m whose log2 bit is set           |
@@ -112,6 +113,9 @@
 #endif
 #ifndef IDC_K56_TMA_STORE_MAXW
 #define IDC_K56_TMA_STORE_MAXW 2
+#endif
+#ifndef IDC_K5_PAIR
+#define IDC_K5_PAIR 1
 #endif
 #ifndef IDC_K5_DOUBLE_XB
 #define IDC_K5_DOUBLE_XB 1

@@ -174,6 +174,14 @@ constexpr bool k5_double_xb() {
   return IDC_K5_DOUBLE_XB && C::W <= IDC_K56_TMA_STORE_MAXW &&
          ((size_t)N * C::W + 2 * (size_t)C::XB) * 16 + 16 <= 227 * 1024;
 }
+// K5 with per-thread stores (wider tiles): the odd and even streams are
+// transformed as a staggered pair (fft2s) where a second exchange buffer fits
+template <int N>
+constexpr bool k5_pair() {
+  using C = K56Cfg<N>;
+  return IDC_K5_PAIR && C::W > IDC_K56_TMA_STORE_MAXW &&
+         ((size_t)N * C::W + 2 * (size_t)C::XB) * 16 + 16 <= 227 * 1024;
+}
 
 // ------------------------------------------------------------------- K5 --
 template <int N, bool DIST = false>
@@ -186,7 +194,8 @@ k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
   using C = K56Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   constexpr bool TS = DIST || W <= IDC_K56_TMA_STORE_MAXW;   // outputs by TMA stores
-  constexpr bool DB = !DIST && k5_double_xb<N>();            // second exchange buffer for the even stream
+  constexpr bool PAIR = !DIST && k5_pair<N>();                 // streams as a staggered pair
+  constexpr bool DB = !DIST && (k5_double_xb<N>() || PAIR);   // second exchange buffer
   extern __shared__ __align__(128) double2 smem[];
   double2* stage = smem;                       // N x W
   double2* xb = stage + N * W;
@@ -235,7 +244,7 @@ k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
     // odd stream u_{2l+1} = sum_k zeta_m^{lk} zeta_{2m}^k U_k  (Eq. cconv1backward)
     // zeta_{2m}^k, k = t + T i: zeta_{2m}^t x zeta_{2E}^i (immediate)
     for_roots<2 * E, 1, +1, E>(cmul(ldtw(&tw2N[t]), ophase), [&](int i, double2 w) { v[i] = cmul(x0[i], w); });
-    fft<N, E, +1>(v, t, xb, twN, CtaSync{}, xs);
+    if constexpr (!PAIR) fft<N, E, +1>(v, t, xb, twN, CtaSync{}, xs);
     if constexpr (TS) {
       if constexpr (DB) {
         // odd stream out of xb while the even stream transforms in xb1; the
@@ -251,6 +260,18 @@ k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
       fft<N, E, +1>(x0, t, xb1, twN, CtaSync{}, xs);   // even stream (in place, or to the send blocks)
       if constexpr (DIST) tile_store_dist<N, E, W>(x0, t, c, xb1, &dio.st[in][0], col0, item, dio.L, dio.BRd);
       else tile_store<N, E, W, BR>(x0, t, c, xb1, in == 0 ? &mf : &mg, col0, item);
+    } else if constexpr (PAIR) {
+      fft2s<N, E, +1>(v, x0, t, xb, xb1, twN, CtaSync{}, xs);   // odd and even streams, staggered
+      const long rs = (long)T * tl.ncols;   // pointer step between a thread's rows
+      if (ok) {
+        double2* p = u + (long)t * tl.ncols;
+        double2* q = a + (long)t * tl.ncols;
+#pragma unroll
+        for (int i = 0; i < E; ++i, p += rs, q += rs) {
+          *p = v[i];
+          *q = x0[i];
+        }
+      }
     } else {
       const long rs = (long)T * tl.ncols;   // pointer step between a thread's rows
       if (ok) {
@@ -775,7 +796,7 @@ cudaError_t pad_bwd_tma(double2* f, double2* g, double2* U, double2* V, long nco
     const size_t smem = ((size_t)N * C::W + (size_t)C::XB) * 16 + 16;
     return launch_t(k_pad_bwd_tma<N, true>, C::THREADS, smem, tl.ntiles, s, args, tag);
   }
-  const size_t smem = ((size_t)N * C::W + (k5_double_xb<N>() ? 2 : 1) * (size_t)C::XB) * 16 + 16;
+  const size_t smem = ((size_t)N * C::W + (k5_double_xb<N>() || k5_pair<N>() ? 2 : 1) * (size_t)C::XB) * 16 + 16;
   return launch_t(k_pad_bwd_tma<N, false>, C::THREADS, smem, tl.ntiles, s, args, tag);
 }
 
