@@ -7,6 +7,8 @@
 //
 // | knob                    | default | what it selects                                                        |
 // |-------------------------|---------|------------------------------------------------------------------------|
+// | IDC_PDL                 | 1       | kernels launched with programmatic dependent launch (pdl.cuh)          |
+// | IDC_PDL_TRIGGER         | 0       | early griddepcontrol.launch_dependents at kernel start (pdl.cuh)       |
 // | IDC_FOLD_TW             | 1       | Stockham pass twiddles folded into FMA-form DIT butterflies (fft_dev.cuh) |
 // | IDC_ROWS_TW_COH_MIN_E   | 16      | row kernels with E >= this reload pass twiddles per pass (coherent loads) |
 // | IDC_V2_MAX_M            | 4096    | rows up to this m run the rows2.cu kernels (K2/K3/K4 register-resident) |

@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS, 1)
 k_cconv_rows(double2* __restrict__ f, double2* __restrict__ g, long nrows,
              const double2* __restrict__ twM, const double2* __restrict__ tw2M,
              double2* __restrict__ gwork) {
+  pdl_entry();
   using C = RowCfg<M>;
   constexpr int E = C::E, T = C::T, G = C::G;
   extern __shared__ __align__(16) double2 smem[];
@@ -151,6 +152,7 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS, 1)
 k_hconv_rows(double2* __restrict__ f, double2* __restrict__ g, long nrows,
              const double2* __restrict__ twM, const double2* __restrict__ tw3M,
              double2* __restrict__ gwork) {
+  pdl_entry();
   using C = RowCfg<M>;
   constexpr int E = C::E, T = C::T, G = C::G;
   extern __shared__ __align__(16) double2 smem[];
@@ -239,6 +241,7 @@ __global__ void __launch_bounds__(RowCfg<M>::THREADS, 1)
 k_tconv_rows(double2* __restrict__ f, double2* __restrict__ g, double2* __restrict__ h, long nrows,
              const double2* __restrict__ twM, const double2* __restrict__ tw4M,
              double2* __restrict__ gwork) {
+  pdl_entry();
   using C = RowCfg<M>;
   constexpr int E = C::E, T = C::T, G = C::G;
   extern __shared__ __align__(16) double2 smem[];

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include "config.cuh"
+#include "pdl.cuh"
 #include <type_traits>
 #include <utility>
 

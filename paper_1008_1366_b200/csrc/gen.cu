@@ -7,6 +7,7 @@
 #include <cstdint>
 
 #include "../../include/idconv.h"
+#include "pdl.cuh"
 
 namespace {
 __host__ __device__ __forceinline__ uint64_t sm64(uint64_t x) {
@@ -16,6 +17,7 @@ __host__ __device__ __forceinline__ uint64_t sm64(uint64_t x) {
   return z ^ (z >> 31);
 }
 __global__ void k_fill_uniform(double2* out, size_t n, uint64_t key, uint64_t start) {
+  idc::pdl_entry();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const uint64_t b = key + 2ull * (start + i);
     const double re = (double)(sm64(b) >> 11) * 0x1.0p-53 * 2.0 - 1.0;

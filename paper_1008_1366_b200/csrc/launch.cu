@@ -8,6 +8,7 @@
 
 #include "../../include/idconv.h"
 #include "fft_dev.cuh"
+#include "pdl.cuh"
 #include "kernels.cuh"
 #include "launch.cuh"
 
@@ -54,7 +55,19 @@ cudaError_t launch_kernel(const void* fn, dim3 grid, dim3 block, void** args, si
     std::lock_guard<std::mutex> lk(g_mu);
     on = g_on;
   }
-  if (!on) return cudaLaunchKernel(fn, grid, block, args, smem, s);
+  // programmatic stream serialization: the kernel may be scheduled while the
+  // previous kernel on the stream drains; its pdl_entry() waits (pdl.cuh)
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = IDC_PDL ? 1 : 0;
+  if (!on) return cudaLaunchKernelExC(&cfg, fn, args);
   cudaEvent_t a, b;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -62,7 +75,7 @@ cudaError_t launch_kernel(const void* fn, dim3 grid, dim3 block, void** args, si
     b = get_event();
   }
   cudaEventRecord(a, s);
-  const cudaError_t e = cudaLaunchKernel(fn, grid, block, args, smem, s);
+  const cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
   cudaEventRecord(b, s);
   std::lock_guard<std::mutex> lk(g_mu);
   g_recs.push_back(Rec{tag.tag, tag.n, tag.units, a, b});

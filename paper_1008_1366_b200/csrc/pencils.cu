@@ -56,6 +56,7 @@ template <int N, int E, int W>
 __global__ void __launch_bounds__(PCfg<N, E, W>::THREADS)
 k_pad_bwd(double2* __restrict__ f, double2* __restrict__ g, double2* __restrict__ U, double2* __restrict__ V,
           Pencil pc, const double2* __restrict__ twN, const double2* __restrict__ tw2N, double2 ophase) {
+  pdl_entry();
   using C = PCfg<N, E, W>;
   constexpr int T = C::T;
   extern __shared__ __align__(16) double2 smem[];
@@ -89,6 +90,7 @@ template <int N, int E, int W>
 __global__ void __launch_bounds__(PCfg<N, E, W>::THREADS)
 k_pad_fwd(double2* __restrict__ f, const double2* __restrict__ U, Pencil pc, const double2* __restrict__ twN,
           const double2* __restrict__ tw2N, double2 ophase) {
+  pdl_entry();
   using C = PCfg<N, E, W>;
   constexpr int T = C::T;
   extern __shared__ __align__(16) double2 smem[];
@@ -120,6 +122,7 @@ template <int N, int E, int W>
 __global__ void __launch_bounds__(PCfg<N, E, W>::THREADS)
 k_pad0_bwd(double2* __restrict__ f, double2* __restrict__ g, double2* __restrict__ U, double2* __restrict__ V,
            Pencil pc, const double2* __restrict__ twN, const double2* __restrict__ tw3N) {
+  pdl_entry();
   using C = PCfg<N, E, W>;
   constexpr int T = C::T;
   extern __shared__ __align__(16) double2 smem[];
@@ -172,6 +175,7 @@ template <int N, int E, int W>
 __global__ void __launch_bounds__(PCfg<N, E, W>::THREADS)
 k_pad0_fwd(double2* __restrict__ f, const double2* __restrict__ U, Pencil pc, const double2* __restrict__ twN,
            const double2* __restrict__ tw3N) {
+  pdl_entry();
   using C = PCfg<N, E, W>;
   constexpr int T = C::T;
   extern __shared__ __align__(16) double2 smem[];

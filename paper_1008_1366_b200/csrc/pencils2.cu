@@ -191,6 +191,7 @@ k_pad_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CU
               const double2* __restrict__ twN, const double2* __restrict__ tw2N, double2 ophase,
               const __grid_constant__ CUtensorMap mU, const __grid_constant__ CUtensorMap mV,
               const __grid_constant__ DistIO dio) {
+  pdl_entry();
   using C = K56Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   constexpr bool TS = DIST || W <= IDC_K56_TMA_STORE_MAXW;   // outputs by TMA stores
@@ -296,6 +297,7 @@ __global__ void __launch_bounds__(K56Cfg<N>::THREADS, IDC_PENCIL_MINB)
 k_pad_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ CUtensorMap mu, double2* __restrict__ f,
               Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw2N, double2 ophase,
               const __grid_constant__ DistIO dio) {
+  pdl_entry();
   using C = K56Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
   constexpr bool TS = W <= IDC_K56_TMA_STORE_MAXW;   // output by TMA stores
@@ -401,6 +403,7 @@ k_pad0_bwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
                double2* __restrict__ f, double2* __restrict__ g, double2* __restrict__ U, double2* __restrict__ V,
                Tiles tl, const double2* __restrict__ twN, const double2* __restrict__ tw3N,
                const __grid_constant__ K7StoreMaps sm, const __grid_constant__ DistIO dio) {
+  pdl_entry();
   static_assert(!DIST || IDC_K7_TMA_STORE, "distributed K7 stores through TMA");
   using C = K78Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;
@@ -564,6 +567,7 @@ k_pad0_fwd_tma(const __grid_constant__ CUtensorMap mf, const __grid_constant__ C
                const double2* __restrict__ twN, const double2* __restrict__ tw3N,
                const __grid_constant__ CUtensorMap mflo, const __grid_constant__ CUtensorMap mfhi,
                const __grid_constant__ DistIO dio) {
+  pdl_entry();
   static_assert(!DIST || IDC_K8_TMA_STORE == 2, "distributed K8 stores through TMA");
   using C = K78Cfg<N>;
   constexpr int E = C::E, T = C::T, W = C::W, BR = C::BR;

@@ -104,6 +104,7 @@ template <int M, int E, int G>
 __global__ void __launch_bounds__(Cfg2<M, E, G>::THREADS, Cfg2<M, E, G>::MINB)
 k_cconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, const double2* __restrict__ twM,
               const double2* __restrict__ tw2M, RowSets rs) {
+  pdl_entry();
   using C = Cfg2<M, E, G>;
   constexpr int T = C::T;
   extern __shared__ __align__(16) double2 smem[];
@@ -274,6 +275,7 @@ template <int M, int E, int G>
 __global__ void __launch_bounds__(Cfg2<M, E, G>::THREADS, Cfg2<M, E, G>::MINB)
 k_hconv_rows2(double2* __restrict__ f, double2* __restrict__ g, long nrows, const double2* __restrict__ twM,
               const double2* __restrict__ tw3M) {
+  pdl_entry();
   using C = Cfg2<M, E, G>;
   constexpr int T = C::T;
   extern __shared__ __align__(16) double2 smem[];
@@ -351,6 +353,7 @@ template <int M, int E, int G>
 __global__ void __launch_bounds__(Cfg2<M, E, G>::THREADS, Cfg2<M, E, G>::MINB)
 k_tconv_rows2(double2* __restrict__ f, double2* __restrict__ g, double2* __restrict__ h, long nrows,
               const double2* __restrict__ twM, const double2* __restrict__ tw4M) {
+  pdl_entry();
   using C = Cfg2<M, E, G>;
   constexpr int T = C::T;
   extern __shared__ __align__(16) double2 smem[];

@@ -80,6 +80,7 @@ template <int M>
 __global__ void __launch_bounds__(Cfg3<M>::THREADS, Cfg3<M>::MINB)
 k_hconv_rows3(double2* __restrict__ f, double2* __restrict__ g, long nrows, const double2* __restrict__ twM,
               const double2* __restrict__ tw3M, RowSets rs) {
+  pdl_entry();
   using C = Cfg3<M>;
   constexpr int E = C::E, T = C::T, G = C::G;
   extern __shared__ __align__(128) double2 smem[];
@@ -209,6 +210,7 @@ template <int M>
 __global__ void __launch_bounds__(Cfg3<M>::THREADS, Cfg3<M>::MINB)
 k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const double2* __restrict__ h, long nrows,
               const double2* __restrict__ twM, const double2* __restrict__ tw4M) {
+  pdl_entry();
   using C = Cfg3<M>;
   constexpr int E = C::E, T = C::T, G = C::G;
   extern __shared__ __align__(128) double2 smem[];

@@ -62,6 +62,7 @@ template <int M>
 __global__ void __launch_bounds__(DCfg<M>::THREADS, 1)
 k_hconv_dot_rows(double2* __restrict__ f, const double2* __restrict__ g, int npairs, long istride, long nrows,
                  const double2* __restrict__ twM, const double2* __restrict__ tw3M) {
+  pdl_entry();
   using C = DCfg<M>;
   constexpr int E = C::E, T = C::T, G = C::G;
   extern __shared__ __align__(16) double2 smem[];
@@ -172,6 +173,7 @@ template <int M>
 __global__ void __launch_bounds__(D2Cfg<M>::THREADS, 1)
 k_cconv_dot_rows(double2* __restrict__ f, const double2* __restrict__ g, int npairs, long istride, long nrows,
                  const double2* __restrict__ twM, const double2* __restrict__ tw2M) {
+  pdl_entry();
   using C = D2Cfg<M>;
   constexpr int E = C::E, T = C::T, G = C::G;
   extern __shared__ __align__(16) double2 smem[];
@@ -232,6 +234,7 @@ template <int M>
 __global__ void __launch_bounds__(D2Cfg<M>::THREADS, 1)
 k_tconv_dot_rows(double2* __restrict__ f, const double2* __restrict__ g, const double2* __restrict__ h, int npairs,
                  long istride, long nrows, const double2* __restrict__ twM, const double2* __restrict__ tw4M) {
+  pdl_entry();
   using C = D2Cfg<M>;
   constexpr int E = C::E, T = C::T, G = C::G;
   extern __shared__ __align__(16) double2 smem[];
@@ -349,6 +352,7 @@ template <int M, int P>
 __global__ void __launch_bounds__(D2Cfg<M>::THREADS, 1)
 k_cconv_pq_rows(double2* __restrict__ f, const double2* __restrict__ g, int q, long nrows,
                 const double2* __restrict__ twM, const double2* __restrict__ twqM) {
+  pdl_entry();
   using C = D2Cfg<M>;
   constexpr int E = C::E, T = C::T, G = C::G;
   extern __shared__ __align__(16) double2 smem[];
@@ -420,6 +424,7 @@ k_cconv_pq_rows(double2* __restrict__ f, const double2* __restrict__ g, int q, l
 // array (AMB-7; "automatically enforce Hermitian symmetry"):
 // U_{kx,0} <- (U_{kx,0} + conj U_{-kx,0}) / 2, U_{0,0} real.
 __global__ void k_enforce_symmetry_2d(double2* __restrict__ a, int mx, int my, long batch) {
+  pdl_entry();
   const long n = (long)mx * batch;                   // kx = 0..mx-1 for every item
   for (long id = (long)blockIdx.x * blockDim.x + threadIdx.x; id < n; id += (long)gridDim.x * blockDim.x) {
     const long b = id / mx;
@@ -440,6 +445,7 @@ __global__ void k_enforce_symmetry_2d(double2* __restrict__ a, int mx, int my, l
 // (1/k^2 := 0 at k = 0: no mean flow).  f, g: 2 x (2mx-1) x my each.
 __global__ void k_advection2d_inputs(const double2* __restrict__ w, double2* __restrict__ f, double2* __restrict__ g,
                                      int mx, int my) {
+  pdl_entry();
   const long n = (long)(2 * mx - 1) * my;
   for (long id = (long)blockIdx.x * blockDim.x + threadIdx.x; id < n; id += (long)gridDim.x * blockDim.x) {
     const long i = id / my;
