@@ -22,6 +22,7 @@
 // | IDC_K2_ONE_READ         | 1       | K2 (E = 8, staged rows) builds both residues' streams from one read     |
 // | IDC_K3_ONE_SPLIT_MAXE   | 16      | K3 splits all three residues from one staged read up to this E          |
 // | IDC_K3_STAGGER_MAX_M    | 512     | K3 runs its transforms as staggered pairs (fft2s, two exchange buffers) |
+// | IDC_K3_STAGE_AS_XB      | 2048    | K3 from this m: first transform pair staggered in the consumed stage    |
 // | IDC_ROWS3_E8_MAX        | 512     | rows3.cu (K3/K4) use E = 8 up to this m, E = 16 above                   |
 // | IDC_ROWS3_MINB_SMALL    | 1       | rows3.cu CTAs per SM for m <= 512                                       |
 // | IDC_PENCIL_TMA          | 1       | 2D/3D pencils use the TMA kernels of pencils2.cu for 64 <= m <= 4096    |
@@ -82,6 +83,9 @@
 #endif
 #ifndef IDC_K3_STAGGER_MAX_M
 #define IDC_K3_STAGGER_MAX_M 512
+#endif
+#ifndef IDC_K3_STAGE_AS_XB
+#define IDC_K3_STAGE_AS_XB 2048
 #endif
 #ifndef IDC_ROWS3_E8_MAX
 #define IDC_ROWS3_E8_MAX 512

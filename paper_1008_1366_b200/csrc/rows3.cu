@@ -139,15 +139,34 @@ k_hconv_rows3(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
         if constexpr (ONE) Vm[i] = cmulc(cadd(A, B), zr);          // conj(zeta^k) (A + B)
       }
     });
-    if constexpr (ONE) {
+    // STAGF (no room for a second exchange buffer): the first pair of
+    // transforms runs staggered with the just-consumed stage as its second
+    // buffer, and the next row's copies are issued after that pair
+    // (m >= IDC_K3_STAGE_AS_XB: hconv1d 4096 0.428 -> 0.415 ms, hconv2d
+    // 4095 x 2048 0.558 -> 0.554 ms; m = 1024 within noise, off;
+    // profiles/r02/ab/k3_stage_as_xb.log)
+    constexpr bool STAGF = ONE && !C::STAG && IDC_K3_STAGE_AS_XB > 0 && M >= IDC_K3_STAGE_AS_XB && 2 * M >= C::XB;
+    auto refill_next = [&]() {
       sync();
       if (t == 0 && row + stride < nrows) {
         mbar_arrive_expect_tx(bar, 2u * M * 16u);
         tma_load_1d(F, row_ptr(f, rs.f1, rs.n0, row + stride, M), M * 16u, bar);
         tma_load_1d(Gs, row_ptr(g, rs.g1, rs.n0, row + stride, M), M * 16u, bar);
       }
-    }
-    if constexpr (C::STAG && ONE) {
+    };
+    if constexpr (ONE && !STAGF) refill_next();
+    if constexpr (STAGF) {
+      sync();                                                   // every thread's split read of the stage done
+      fft2s<M, E, +1>(v, Q, t, xb, F, twM, sync);               // two c2r pairs, residues 0 and 1
+#pragma unroll
+      for (int i = 0; i < E; ++i) Q[i] = make_double2(v[i].x * v[i].y, Q[i].x * Q[i].y);
+      fence_proxy_async_smem();                                 // generic writes to the stage before the TMA refill
+      refill_next();                                            // the stage's last use as a buffer is over
+      fft<M, E, -1>(Q, t, xb, twM, sync);                       // Q = fft(p_0 + i p_1)
+      fft<M, E, +1>(Vm, t, xb, twM, sync);                      // r = -1 pair
+#pragma unroll
+      for (int i = 0; i < E; ++i) v[i] = make_double2(Vm[i].x * Vm[i].y, 0.0);
+    } else if constexpr (C::STAG && ONE) {
       // five transforms as two staggered pairs and one single: (v, Q)
       // backward; (Q forward, r = -1 stream backward); P_{-1} forward
       double2* xb2 = xb + C::XB;
