@@ -168,8 +168,11 @@ int main(int argc, char** argv) {
       continue;
     }
     const int ncb = (int)(ucols / W);
+    // TSB_SMS=<n>: use n CTAs (one per SM) instead of all SMs -- tells a
+    // per-SM request-rate limit (GB/s scales with n) from a device-wide one
+    const int nuse = getenv("TSB_SMS") ? atoi(getenv("TSB_SMS")) : nsm;
     for (int per_sm : {1}) {
-      const int grid = nsm * per_sm;
+      const int grid = nuse * per_sm;
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
