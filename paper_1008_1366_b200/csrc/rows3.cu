@@ -30,11 +30,15 @@ namespace idc {
 
 namespace {
 
-template <int M>
+// H: K3 (true) or K4 (false); they differ only in the row groups per CTA at m <= 512
+template <int M, bool H = true>
 struct Cfg3 {
   static constexpr int E = M <= IDC_ROWS3_E8_MAX ? 8 : 16;   // 8 at m = 512 (measured 8% faster there)
   static constexpr int T = M / E;
-  static constexpr int G = T >= 256 ? 1 : 256 / T;     // row groups per CTA
+  // row groups per CTA: at m <= 512 K3 runs 6 (12 warps per SM at 168
+  // registers: hconv1d 512 0.569 -> 0.537 ms, hconv3d 55.5 -> 54.4 ms), K4
+  // keeps 4 (6 groups spill 88 bytes: tconv1d 512 +5%; profiles/r02/ab/rows3_groups_512.log)
+  static constexpr int G = M <= 512 ? (H ? IDC_K3_G512 : IDC_K4_G512) : (T >= 256 ? 1 : 256 / T);
   static constexpr int THREADS = G * T;
   static constexpr int XB = xbuf_elems<M, E>() > M ? xbuf_elems<M, E>() : M;
   // K3 pairs independent transforms with staggered exchanges (fft2s) where a
@@ -58,9 +62,9 @@ struct Sync3<false> {
   __device__ __forceinline__ void operator()() const { asm volatile("bar.sync 0;" ::: "memory"); }
 };
 
-template <int M>
-__device__ __forceinline__ Sync3<Cfg3<M>::NAMED> sync3(int grp) {
-  if constexpr (Cfg3<M>::NAMED) return Sync3<true>{1 + grp, Cfg3<M>::T};
+template <int M, bool H = true>
+__device__ __forceinline__ Sync3<Cfg3<M, H>::NAMED> sync3(int grp) {
+  if constexpr (Cfg3<M, H>::NAMED) return Sync3<true>{1 + grp, Cfg3<M, H>::T};
   else return Sync3<false>{};
 }
 
@@ -226,11 +230,11 @@ k_hconv_rows3(double2* __restrict__ f, double2* __restrict__ g, long nrows, cons
 
 // ====================================================================== K4 ==
 template <int M>
-__global__ void __launch_bounds__(Cfg3<M>::THREADS, Cfg3<M>::MINB)
+__global__ void __launch_bounds__(Cfg3<M, false>::THREADS, Cfg3<M, false>::MINB)
 k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const double2* __restrict__ h, long nrows,
               const double2* __restrict__ twM, const double2* __restrict__ tw4M) {
   pdl_entry();
-  using C = Cfg3<M>;
+  using C = Cfg3<M, false>;
   constexpr int E = C::E, T = C::T, G = C::G;
   extern __shared__ __align__(128) double2 smem[];
   const int grp = threadIdx.x / T, t = threadIdx.x - grp * T;
@@ -238,7 +242,7 @@ k_tconv_rows3(double2* __restrict__ f, const double2* __restrict__ g, const doub
   double2* Gs = F + M;
   double2* xb = Gs + M;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G * C::PER) + grp;
-  const auto sync = sync3<M>(grp);
+  const auto sync = sync3<M, false>(grp);
   const long stride = (long)gridDim.x * G;
   long row = (long)blockIdx.x * G + grp;
   if (t == 0) {
@@ -391,8 +395,8 @@ cudaError_t hconv_rows3(double2* f, double2* g, long nrows, cudaStream_t s, RowS
 
 template <int M>
 cudaError_t tconv_rows3(double2* f, double2* g, double2* h, long nrows, cudaStream_t s) {
-  using C = Cfg3<M>;
-  const double2* twM = pass_table(M, Cfg3<M>::E);
+  using C = Cfg3<M, false>;
+  const double2* twM = pass_table(M, C::E);
   const double2* tw4M = zeta_table(4 * M);
   if (!twM || !tw4M) return cudaErrorMemoryAllocation;
   void* args[] = {&f, &g, &h, &nrows, &twM, &tw4M};
