@@ -24,6 +24,7 @@
 // | IDC_K3_STAGGER_MAX_M    | 512     | K3 runs its transforms as staggered pairs (fft2s, two exchange buffers) |
 // | IDC_K3_STAGE_AS_XB      | 2048    | K3 from this m: first transform pair staggered in the consumed stage    |
 // | IDC_ROWS3_E8_MAX        | 512     | rows3.cu (K3/K4) use E = 8 up to this m, E = 16 above                   |
+// | IDC_K2_G512             | 4       | rows2.cu row groups (64-thread rows) per CTA at m = 512 (K2)            |
 // | IDC_K3_G512 / K4_G512   | 6 / 4   | K3 / K4 row groups (64-thread rows) per CTA at m <= 512                 |
 // | IDC_ROWS3_MINB_SMALL    | 1       | rows3.cu CTAs per SM for m <= 512                                       |
 // | IDC_PENCIL_TMA          | 1       | 2D/3D pencils use the TMA kernels of pencils2.cu for 64 <= m <= 4096    |
@@ -90,6 +91,9 @@
 #endif
 #ifndef IDC_ROWS3_E8_MAX
 #define IDC_ROWS3_E8_MAX 512
+#endif
+#ifndef IDC_K2_G512
+#define IDC_K2_G512 4
 #endif
 #ifndef IDC_K3_G512
 #define IDC_K3_G512 6

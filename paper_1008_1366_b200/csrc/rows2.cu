@@ -465,7 +465,7 @@ template <int M>
 struct Tune {
   static constexpr int E = M < IDC_ROWS_E ? M : (M <= 512 ? 8 : IDC_ROWS_E);
   static constexpr int T = M / E;
-  static constexpr int G = T >= IDC_ROWS_CTA_THREADS ? 1 : IDC_ROWS_CTA_THREADS / T;
+  static constexpr int G = M == 512 ? IDC_K2_G512 : (T >= IDC_ROWS_CTA_THREADS ? 1 : IDC_ROWS_CTA_THREADS / T);
 };
 
 }  // namespace
