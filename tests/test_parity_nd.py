@@ -208,7 +208,7 @@ def test_config5b_hconv3d_512(idc):
 # the oracle's naive-DFT explicitly padded convolution (O2).
 
 @pytest.mark.parametrize("shape", [(64, 64, 64), (128, 64, 64), (64, 128, 32), (512, 8, 8), (8, 512, 8),
-                                   (8, 8, 512), (256, 64, 8)])
+                                   (8, 8, 512), (256, 64, 8), (128, 128, 128)])
 def test_cconv3d_tma_vs_explicit(idc, shape):
     f, g = synthgen.cconv3d_inputs(*shape)
     ref = explicit.cconv3d(f, g)
@@ -218,7 +218,7 @@ def test_cconv3d_tma_vs_explicit(idc, shape):
 
 
 @pytest.mark.parametrize("ms", [(64, 64, 32), (32, 64, 64), (512, 4, 4), (4, 512, 4), (4, 4, 512), (64, 64, 16),
-                                (128, 64, 8)])
+                                (128, 64, 8), (64, 64, 64)])
 def test_hconv3d_tma_vs_explicit(idc, ms):
     f, g = synthgen.hconv3d_inputs(*ms)
     ref = explicit.hconv3d(f, g)
