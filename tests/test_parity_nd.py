@@ -218,7 +218,7 @@ def test_cconv3d_tma_vs_explicit(idc, shape):
 
 
 @pytest.mark.parametrize("ms", [(64, 64, 32), (32, 64, 64), (512, 4, 4), (4, 512, 4), (4, 4, 512), (64, 64, 16),
-                                (128, 64, 8), (64, 64, 64)])
+                                (128, 64, 8), (64, 64, 64), (128, 128, 64), (128, 128, 128)])
 def test_hconv3d_tma_vs_explicit(idc, ms):
     f, g = synthgen.hconv3d_inputs(*ms)
     ref = explicit.hconv3d(f, g)
